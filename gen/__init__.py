@@ -1,0 +1,117 @@
+"""Seeded synthetic input generator (shared by the oracle and the CUDA path).
+
+This module holds none of the method's arithmetic (no sort keys, flags,
+MTTKRP/TTM/CP maths): it draws coordinates, values and dense factor entries
+from a counter-based generator (see tensorgen.c for the recipe) plus the
+paper-shaped workload table used by tests and bench.py.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "tensorgen.c")
+_LIB = os.path.join(_HERE, "libtensorgen.so")
+_lib = None
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        lib = ctypes.CDLL(_LIB)
+        lib.tg_coo.restype = ctypes.c_int
+        lib.tg_coo.argtypes = [ctypes.c_int, ctypes.c_void_p, ctypes.c_int64, ctypes.c_void_p, ctypes.c_uint64,
+                               ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p]
+        lib.tg_uniform_f32.restype = None
+        lib.tg_uniform_f32.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int64, ctypes.c_int64,
+                                       ctypes.c_int, ctypes.c_void_p]
+        lib.tg_hash.restype = ctypes.c_uint64
+        lib.tg_hash.argtypes = [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64]
+        _lib = lib
+    return _lib
+
+
+def coo(dims, nnz: int, alpha=None, seed: int = 1):
+    """Duplicate-free synthetic COO tensor in draw order.
+
+    Returns (idx, val): idx is uint32 (order, nnz) C-contiguous (SoA), val float32 (nnz,).
+    """
+    lib = _load()
+    order = len(dims)
+    d = np.asarray(dims, dtype=np.int64)
+    a = np.asarray(alpha if alpha is not None else [0.0] * order, dtype=np.float64)
+    idx = np.empty((order, nnz), dtype=np.uint32)
+    val = np.empty((nnz,), dtype=np.float32)
+    draws = ctypes.c_int64(0)
+    rc = lib.tg_coo(order, d.ctypes.data, nnz, a.ctypes.data, seed, idx.ctypes.data, val.ctypes.data,
+                    ctypes.byref(draws))
+    if rc != 0:
+        raise ValueError(f"tensorgen.tg_coo failed rc={rc} dims={list(dims)} nnz={nnz}")
+    return idx, val
+
+
+def uniform(shape, seed: int, stream: int = 0, signed: bool = False) -> np.ndarray:
+    """Counter-based uniform fp32 entries in [0,1) (or [-1,1) if signed), 24-bit exact."""
+    lib = _load()
+    out = np.empty(shape, dtype=np.float32)
+    lib.tg_uniform_f32(seed, stream, 0, out.size, 1 if signed else 0, out.ctypes.data)
+    return out
+
+
+def factors(dims, R: int, seed: int, signed: bool = False):
+    """One I_m x R row-major fp32 factor matrix per mode (stream = 1000 + m)."""
+    return [uniform((int(I), R), seed, 1000 + m, signed) for m, I in enumerate(dims)]
+
+
+def hash64(seed: int, stream: int, ctr: int) -> int:
+    return int(_load().tg_hash(seed, stream, ctr))
+
+
+def kruskal_coo(factors_list, lam, coords):
+    """Values of a known Kruskal model sum_r lam_r prod_m U_m(i_m, r) at given coordinates.
+
+    Test-data synthesis for the CP recovery inputs (the model the tensor is drawn
+    from), evaluated in fp64 and rounded once to fp32.  coords: (order, nnz) uint32.
+    """
+    acc = np.zeros((coords.shape[1], len(lam)), dtype=np.float64)
+    acc[:] = np.asarray(lam, dtype=np.float64)[None, :]
+    for m, U in enumerate(factors_list):
+        acc *= np.asarray(U, dtype=np.float64)[coords[m].astype(np.int64)]
+    return acc.sum(axis=1).astype(np.float32)
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    dims: tuple
+    nnz: int
+    alpha: tuple
+    seed: int
+
+
+# SURVEY.md §8(d) table; shapes follow PAPER.md Table IV (L406-419) and BASELINE.json configs.
+WORKLOADS = {
+    "tiny": Workload("tiny", (50, 40, 30), 1000, (0.0, 0.0, 0.0), 101),
+    "nell2": Workload("nell2", (12092, 9184, 28818), 76879419, (0.5, 0.5, 0.5), 102),
+    "netflix": Workload("netflix", (480189, 17770, 2182), 100480507, (0.5, 0.5, 0.2), 103),
+    "brainq": Workload("brainq", (60, 70000, 9), 11000000, (0.0, 0.0, 0.0), 104),
+    "order4": Workload("order4", (500000, 20000, 2000, 1000), 150000000, (0.5, 0.5, 0.5, 0.5), 105),
+}
+
+
+def workload(name: str, nnz: int | None = None):
+    w = WORKLOADS[name]
+    idx, val = coo(w.dims, nnz if nnz is not None else w.nnz, w.alpha, w.seed)
+    return w, idx, val

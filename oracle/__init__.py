@@ -1,0 +1,203 @@
+"""fp64 CPU oracle for the F-COO hot path (arXiv 1705.09905) — TEST INFRASTRUCTURE ONLY.
+
+Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline / --impl reference
+legs may import this package.  It shares no code with paper_1705_09905_b200/ (the
+CUDA product path) and the product path never imports it.  See fcoo_oracle.cpp for
+the passage each function follows and the pins that check it.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "fcoo_oracle.cpp")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lib = None
+
+OK, ERR_ARG, ERR_ORDER, ERR_MODE, ERR_INDEX_RANGE, ERR_DUPLICATE, ERR_EMPTY = range(7)
+OP_MTTKRP, OP_TTM = 0, 1
+
+
+class OracleError(RuntimeError):
+    def __init__(self, code: int, what: str):
+        super().__init__(f"{what}: oracle status {code}")
+        self.code = code
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        subprocess.check_call(["g++", "-O2", "-fopenmp", "-fPIC", "-shared", "-std=c++17", "-o", _LIB, _SRC])
+    return _LIB
+
+
+def _load():
+    global _lib
+    if _lib is None:
+        build()
+        L = ctypes.CDLL(_LIB)
+        vp, i64, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        L.orc_mode_spec.argtypes = [ci, vp, ci, ci, vp, vp, vp, vp]
+        L.orc_storage_bytes.restype = i64
+        L.orc_storage_bytes.argtypes = [i64, ci, i64]
+        L.orc_build.argtypes = [ci, vp, i64, vp, vp, ci, ci, i64, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_mttkrp.argtypes = [ci, vp, i64, vp, vp, ci, vp, ci, vp, vp, ci]
+        L.orc_ttm.argtypes = [ci, vp, i64, vp, vp, ci, vp, ci, vp, vp, vp, vp]
+        L.orc_gram.argtypes = [i64, ci, vp, vp]
+        L.orc_pinv_sym.argtypes = [ci, vp, vp]
+        L.orc_normalize.argtypes = [i64, ci, vp, vp]
+        L.orc_cp_als.argtypes = [ci, vp, i64, vp, vp, ci, ci, ctypes.c_double, vp, vp, vp, vp]
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray):
+    return a.ctypes.data
+
+
+def _coo(dims, idx, val):
+    d = np.ascontiguousarray(dims, dtype=np.int64)
+    idx = np.ascontiguousarray(idx, dtype=np.uint32)
+    val = np.ascontiguousarray(val, dtype=np.float32)
+    assert idx.ndim == 2 and idx.shape[0] == len(d) and idx.shape[1] == val.shape[0]
+    return d, idx, val
+
+
+def mode_spec(dims, op: int, mode: int):
+    L = _load()
+    d = np.ascontiguousarray(dims, dtype=np.int64)
+    im, pm = np.zeros(8, np.int32), np.zeros(8, np.int32)
+    ni, npr = ctypes.c_int(0), ctypes.c_int(0)
+    rc = L.orc_mode_spec(len(d), _ptr(d), op, mode, _ptr(im), ctypes.byref(ni), _ptr(pm), ctypes.byref(npr))
+    if rc:
+        raise OracleError(rc, "mode_spec")
+    return list(im[: ni.value]), list(pm[: npr.value])
+
+
+def storage_bytes(nnz: int, n_prod: int, T: int) -> int:
+    return int(_load().orc_storage_bytes(nnz, n_prod, T))
+
+
+@dataclass
+class Fcoo:
+    """Oracle F-COO build result (numpy arrays, exact bytes)."""
+    index_modes: list
+    product_modes: list
+    perm: np.ndarray        # u32[nnz]
+    bf: np.ndarray          # u8[ceil(nnz/8)]
+    sf: np.ndarray          # u32[ceil(ntiles/32)]
+    seg_base: np.ndarray    # u32[ntiles]
+    seg_coord: np.ndarray   # u32[nsegs, n_idx]
+    pidx: np.ndarray        # u32[n_prod, nnz]
+    val: np.ndarray         # f32[nnz]
+    nsegs: int
+    T: int
+
+    def bf_bits(self) -> np.ndarray:
+        return np.unpackbits(self.bf, bitorder="little")[: self.val.shape[0]]
+
+
+def build_fcoo(dims, idx, val, op: int, mode: int, T: int) -> Fcoo:
+    L = _load()
+    d, idx, val = _coo(dims, idx, val)
+    nnz = val.shape[0]
+    order = len(d)
+    if order < 2 or order > 8:
+        raise OracleError(ERR_ORDER, "build")
+    im, pm = mode_spec(d, op, mode)
+    ntiles = max(1, (nnz + T - 1) // T)
+    perm = np.zeros(nnz, np.uint32)
+    bf = np.zeros(max(1, (nnz + 7) // 8), np.uint8)
+    sf = np.zeros(max(1, (ntiles + 31) // 32), np.uint32)
+    seg_base = np.zeros(ntiles, np.uint32)
+    seg_coord = np.zeros((max(1, nnz), len(im)), np.uint32)
+    pidx = np.zeros((len(pm), nnz), np.uint32)
+    pval = np.zeros(nnz, np.float32)
+    ns = ctypes.c_int64(0)
+    rc = L.orc_build(order, _ptr(d), nnz, _ptr(idx), _ptr(val), op, mode, T, _ptr(perm), _ptr(bf), _ptr(sf),
+                     _ptr(seg_base), _ptr(seg_coord), _ptr(pidx), _ptr(pval), ctypes.byref(ns))
+    if rc:
+        raise OracleError(rc, "build")
+    nsegs = ns.value
+    return Fcoo(im, pm, perm, bf[: (nnz + 7) // 8], sf[: (((nnz + T - 1) // T) + 31) // 32],
+                seg_base[: (nnz + T - 1) // T], seg_coord[:nsegs].copy(), pidx, pval, nsegs, T)
+
+
+def mttkrp(dims, idx, val, mode: int, factors, R: int | None = None, with_D: bool = True, nthreads: int = 1):
+    """Returns (M, D) fp64 I_mode x R (D None if with_D False)."""
+    L = _load()
+    d, idx, val = _coo(dims, idx, val)
+    fs = [np.ascontiguousarray(f, dtype=np.float32) for f in factors]
+    R = fs[(mode + 1) % len(d)].shape[1] if R is None else R
+    ptrs = (ctypes.c_void_p * len(d))(*[_ptr(f) for f in fs])
+    M = np.zeros((int(d[mode]), R), np.float64)
+    D = np.zeros_like(M) if with_D else None
+    rc = L.orc_mttkrp(len(d), _ptr(d), val.shape[0], _ptr(idx), _ptr(val), mode, ptrs, R, _ptr(M),
+                      _ptr(D) if with_D else None, nthreads)
+    if rc:
+        raise OracleError(rc, "mttkrp")
+    return M, D
+
+
+def ttm(dims, idx, val, mode: int, U):
+    """Returns (coords u32[nfib, order-1], Y fp64[nfib, R], D fp64[nfib, R])."""
+    L = _load()
+    d, idx, val = _coo(dims, idx, val)
+    U = np.ascontiguousarray(U, dtype=np.float32)
+    R = U.shape[1]
+    nnz = val.shape[0]
+    cap = max(1, nnz)
+    coords = np.zeros((cap, len(d) - 1), np.uint32)
+    Y = np.zeros((cap, R), np.float64)
+    D = np.zeros((cap, R), np.float64)
+    nf = ctypes.c_int64(0)
+    rc = L.orc_ttm(len(d), _ptr(d), nnz, _ptr(idx), _ptr(val), mode, _ptr(U), R, ctypes.byref(nf), _ptr(coords),
+                   _ptr(Y), _ptr(D))
+    if rc:
+        raise OracleError(rc, "ttm")
+    n = nf.value
+    return coords[:n].copy(), Y[:n].copy(), D[:n].copy()
+
+
+def gram(A):
+    A = np.ascontiguousarray(A, dtype=np.float64)
+    G = np.zeros((A.shape[1], A.shape[1]), np.float64)
+    _load().orc_gram(A.shape[0], A.shape[1], _ptr(A), _ptr(G))
+    return G
+
+
+def pinv_sym(G):
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    P = np.zeros_like(G)
+    rc = _load().orc_pinv_sym(G.shape[0], _ptr(G), _ptr(P))
+    if rc < 0:
+        raise OracleError(ERR_ARG, "pinv_sym (not symmetric)")
+    return P
+
+
+def normalize(A):
+    A = np.array(A, dtype=np.float64, order="C")
+    lam = np.zeros(A.shape[1], np.float64)
+    _load().orc_normalize(A.shape[0], A.shape[1], _ptr(A), _ptr(lam))
+    return A, lam
+
+
+def cp_als(dims, idx, val, R: int, iters: int, init, tol: float = 0.0):
+    """Returns (factors fp64 list, lambda fp64[R], fit_trace fp64[iters_done])."""
+    L = _load()
+    d, idx, val = _coo(dims, idx, val)
+    ins = [np.ascontiguousarray(f, dtype=np.float32) for f in init]
+    outs = [np.zeros((int(I), R), np.float64) for I in d]
+    ip = (ctypes.c_void_p * len(d))(*[_ptr(f) for f in ins])
+    op = (ctypes.c_void_p * len(d))(*[_ptr(f) for f in outs])
+    lam = np.zeros(R, np.float64)
+    trace = np.zeros(iters, np.float64)
+    n = L.orc_cp_als(len(d), _ptr(d), val.shape[0], _ptr(idx), _ptr(val), R, iters, tol, ip, op, _ptr(lam),
+                     _ptr(trace))
+    if n < 0:
+        raise OracleError(-n, "cp_als")
+    return outs, lam, trace[:n].copy()
