@@ -1,0 +1,216 @@
+/*
+ * fcoo.h — C ABI of libfcoo, a B200-native (sm_100a) implementation of the F-COO hot path of
+ * Liu, Wen, Sarwate, Dehnavi, "A Unified Optimization Approach for Sparse Tensor Operations on
+ * GPUs" (arXiv 1705.09905).  Citations: P:Lnnn = /root/reference/PAPER.md line (section / eq.).
+ *
+ * Conventions
+ *   - Modes are 0-based (the paper is 1-based).  Rank R is the number of factor columns.
+ *   - "device" = a CUDA device pointer on the current device; "host" = host memory.
+ *   - Every call that launches work enqueues it on `stream` (a cudaStream_t passed as void*;
+ *     NULL = legacy default stream) and returns without synchronising, except where stated.
+ *   - Outputs are overwritten, never accumulated.  Rows of an MTTKRP output with no nonzeros
+ *     are exactly 0.
+ *   - Errors are returned as fcoo_status; nothing is thrown across the ABI and nothing exits.
+ *     Host-checkable errors return before any launch.  fcoo_last_error() gives a
+ *     thread-local detail string for the last failure.
+ *   - Floating point: fp32 storage and fp32 accumulation (the paper's single precision,
+ *     P:L272 Table II caption); the CP-ALS R x R algebra is done in fp64.
+ */
+#ifndef FCOO_H
+#define FCOO_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes.  The numeric values 0..6 coincide with the oracle's own enum (oracle/). */
+typedef enum {
+  FCOO_OK = 0,
+  FCOO_ERR_ARG = 1,         /* NULL pointer, bad size, bad option */
+  FCOO_ERR_ORDER = 2,       /* order outside [2, 8] */
+  FCOO_ERR_MODE = 3,        /* mode >= order */
+  FCOO_ERR_INDEX_RANGE = 4, /* some idx[m][q] >= dims[m] (detected on device) */
+  FCOO_ERR_DUPLICATE = 5,   /* two nonzeros share all coordinates (detected on device) */
+  FCOO_ERR_EMPTY = 6,       /* nnz == 0 */
+  FCOO_ERR_KEY_BITS = 7,    /* sum_m ceil(log2 dims[m]) > 64: sort key does not fit */
+  FCOO_ERR_RANK = 8,        /* R outside [1, 256] */
+  FCOO_ERR_SHAPE = 9,       /* op/handle mismatch (e.g. fcoo_ttm on an MTTKRP handle) */
+  FCOO_ERR_ALIGN = 10,      /* reserved */
+  FCOO_ERR_OOM = 11,        /* device allocation failed */
+  FCOO_ERR_CUDA = 12,       /* CUDA launch / runtime error */
+  FCOO_ERR_NCCL = 13,       /* NCCL error */
+  FCOO_ERR_NOT_FINITE = 14  /* reserved */
+} fcoo_status;
+
+/* Operation a handle is built for: Table I.
+ *   FCOO_OP_MTTKRP on mode n: index mode {n}; product modes = all others (Eq.(6)).
+ *   FCOO_OP_TTM    on mode n: product mode {n}; index modes = all others (Eq.(3)). */
+typedef enum { FCOO_OP_MTTKRP = 0, FCOO_OP_TTM = 1 } fcoo_op;
+
+/* COO input.  Borrowed: must stay valid until the stream work of the call
+ * that reads it completes.  Coordinates are 0-based; duplicates are an error (reading Q6). */
+typedef struct {
+  int order;                   /* N, 2..8 */
+  const int64_t* dims;         /* host [order]; 1 <= dims[m] < 2^32 */
+  int64_t nnz;                 /* >= 1, < 2^32 */
+  const uint32_t* const* idx;  /* host array of `order` DEVICE pointers, idx[m][q] (SoA) */
+  const float* val;            /* device [nnz] */
+} fcoo_coo;
+
+/* Optional device allocator (the Python binding passes torch's caching allocator).
+ * NULL -> cudaMallocAsync / cudaFreeAsync on the call's stream. */
+typedef struct {
+  void* (*alloc)(size_t bytes, void* stream, void* ctx);
+  void (*free)(void* ptr, size_t bytes, void* stream, void* ctx);
+  void* ctx;
+} fcoo_allocator;
+
+#define FCOO_BUILD_KEEP_PERM 1u /* keep the sorted->input permutation for fcoo_export */
+
+/* Build options.  NULL -> {FCOO_OP_MTTKRP, 256, 0}.
+ * tile_nnz = T, the partition length ("threadlen", P:L272 / P:L426): a multiple of 32 in
+ * [32, 8192].  sf has one bit per tile; one GPU lane-group processes one tile. */
+typedef struct {
+  int op;          /* fcoo_op */
+  int tile_nnz;    /* T */
+  unsigned flags;  /* FCOO_BUILD_* */
+} fcoo_build_opts;
+
+typedef struct fcoo_s* fcoo_t;
+typedef struct fcoo_comm_s* fcoo_comm_t;
+
+/*
+ * fcoo_build — F-COO format for (op, mode) (§IV-B, Fig. 2; Table II).
+ * Sorts the nonzeros on the device with the index modes as major key (ascending mode order)
+ * and the product modes as minor keys in ascending extent order (reading Q5), then writes:
+ *   product-mode index arrays and values in sorted order ("only keeps the indices on the
+ *   product mode"), bf (1 bit per nonzero, 1 = first nonzero of a new index tuple, i.e. a new
+ *   slice/fibre; reading Q1), sf (1 bit per tile: sf[t] = bf[t*T]; reading Q3), and
+ *   the segment tables seg_base[t] (heads before tile t) and seg_coord[s] (index tuple of
+ *   segment s) which the paper leaves implicit (reading Q4).
+ * Inputs are device arrays (see fcoo_coo).  Performs ONE host synchronisation on `stream` to
+ * report data errors (INDEX_RANGE, DUPLICATE) and to size the segment table; on success *out
+ * owns all its device memory (allocated through `alloc`) until fcoo_destroy.  The result is a
+ * pure function of the input (bit-exact against the oracle build).
+ */
+fcoo_status fcoo_build(const fcoo_coo* coo, int mode, const fcoo_build_opts* opts, const fcoo_allocator* alloc,
+                       void* stream, fcoo_t* out);
+
+/*
+ * fcoo_mttkrp — SpMTTKRP on the handle's mode n, one-shot (§IV-C, Eq.(6)):
+ *   out(i_n, :) = sum_{nonzeros q of slice i_n} v_q * Hadamard_{m != n} factors[m](i_m(q), :)
+ * as a flag-driven segmented reduction: each lane-group walks one tile of T
+ * nonzeros, gathers the product-mode factor rows (fp32 row-major I_m x R, 16-B aligned rows on
+ * the vector path when R % 4 == 0), accumulates in registers, stores segments it owns and uses
+ * red.global.add only for the (at most two) segments it shares with a neighbouring tile.
+ *   factors: host array of `order` DEVICE pointers; factors[n] is ignored (may be NULL).
+ *   R: 1..256.  out: device, I_n x R fp32 row-major, overwritten.
+ * On a sharded handle (fcoo_set_shard) only the shard's tiles are processed; with a comm the
+ * partial outputs are summed by an NCCL all-reduce so every rank holds the full result.
+ * Errors: SHAPE (handle built for TTM), RANK, ARG, CUDA, NCCL.  Asynchronous.
+ */
+fcoo_status fcoo_mttkrp(fcoo_t f, const float* const* factors, int R, float* out, void* stream);
+
+/*
+ * fcoo_ttm — SpTTM on the handle's mode n (Eq.(3); Table I row 1):
+ *   out(s, :) = sum_{nonzeros q of fibre s} v_q * U(i_n(q), :)
+ * on the same segmented-reduction engine.  Output is semi-sparse: one dense R-row
+ * per non-empty fibre s (segment ordinal, in lexicographic order of the index tuple); the
+ * fibre coordinates are the seg_coord table (fcoo_export).
+ *   U: device, I_n x R fp32 row-major.  out: device, nsegs x R fp32, overwritten.
+ * Errors: SHAPE (handle built for MTTKRP), RANK, ARG, CUDA, NCCL.  Asynchronous.
+ */
+fcoo_status fcoo_ttm(fcoo_t f, const float* U, int R, float* out, void* stream);
+
+typedef struct {
+  int order, op, mode;
+  int n_idx, n_prod;
+  int idx_modes[8], prod_modes[8]; /* prod_modes in stored (ascending extent) order */
+  int64_t dims[8];
+  int64_t nnz, nsegs, ntiles, tile_nnz;
+  int dense_rows;          /* MTTKRP with every slice non-empty: seg_coord is the identity */
+  int64_t storage_bytes;   /* Table II core bytes: (4*n_prod+4)*nnz + ceil(nnz/8) + 4*ceil(ntiles/32) */
+  int64_t seg_table_bytes; /* seg_base + seg_coord bytes (reading Q4) */
+  int64_t device_bytes;    /* everything the handle holds on the device (with padding) */
+  int shard, nshards;      /* tile range in use: [tile_begin, tile_end) */
+  int64_t tile_begin, tile_end;
+} fcoo_info_t;
+
+/* fcoo_info — host-side metadata; no device work. */
+fcoo_status fcoo_info(fcoo_t f, fcoo_info_t* info);
+
+/* Host view for fcoo_export: each non-NULL pointer receives a copy (host memory, caller-owned).
+ * Sizes: perm u32[nnz] (only with FCOO_BUILD_KEEP_PERM), bf u8[ceil(nnz/8)] (LSB-first, pad 0),
+ * sf u32[ceil(ntiles/32)], seg_base u32[ntiles], seg_coord u32[nsegs*n_idx],
+ * pidx u32[n_prod*nnz] (product modes in prod_modes order), val f32[nnz]. */
+typedef struct {
+  uint32_t* perm;
+  uint8_t* bf;
+  uint32_t* sf;
+  uint32_t* seg_base;
+  uint32_t* seg_coord;
+  uint32_t* pidx;
+  float* val;
+} fcoo_host_view;
+
+/* fcoo_export — copy the handle's arrays to host buffers; synchronises `stream`. */
+fcoo_status fcoo_export(fcoo_t f, fcoo_host_view* view, void* stream);
+
+/* fcoo_destroy — free the handle (stream-ordered frees on the build stream). NULL is OK. */
+fcoo_status fcoo_destroy(fcoo_t f);
+
+/* ---- multi-GPU ("multiple-GPUs can be used") ----
+ * One process per GPU.  Rank 0 calls fcoo_comm_unique_id and broadcasts the 128 bytes (the
+ * Python binding uses torch.distributed); every rank calls fcoo_comm_init on its device. */
+fcoo_status fcoo_comm_unique_id(void* out128);
+fcoo_status fcoo_comm_init(int rank, int nranks, const void* uid128, fcoo_comm_t* out);
+fcoo_status fcoo_comm_destroy(fcoo_comm_t comm);
+/* In-place sum all-reduce of `count` fp32 values on `stream` (NCCL over NVLink/NVSwitch). */
+fcoo_status fcoo_allreduce_sum(fcoo_comm_t comm, float* buf, size_t count, void* stream);
+
+/* fcoo_set_shard — restrict the handle to the tiles of shard `shard` of `nshards`: the
+ * tile-aligned nnz range [floor(shard*ntiles/nshards), floor((shard+1)*ntiles/nshards)).
+ * comm (may be NULL) is used by fcoo_mttkrp / fcoo_ttm to all-reduce the partial outputs.
+ * nshards == 1 restores the whole handle. */
+fcoo_status fcoo_set_shard(fcoo_t f, int shard, int nshards, fcoo_comm_t comm);
+
+/* ---- CP-ALS (Algorithm 1, generalised to order N) ----
+ * Per iteration, for n = 0..N-1: M = MTTKRP_n (fcoo_mttkrp, one F-COO handle per mode built up
+ * front); V = Hadamard_{m != n} U_m^T U_m (fp64); U_n = M V^{-1} (fp64 Cholesky, with a
+ * Jacobi pseudo-inverse fallback when V is not positive definite, reading Q14); lambda =
+ * column 2-norms of U_n; U_n normalised (reading Q13).  After the last mode:
+ *   fit = 1 - sqrt(max(0, |X|^2 + |Xhat|^2 - 2 <X, Xhat>)) / |X|,
+ *   <X, Xhat> = sum_r lambda_r sum_i M(i,r) U_N(i,r),  |Xhat|^2 = lambda^T (Hadamard_m G_m) lambda.
+ * Stops early when tol > 0 and |fit - fit_prev| < tol ("no improvement").
+ * With comm != NULL every rank builds all modes, processes its shard of every mode, and
+ * all-reduces M; the R x R work is replicated, so the factors stay identical on all ranks. */
+typedef struct {
+  int R;            /* 1..256 */
+  int iters;        /* >= 1 */
+  double tol;       /* 0 = run all iterations */
+  int tile_nnz;     /* 0 -> 256 */
+  fcoo_comm_t comm; /* NULL = single GPU */
+  int rank, nranks; /* shard of this process (ignored when comm == NULL) */
+} fcoo_cp_opts;
+
+/*
+ * cp_als — factors: host array of `order` DEVICE pointers to I_m x R fp32 buffers holding the
+ * initial factors on entry (caller-seeded) and the unit-column factors on exit.
+ * lambda: device [R] fp32 (out).  fit_trace: host [iters] (out).  iters_done: host (out).
+ * Synchronises `stream` once per iteration (to read the fit for `tol`).
+ */
+fcoo_status cp_als(const fcoo_coo* tensor, const fcoo_cp_opts* opts, float* const* factors, float* lambda,
+                   double* fit_trace, int* iters_done, const fcoo_allocator* alloc, void* stream);
+
+const char* fcoo_status_str(fcoo_status s);
+const char* fcoo_last_error(void);
+/* Number of kernel launches this library enqueued so far in this process (for bench.py). */
+uint64_t fcoo_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FCOO_H */

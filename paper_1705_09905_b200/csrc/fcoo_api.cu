@@ -1,0 +1,156 @@
+// fcoo_api.cu — the C ABI surface of libfcoo (include/fcoo.h): argument validation, status
+// strings, allocator plumbing, handle metadata/export, sharding.
+#include <stdarg.h>
+#include <string.h>
+
+#include <algorithm>
+
+#include "fcoo_internal.cuh"
+
+namespace fcoo {
+
+std::atomic<uint64_t> g_launches{0};
+static thread_local char t_err[512] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(t_err, sizeof(t_err), fmt, ap);
+  va_end(ap);
+}
+
+fcoo_status fail(fcoo_status s, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(t_err, sizeof(t_err), fmt, ap);
+  va_end(ap);
+  return s;
+}
+
+void* Alloc::get(size_t bytes, cudaStream_t s) const {
+  if (bytes == 0) return nullptr;
+  if (custom) return a.alloc(bytes, (void*)s, a.ctx);
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, s) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+
+void Alloc::put(void* p, size_t bytes, cudaStream_t s) const {
+  if (!p) return;
+  if (custom) a.free(p, bytes, (void*)s, a.ctx);
+  else cudaFreeAsync(p, s);
+}
+
+fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opts, const fcoo_allocator* alloc,
+                       cudaStream_t s, fcoo_t* out);
+void destroy_impl(fcoo_s* f);
+
+}  // namespace fcoo
+
+extern "C" {
+
+const char* fcoo_status_str(fcoo_status s) {
+  switch (s) {
+    case FCOO_OK: return "FCOO_OK";
+    case FCOO_ERR_ARG: return "FCOO_ERR_ARG";
+    case FCOO_ERR_ORDER: return "FCOO_ERR_ORDER";
+    case FCOO_ERR_MODE: return "FCOO_ERR_MODE";
+    case FCOO_ERR_INDEX_RANGE: return "FCOO_ERR_INDEX_RANGE";
+    case FCOO_ERR_DUPLICATE: return "FCOO_ERR_DUPLICATE";
+    case FCOO_ERR_EMPTY: return "FCOO_ERR_EMPTY";
+    case FCOO_ERR_KEY_BITS: return "FCOO_ERR_KEY_BITS";
+    case FCOO_ERR_RANK: return "FCOO_ERR_RANK";
+    case FCOO_ERR_SHAPE: return "FCOO_ERR_SHAPE";
+    case FCOO_ERR_ALIGN: return "FCOO_ERR_ALIGN";
+    case FCOO_ERR_OOM: return "FCOO_ERR_OOM";
+    case FCOO_ERR_CUDA: return "FCOO_ERR_CUDA";
+    case FCOO_ERR_NCCL: return "FCOO_ERR_NCCL";
+    case FCOO_ERR_NOT_FINITE: return "FCOO_ERR_NOT_FINITE";
+  }
+  return "FCOO_ERR_UNKNOWN";
+}
+
+const char* fcoo_last_error(void) { return fcoo::t_err; }
+
+uint64_t fcoo_launch_count(void) { return fcoo::g_launches.load(); }
+
+fcoo_status fcoo_build(const fcoo_coo* coo, int mode, const fcoo_build_opts* opts, const fcoo_allocator* alloc,
+                       void* stream, fcoo_t* out) {
+  return fcoo::build_impl(coo, mode, opts, alloc, (cudaStream_t)stream, out);
+}
+
+fcoo_status fcoo_mttkrp(fcoo_t f, const float* const* factors, int R, float* out, void* stream) {
+  if (!f || !factors || !out) return fcoo::fail(FCOO_ERR_ARG, "NULL handle/factors/out");
+  if (f->op != FCOO_OP_MTTKRP) return fcoo::fail(FCOO_ERR_SHAPE, "handle was built for SpTTM");
+  if (R < 1 || R > 256) return fcoo::fail(FCOO_ERR_RANK, "R=%d outside [1,256]", R);
+  return fcoo::run_mttkrp(f, factors, R, out, (cudaStream_t)stream);
+}
+
+fcoo_status fcoo_ttm(fcoo_t f, const float* U, int R, float* out, void* stream) {
+  if (!f || !U || !out) return fcoo::fail(FCOO_ERR_ARG, "NULL handle/U/out");
+  if (f->op != FCOO_OP_TTM) return fcoo::fail(FCOO_ERR_SHAPE, "handle was built for SpMTTKRP");
+  if (R < 1 || R > 256) return fcoo::fail(FCOO_ERR_RANK, "R=%d outside [1,256]", R);
+  return fcoo::run_ttm(f, U, R, out, (cudaStream_t)stream);
+}
+
+fcoo_status fcoo_info(fcoo_t f, fcoo_info_t* info) {
+  if (!f || !info) return fcoo::fail(FCOO_ERR_ARG, "NULL handle/info");
+  memset(info, 0, sizeof(*info));
+  info->order = f->order; info->op = f->op; info->mode = f->mode;
+  info->n_idx = f->n_idx; info->n_prod = f->n_prod;
+  for (int m = 0; m < fcoo::kMaxOrder; ++m) {
+    info->idx_modes[m] = f->idx_modes[m];
+    info->prod_modes[m] = f->prod_modes[m];
+    info->dims[m] = f->dims[m];
+  }
+  info->nnz = f->nnz; info->nsegs = f->nsegs; info->ntiles = f->ntiles; info->tile_nnz = f->T;
+  info->dense_rows = f->dense_rows;
+  info->storage_bytes = (4 * (int64_t)f->n_prod + 4) * f->nnz + (f->nnz + 7) / 8 + 4 * ((f->ntiles + 31) / 32);
+  info->seg_table_bytes = 4 * (f->ntiles + 1) + 4 * f->nsegs * f->n_idx;
+  info->device_bytes = (int64_t)(f->bytes_pidx + f->bytes_val + f->bytes_bf + f->bytes_sf + f->bytes_seg_base +
+                                 f->bytes_seg_coord + f->bytes_perm);
+  info->shard = f->shard; info->nshards = f->nshards;
+  info->tile_begin = f->tile_begin; info->tile_end = f->tile_end;
+  return FCOO_OK;
+}
+
+fcoo_status fcoo_export(fcoo_t f, fcoo_host_view* v, void* stream) {
+  if (!f || !v) return fcoo::fail(FCOO_ERR_ARG, "NULL handle/view");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int64_t nnz = f->nnz;
+  if (v->perm) {
+    if (!f->perm) return fcoo::fail(FCOO_ERR_ARG, "perm requested but the handle was built without KEEP_PERM");
+    FCOO_CUDA_TRY(cudaMemcpyAsync(v->perm, f->perm, 4 * nnz, cudaMemcpyDeviceToHost, s));
+  }
+  if (v->bf) FCOO_CUDA_TRY(cudaMemcpyAsync(v->bf, f->bf, (nnz + 7) / 8, cudaMemcpyDeviceToHost, s));
+  if (v->sf) FCOO_CUDA_TRY(cudaMemcpyAsync(v->sf, f->sf, 4 * ((f->ntiles + 31) / 32), cudaMemcpyDeviceToHost, s));
+  if (v->seg_base) FCOO_CUDA_TRY(cudaMemcpyAsync(v->seg_base, f->seg_base, 4 * f->ntiles, cudaMemcpyDeviceToHost, s));
+  if (v->seg_coord && f->nsegs > 0)
+    FCOO_CUDA_TRY(cudaMemcpyAsync(v->seg_coord, f->seg_coord, 4 * f->nsegs * f->n_idx, cudaMemcpyDeviceToHost, s));
+  if (v->pidx)
+    for (int a = 0; a < f->n_prod; ++a)
+      FCOO_CUDA_TRY(cudaMemcpyAsync(v->pidx + a * nnz, f->pidx + a * f->nnz_pad, 4 * nnz, cudaMemcpyDeviceToHost, s));
+  if (v->val) FCOO_CUDA_TRY(cudaMemcpyAsync(v->val, f->val, 4 * nnz, cudaMemcpyDeviceToHost, s));
+  FCOO_CUDA_TRY(cudaStreamSynchronize(s));
+  return FCOO_OK;
+}
+
+fcoo_status fcoo_destroy(fcoo_t f) {
+  fcoo::destroy_impl(f);
+  return FCOO_OK;
+}
+
+fcoo_status fcoo_set_shard(fcoo_t f, int shard, int nshards, fcoo_comm_t comm) {
+  if (!f || nshards < 1 || shard < 0 || shard >= nshards) return fcoo::fail(FCOO_ERR_ARG, "bad shard %d/%d", shard, nshards);
+  f->shard = shard;
+  f->nshards = nshards;
+  f->tile_begin = f->ntiles * shard / nshards;
+  f->tile_end = f->ntiles * (shard + 1) / nshards;
+  f->comm = nshards > 1 ? comm : nullptr;
+  return FCOO_OK;
+}
+
+}  // extern "C"

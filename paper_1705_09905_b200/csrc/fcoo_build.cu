@@ -1,0 +1,323 @@
+// fcoo_build.cu — F-COO construction on the device (§IV-B, Fig. 2, Table II).
+//
+// Pipeline:
+//   k_pack_keys   validate coordinates, pack one u64 sort key per nonzero:
+//                 index modes (ascending mode id) most significant, then the product modes in
+//                 ascending-extent order (reading Q5); ord = input ordinal
+//   CUB onesweep radix sort of (key, ord) over the key bits actually used (stable)
+//   k_flags       bf word per 32 nonzeros by warp ballot (head = index bits differ from the
+//                 previous key; reading Q1), duplicate detection (Q6), unpack product
+//                 indices from the key, gather values by ord, per-word head counts
+//   CUB exclusive scan of the word counts -> word_base (heads before word w)
+//   k_tiles       sf[t] = bf[t*T] by ballot (Q3), seg_base[t] = word_base[t*T/32]
+//   one host sync: error flags + nsegs
+//   k_seg_coord   seg_coord[s] = index tuple of the s-th head (reading Q4)
+#include <cub/cub.cuh>
+#include <stdarg.h>
+
+#include "fcoo_internal.cuh"
+
+namespace fcoo {
+
+namespace {
+
+enum : uint32_t { ERRF_INDEX_RANGE = 1u, ERRF_DUPLICATE = 2u };
+
+struct KeyLayout {
+  int order;
+  int key_modes[kMaxOrder];   // key position a -> tensor mode
+  int shift[kMaxOrder];       // bit offset of key position a
+  uint32_t dims[kMaxOrder];   // extent of key position a (for validation), 0 = 2^32
+  uint64_t mask[kMaxOrder];
+  int n_idx;
+  int prod_bits;              // bits below the index part
+};
+
+struct IdxPtrs {
+  const uint32_t* p[kMaxOrder];
+};
+
+__global__ void k_pack_keys(IdxPtrs idx, KeyLayout L, int64_t nnz, uint64_t* __restrict__ keys,
+                            uint32_t* __restrict__ ord, uint32_t* __restrict__ err) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nnz) return;
+  uint64_t key = 0;
+  bool bad = false;
+#pragma unroll
+  for (int a = 0; a < kMaxOrder; ++a) {
+    if (a < L.order) {
+      uint32_t c = idx.p[a][q];
+      bad |= (L.dims[a] != 0u && c >= L.dims[a]);
+      key |= ((uint64_t)c & L.mask[a]) << L.shift[a];
+    }
+  }
+  if (bad) atomicOr(err, ERRF_INDEX_RANGE);
+  keys[q] = key;
+  ord[q] = (uint32_t)q;
+}
+
+__device__ __forceinline__ uint64_t index_part(uint64_t key, int prod_bits) {
+  return prod_bits >= 64 ? 0ull : (key >> prod_bits);
+}
+
+// One thread per (padded) position p; nnz_pad is a multiple of 32 so warps are whole words.
+__global__ void k_flags(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ord,
+                        const float* __restrict__ val_in, KeyLayout L, int n_prod, int64_t nnz, int64_t nnz_pad,
+                        uint32_t* __restrict__ pidx, float* __restrict__ val, uint32_t* __restrict__ bf,
+                        uint32_t* __restrict__ wcount, uint32_t* __restrict__ perm, uint32_t* __restrict__ err) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nnz_pad) return;  // nnz_pad % 32 == 0 and blockDim % 32 == 0: whole warps exit together
+  bool live = p < nnz;
+  bool head = false;
+  if (live) {
+    uint64_t key = keys[p];
+    if (p == 0) {
+      head = true;
+    } else {
+      uint64_t prev = keys[p - 1];
+      head = index_part(key, L.prod_bits) != index_part(prev, L.prod_bits);
+      if (key == prev) atomicOr(err, ERRF_DUPLICATE);
+    }
+    for (int a = 0; a < n_prod; ++a) {
+      int ka = L.n_idx + a;
+      pidx[(int64_t)a * nnz_pad + p] = (uint32_t)((key >> L.shift[ka]) & L.mask[ka]);
+    }
+    uint32_t o = ord[p];
+    val[p] = val_in[o];
+    if (perm) perm[p] = o;
+  } else {
+    for (int a = 0; a < n_prod; ++a) pidx[(int64_t)a * nnz_pad + p] = 0u;
+    val[p] = 0.0f;
+  }
+  uint32_t word = __ballot_sync(0xffffffffu, head);
+  if ((threadIdx.x & 31) == 0) {
+    bf[p >> 5] = word;
+    wcount[p >> 5] = __popc(word);
+  }
+}
+
+// One thread per tile: sf bit (ballot over 32 tiles) and seg_base.
+__global__ void k_tiles(const uint32_t* __restrict__ bf, const uint32_t* __restrict__ wbase, int64_t ntiles,
+                        int64_t words_per_tile, int64_t nwords, uint32_t* __restrict__ sf,
+                        uint32_t* __restrict__ seg_base) {
+  int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  bool bit = false;
+  if (t < ntiles) {
+    int64_t w = t * words_per_tile;
+    bit = bf[w] & 1u;
+    seg_base[t] = wbase[w];
+  }
+  if (t == ntiles) seg_base[t] = wbase[nwords];
+  uint32_t word = __ballot_sync(0xffffffffu, bit);
+  if ((threadIdx.x & 31) == 0 && (t >> 5) <= (ntiles - 1) >> 5) sf[t >> 5] = word;
+}
+
+__global__ void k_seg_coord(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ bf,
+                            const uint32_t* __restrict__ wbase, KeyLayout L, int64_t nnz,
+                            uint32_t* __restrict__ seg_coord) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nnz) return;
+  uint32_t word = bf[p >> 5];
+  int b = (int)(p & 31);
+  if (!((word >> b) & 1u)) return;
+  uint32_t s = wbase[p >> 5] + __popc(word & ((1u << b) - 1u));
+  uint64_t key = keys[p];
+  for (int a = 0; a < L.n_idx; ++a) seg_coord[(int64_t)s * L.n_idx + a] = (uint32_t)((key >> L.shift[a]) & L.mask[a]);
+}
+
+int bits_for(int64_t n) {
+  int b = 0;
+  while (b < 63 && ((int64_t)1 << b) < n) ++b;
+  return b;
+}
+
+template <class T>
+T* grab(fcoo_s* f, size_t bytes, cudaStream_t s, size_t* rec) {
+  *rec = bytes;
+  return reinterpret_cast<T*>(f->alloc.get(bytes, s));
+}
+
+void free_handle_arrays(fcoo_s* f) {
+  cudaStream_t s = f->build_stream;
+  if (f->pidx) f->alloc.put(f->pidx, f->bytes_pidx, s);
+  if (f->val) f->alloc.put(f->val, f->bytes_val, s);
+  if (f->bf) f->alloc.put(f->bf, f->bytes_bf, s);
+  if (f->sf) f->alloc.put(f->sf, f->bytes_sf, s);
+  if (f->seg_base) f->alloc.put(f->seg_base, f->bytes_seg_base, s);
+  if (f->seg_coord) f->alloc.put(f->seg_coord, f->bytes_seg_coord, s);
+  if (f->perm) f->alloc.put(f->perm, f->bytes_perm, s);
+  f->pidx = nullptr; f->val = nullptr; f->bf = nullptr; f->sf = nullptr;
+  f->seg_base = nullptr; f->seg_coord = nullptr; f->perm = nullptr;
+}
+
+}  // namespace
+
+// Host-side mode taxonomy (Table I) and key layout; used by fcoo_build.
+fcoo_status plan_modes(fcoo_s* f, int order, const int64_t* dims, int op, int mode) {
+  if (order < 2 || order > kMaxOrder) return fail(FCOO_ERR_ORDER, "order %d outside [2,8]", order);
+  if (mode < 0 || mode >= order) return fail(FCOO_ERR_MODE, "mode %d outside [0,%d)", mode, order);
+  if (op != FCOO_OP_MTTKRP && op != FCOO_OP_TTM) return fail(FCOO_ERR_ARG, "unknown op %d", op);
+  f->order = order; f->op = op; f->mode = mode;
+  for (int m = 0; m < order; ++m) {
+    if (dims[m] < 1 || dims[m] > 4294967295LL) return fail(FCOO_ERR_ARG, "dims[%d]=%lld outside [1,2^32)", m, (long long)dims[m]);
+    f->dims[m] = dims[m];
+  }
+  int ni = 0, np = 0;
+  if (op == FCOO_OP_MTTKRP) {
+    f->idx_modes[ni++] = mode;
+    for (int m = 0; m < order; ++m) if (m != mode) f->prod_modes[np++] = m;
+    for (int a = 1; a < np; ++a)  // reading Q5: ascending extent, ties by mode id (stable)
+      for (int b = a; b > 0 && dims[f->prod_modes[b]] < dims[f->prod_modes[b - 1]]; --b) {
+        int t = f->prod_modes[b]; f->prod_modes[b] = f->prod_modes[b - 1]; f->prod_modes[b - 1] = t;
+      }
+  } else {
+    for (int m = 0; m < order; ++m) if (m != mode) f->idx_modes[ni++] = m;
+    f->prod_modes[np++] = mode;
+  }
+  f->n_idx = ni; f->n_prod = np;
+  return FCOO_OK;
+}
+
+fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opts, const fcoo_allocator* alloc,
+                       cudaStream_t s, fcoo_t* out) {
+  if (!coo || !out) return fail(FCOO_ERR_ARG, "NULL coo/out");
+  *out = nullptr;
+  int op = opts ? opts->op : FCOO_OP_MTTKRP;
+  int T = opts ? opts->tile_nnz : 256;
+  unsigned flags = opts ? opts->flags : 0u;
+  if (T < 32 || T > 8192 || (T % 32) != 0) return fail(FCOO_ERR_ARG, "tile_nnz %d must be a multiple of 32 in [32,8192]", T);
+  if (!coo->dims || !coo->idx || !coo->val) return fail(FCOO_ERR_ARG, "NULL dims/idx/val");
+  fcoo_s tmp;
+  fcoo_status st = plan_modes(&tmp, coo->order, coo->dims, op, mode);
+  if (st) return st;
+  if (coo->nnz <= 0) return fail(FCOO_ERR_EMPTY, "nnz == 0");
+  if (coo->nnz >= 4294967295LL) return fail(FCOO_ERR_ARG, "nnz must be < 2^32");
+  for (int m = 0; m < coo->order; ++m) if (!coo->idx[m]) return fail(FCOO_ERR_ARG, "idx[%d] is NULL", m);
+
+  // key layout: key position a -> mode; first position most significant
+  KeyLayout L{};
+  L.order = coo->order;
+  L.n_idx = tmp.n_idx;
+  for (int a = 0; a < tmp.n_idx; ++a) L.key_modes[a] = tmp.idx_modes[a];
+  for (int a = 0; a < tmp.n_prod; ++a) L.key_modes[tmp.n_idx + a] = tmp.prod_modes[a];
+  int total = 0, bits[kMaxOrder];
+  for (int a = 0; a < L.order; ++a) { bits[a] = bits_for(coo->dims[L.key_modes[a]]); total += bits[a]; }
+  if (total > 64) return fail(FCOO_ERR_KEY_BITS, "sort key needs %d bits > 64", total);
+  int sh = 0;
+  for (int a = L.order - 1; a >= 0; --a) {
+    L.shift[a] = sh;
+    L.mask[a] = bits[a] >= 64 ? ~0ull : ((1ull << bits[a]) - 1ull);
+    int64_t d = coo->dims[L.key_modes[a]];
+    L.dims[a] = d >= 4294967296LL ? 0u : (uint32_t)d;
+    sh += bits[a];
+  }
+  L.prod_bits = 0;
+  for (int a = tmp.n_idx; a < L.order; ++a) L.prod_bits += bits[a];
+  IdxPtrs ip{};
+  for (int a = 0; a < L.order; ++a) ip.p[a] = coo->idx[L.key_modes[a]];
+
+  fcoo_s* f = new fcoo_s(tmp);
+  if (alloc && alloc->alloc && alloc->free) { f->alloc.a = *alloc; f->alloc.custom = true; }
+  f->build_stream = s;
+  cudaGetDevice(&f->device);
+  f->T = T;
+  f->nnz = coo->nnz;
+  f->ntiles = (f->nnz + T - 1) / T;
+  f->nnz_pad = f->ntiles * T;
+  f->tile_begin = 0; f->tile_end = f->ntiles;
+  const int64_t nnz = f->nnz, nnz_pad = f->nnz_pad, nwords = nnz_pad / 32, ntiles = f->ntiles;
+
+  auto bail = [&](fcoo_status e) { free_handle_arrays(f); delete f; return e; };
+
+  f->pidx = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)(f->n_prod * nnz_pad), s, &f->bytes_pidx);
+  f->val = grab<float>(f, sizeof(float) * (size_t)nnz_pad, s, &f->bytes_val);
+  f->bf = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)nwords, s, &f->bytes_bf);
+  f->sf = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)((ntiles + 31) / 32 + 1), s, &f->bytes_sf);
+  f->seg_base = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)(ntiles + 1), s, &f->bytes_seg_base);
+  if (flags & FCOO_BUILD_KEEP_PERM) f->perm = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)nnz, s, &f->bytes_perm);
+  if (!f->pidx || !f->val || !f->bf || !f->sf || !f->seg_base || ((flags & FCOO_BUILD_KEEP_PERM) && !f->perm))
+    return bail(fail(FCOO_ERR_OOM, "handle allocation failed"));
+
+  {
+    Buf keys0(&f->alloc, sizeof(uint64_t) * nnz, s), keys1(&f->alloc, sizeof(uint64_t) * nnz, s);
+    Buf ord0(&f->alloc, sizeof(uint32_t) * nnz, s), ord1(&f->alloc, sizeof(uint32_t) * nnz, s);
+    Buf wcount(&f->alloc, sizeof(uint32_t) * (nwords + 1), s), wbase(&f->alloc, sizeof(uint32_t) * (nwords + 1), s);
+    Buf errb(&f->alloc, sizeof(uint32_t) * 2, s);
+    if (!keys0.ok() || !keys1.ok() || !ord0.ok() || !ord1.ok() || !wcount.ok() || !wbase.ok() || !errb.ok())
+      return bail(fail(FCOO_ERR_OOM, "build scratch allocation failed"));
+    cudaError_t ce;
+    if ((ce = cudaMemsetAsync(errb.p, 0, sizeof(uint32_t) * 2, s)) != cudaSuccess ||
+        (ce = cudaMemsetAsync(wcount.p, 0, sizeof(uint32_t) * (nwords + 1), s)) != cudaSuccess)
+      return bail(fail(FCOO_ERR_CUDA, "memset: %s", cudaGetErrorString(ce)));
+
+    const int TB = 256;
+    k_pack_keys<<<(unsigned)((nnz + TB - 1) / TB), TB, 0, s>>>(ip, L, nnz, keys0.as<uint64_t>(), ord0.as<uint32_t>(),
+                                                               errb.as<uint32_t>());
+    count_launch();
+    if ((ce = cudaGetLastError()) != cudaSuccess) return bail(fail(FCOO_ERR_CUDA, "k_pack_keys: %s", cudaGetErrorString(ce)));
+
+    cub::DoubleBuffer<uint64_t> dk(keys0.as<uint64_t>(), keys1.as<uint64_t>());
+    cub::DoubleBuffer<uint32_t> dv(ord0.as<uint32_t>(), ord1.as<uint32_t>());
+    int end_bit = total > 0 ? total : 1;
+    size_t tmp_bytes = 0;
+    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, (int64_t)nnz, 0, end_bit, s);
+    {
+      Buf cubtmp(&f->alloc, tmp_bytes, s);
+      if (!cubtmp.ok()) return bail(fail(FCOO_ERR_OOM, "radix sort scratch"));
+      if ((ce = cub::DeviceRadixSort::SortPairs(cubtmp.p, tmp_bytes, dk, dv, (int64_t)nnz, 0, end_bit, s)) != cudaSuccess)
+        return bail(fail(FCOO_ERR_CUDA, "radix sort: %s", cudaGetErrorString(ce)));
+      count_launch(2 + (end_bit + 7) / 8);
+    }
+    const uint64_t* keys = dk.Current();
+    const uint32_t* ord = dv.Current();
+
+    k_flags<<<(unsigned)((nnz_pad + TB - 1) / TB), TB, 0, s>>>(keys, ord, coo->val, L, f->n_prod, nnz, nnz_pad, f->pidx,
+                                                              f->val, f->bf, wcount.as<uint32_t>(), f->perm,
+                                                              errb.as<uint32_t>());
+    count_launch();
+    if ((ce = cudaGetLastError()) != cudaSuccess) return bail(fail(FCOO_ERR_CUDA, "k_flags: %s", cudaGetErrorString(ce)));
+
+    size_t scan_bytes = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, wcount.as<uint32_t>(), wbase.as<uint32_t>(), (int64_t)(nwords + 1), s);
+    {
+      Buf scantmp(&f->alloc, scan_bytes, s);
+      if (!scantmp.ok()) return bail(fail(FCOO_ERR_OOM, "scan scratch"));
+      if ((ce = cub::DeviceScan::ExclusiveSum(scantmp.p, scan_bytes, wcount.as<uint32_t>(), wbase.as<uint32_t>(),
+                                              (int64_t)(nwords + 1), s)) != cudaSuccess)
+        return bail(fail(FCOO_ERR_CUDA, "scan: %s", cudaGetErrorString(ce)));
+      count_launch(2);
+    }
+    int64_t tthreads = ((ntiles + 1 + 31) / 32) * 32;
+    k_tiles<<<(unsigned)((tthreads + TB - 1) / TB), TB, 0, s>>>(f->bf, wbase.as<uint32_t>(), ntiles, T / 32, nwords,
+                                                               f->sf, f->seg_base);
+    count_launch();
+    if ((ce = cudaGetLastError()) != cudaSuccess) return bail(fail(FCOO_ERR_CUDA, "k_tiles: %s", cudaGetErrorString(ce)));
+
+    uint32_t host[2] = {0, 0};
+    if ((ce = cudaMemcpyAsync(&host[0], errb.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (ce = cudaMemcpyAsync(&host[1], wbase.as<uint32_t>() + nwords, sizeof(uint32_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+        (ce = cudaStreamSynchronize(s)) != cudaSuccess)
+      return bail(fail(FCOO_ERR_CUDA, "build sync: %s", cudaGetErrorString(ce)));
+    if (host[0] & ERRF_INDEX_RANGE) return bail(fail(FCOO_ERR_INDEX_RANGE, "a coordinate is >= its mode extent"));
+    if (host[0] & ERRF_DUPLICATE) return bail(fail(FCOO_ERR_DUPLICATE, "duplicate coordinates"));
+    f->nsegs = host[1];
+    f->dense_rows = (f->op == FCOO_OP_MTTKRP && f->nsegs == f->dims[f->mode]) ? 1 : 0;
+
+    f->seg_coord = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)std::max<int64_t>(1, f->nsegs * f->n_idx), s,
+                                  &f->bytes_seg_coord);
+    if (!f->seg_coord) return bail(fail(FCOO_ERR_OOM, "seg_coord allocation"));
+    k_seg_coord<<<(unsigned)((nnz + TB - 1) / TB), TB, 0, s>>>(keys, f->bf, wbase.as<uint32_t>(), L, nnz, f->seg_coord);
+    count_launch();
+    if ((ce = cudaGetLastError()) != cudaSuccess) return bail(fail(FCOO_ERR_CUDA, "k_seg_coord: %s", cudaGetErrorString(ce)));
+  }  // scratch freed (stream-ordered)
+  *out = f;
+  return FCOO_OK;
+}
+
+void destroy_impl(fcoo_s* f) {
+  if (!f) return;
+  free_handle_arrays(f);
+  delete f;
+}
+
+}  // namespace fcoo

@@ -1,0 +1,381 @@
+// fcoo_cp.cu — CP-ALS (Algorithm 1) on top of the F-COO MTTKRP engine.
+//
+// Per mode n: MTTKRP -> M (fcoo_mttkrp, all-reduced across ranks when
+// sharded); k_solve (one CTA): V = Hadamard_{m!=n} G_m, fp64 Cholesky, W = V^{-1}, falling back to
+// a Jacobi pseudo-inverse when V is not positive definite (reading Q14); k_apply: U_n = M W
+// (fp64 accumulation, fp32 store); k_gram_partial + k_gram_reduce: G_raw = U_n^T U_n (fp64,
+// deterministic two-stage sum); k_norm_stats: lambda = sqrt(diag G_raw), G_n = G_raw / (lambda
+// lambda^T); k_scale: U_n /= lambda (reading Q13).  After the last mode, k_inner_partial +
+// k_fit compute the fit from <X,Xhat> = sum_r lambda_r sum_i M(i,r) U_N(i,r) and
+// |Xhat|^2 = lambda^T (Hadamard G_m) lambda with no extra pass over X.  Every reduction has a
+// fixed order, so replicated ranks compute bit-identical factors from identical M.
+// The paper runs the small matrix ops with CUBLAS on a second stream; here they are
+// microsecond-scale single-purpose kernels on the same stream.
+#include <math.h>
+#include <string.h>
+
+#include <vector>
+
+#include "fcoo_internal.cuh"
+
+namespace fcoo {
+
+namespace {
+
+constexpr int kCT = 256;  // threads per CTA for the small kernels
+
+struct GramPtrs {
+  const double* g[kMaxOrder];
+};
+
+// Deterministic block sum of a double (fixed tree).
+__device__ double block_sum(double v, double* sh) {
+  int t = threadIdx.x;
+  sh[t] = v;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (t < w) sh[t] += sh[t + w];
+    __syncthreads();
+  }
+  double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// One CTA.  V = Hadamard_{m != n} G_m; W = V^{-1} by Cholesky, else Jacobi pinv (tau = R*eps*max|lambda|).
+// Scratch A, Q: R x R doubles each.  status[0] = 0 Cholesky, 1 Jacobi fallback.
+__global__ void k_solve(GramPtrs G, int order, int n, int R, double* __restrict__ A, double* __restrict__ Q,
+                        double* __restrict__ W, int* __restrict__ status) {
+  __shared__ double sh[kCT];
+  __shared__ int fail;
+  __shared__ double cs[2];
+  const int tid = threadIdx.x, nt = blockDim.x, RR = R * R;
+  for (int e = tid; e < RR; e += nt) {
+    double v = 1.0;
+    for (int m = 0; m < order; ++m)
+      if (m != n) v *= G.g[m][e];
+    A[e] = v;   // V (kept for the fallback)
+    W[e] = v;   // Cholesky works in W's lower triangle, then becomes the inverse
+  }
+  if (tid == 0) fail = 0;
+  __syncthreads();
+  double tr = 0.0;
+  for (int a = tid; a < R; a += nt) tr += A[a * R + a];
+  tr = block_sum(tr, sh);
+  const double tiny = 1e-12 * (tr > 0 ? tr / R : 1.0);
+  // Cholesky V = L L^T in the lower triangle of W (column j at a time)
+  for (int j = 0; j < R; ++j) {
+    if (tid == 0) {
+      double d = W[j * R + j];
+      for (int k = 0; k < j; ++k) d -= W[j * R + k] * W[j * R + k];
+      if (!(d > tiny)) fail = 1;
+      W[j * R + j] = d > 0 ? sqrt(d) : 1.0;
+    }
+    __syncthreads();
+    if (fail) break;
+    double ljj = W[j * R + j];
+    for (int i = j + 1 + tid; i < R; i += nt) {
+      double s = W[i * R + j];
+      for (int k = 0; k < j; ++k) s -= W[i * R + k] * W[j * R + k];
+      W[i * R + j] = s / ljj;
+    }
+    __syncthreads();
+  }
+  if (!fail) {
+    // inverse: column c of V^{-1} solves L L^T x = e_c; thread per column, result in Q then W
+    for (int c = tid; c < R; c += nt) {
+      for (int i = 0; i < R; ++i) {  // forward: L y = e_c  (y in Q[:, c])
+        double s = (i == c) ? 1.0 : 0.0;
+        for (int k = 0; k < i; ++k) s -= W[i * R + k] * Q[k * R + c];
+        Q[i * R + c] = s / W[i * R + i];
+      }
+      for (int i = R - 1; i >= 0; --i) {  // backward: L^T x = y (in place in Q[:, c])
+        double s = Q[i * R + c];
+        for (int k = i + 1; k < R; ++k) s -= W[k * R + i] * Q[k * R + c];
+        Q[i * R + c] = s / W[i * R + i];
+      }
+    }
+    __syncthreads();
+    for (int e = tid; e < RR; e += nt) W[e] = Q[e];
+    if (tid == 0) status[0] = 0;
+    return;
+  }
+  // ---- fallback: cyclic Jacobi eigendecomposition of A = V; Q accumulates eigenvectors ----
+  double fro = 0.0;
+  for (int e = tid; e < RR; e += nt) fro += A[e] * A[e];
+  fro = sqrt(block_sum(fro, sh));
+  for (int e = tid; e < RR; e += nt) Q[e] = (e / R == e % R) ? 1.0 : 0.0;
+  __syncthreads();
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0;
+    for (int e = tid; e < RR; e += nt)
+      if (e / R != e % R) off += A[e] * A[e];
+    off = block_sum(off, sh);
+    if (sqrt(off) <= 1e-15 * (fro > 0 ? fro : 1.0)) break;
+    for (int p = 0; p < R - 1; ++p)
+      for (int q = p + 1; q < R; ++q) {
+        if (tid == 0) {
+          double apq = A[p * R + q], c = 1.0, s = 0.0;
+          if (apq != 0.0) {
+            double theta = (A[q * R + q] - A[p * R + p]) / (2.0 * apq);
+            double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+            c = 1.0 / sqrt(t * t + 1.0);
+            s = t * c;
+          }
+          cs[0] = c; cs[1] = s;
+        }
+        __syncthreads();
+        double c = cs[0], s = cs[1];
+        if (s != 0.0) {
+          for (int k = tid; k < R; k += nt) {  // columns p, q of A and Q
+            double akp = A[k * R + p], akq = A[k * R + q];
+            A[k * R + p] = c * akp - s * akq;
+            A[k * R + q] = s * akp + c * akq;
+            double qkp = Q[k * R + p], qkq = Q[k * R + q];
+            Q[k * R + p] = c * qkp - s * qkq;
+            Q[k * R + q] = s * qkp + c * qkq;
+          }
+          __syncthreads();
+          for (int k = tid; k < R; k += nt) {  // rows p, q of A
+            double apk = A[p * R + k], aqk = A[q * R + k];
+            A[p * R + k] = c * apk - s * aqk;
+            A[q * R + k] = s * apk + c * aqk;
+          }
+        }
+        __syncthreads();
+      }
+  }
+  double lmax = 0.0;
+  for (int a = tid; a < R; a += nt) lmax = fmax(lmax, fabs(A[a * R + a]));
+  sh[tid] = lmax;
+  __syncthreads();
+  for (int w = nt / 2; w > 0; w >>= 1) {
+    if (tid < w) sh[tid] = fmax(sh[tid], sh[tid + w]);
+    __syncthreads();
+  }
+  const double tau = (double)R * 2.220446049250313e-16 * sh[0];
+  for (int e = tid; e < RR; e += nt) {
+    int a = e / R, b = e % R;
+    double s = 0.0;
+    for (int k = 0; k < R; ++k) {
+      double lk = A[k * R + k];
+      if (lk > tau) s += Q[a * R + k] * Q[b * R + k] / lk;
+    }
+    W[e] = s;
+  }
+  if (tid == 0) status[0] = 1;
+}
+
+// U[i, b] = sum_a M[i, a] W[a, b]  (fp64 accumulation)
+__global__ void k_apply(const float* __restrict__ M, const double* __restrict__ W, int64_t I, int R,
+                        float* __restrict__ U) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= I * R) return;
+  int64_t i = e / R;
+  int b = (int)(e % R);
+  const float* m = M + i * R;
+  double s = 0.0;
+  for (int a = 0; a < R; ++a) s += (double)m[a] * W[a * R + b];
+  U[e] = (float)s;
+}
+
+// part[c][a*R+b] = sum_{i in chunk c} U[i,a] U[i,b]
+__global__ void k_gram_partial(const float* __restrict__ U, int64_t I, int R, int64_t rows_per,
+                               double* __restrict__ part) {
+  const int c = blockIdx.x;
+  const int64_t i0 = (int64_t)c * rows_per, i1 = min(I, i0 + rows_per);
+  const int RR = R * R;
+  for (int e = threadIdx.x; e < RR; e += blockDim.x) {
+    int a = e / R, b = e % R;
+    double s = 0.0;
+    for (int64_t i = i0; i < i1; ++i) s += (double)U[i * R + a] * (double)U[i * R + b];
+    part[(int64_t)c * RR + e] = s;
+  }
+}
+
+__global__ void k_gram_reduce(const double* __restrict__ part, int nchunks, int RR, double* __restrict__ G) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= RR) return;
+  double s = 0.0;
+  for (int c = 0; c < nchunks; ++c) s += part[(int64_t)c * RR + e];
+  G[e] = s;
+}
+
+// lambda = sqrt(diag Graw); G = Graw / (lambda lambda^T) (0 where lambda == 0)
+__global__ void k_norm_stats(const double* __restrict__ Graw, int R, double* __restrict__ lam,
+                             float* __restrict__ lam_f, double* __restrict__ G) {
+  for (int r = threadIdx.x; r < R; r += blockDim.x) {
+    double l = sqrt(Graw[r * R + r]);
+    lam[r] = l;
+    if (lam_f) lam_f[r] = (float)l;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    int a = e / R, b = e % R;
+    double d = lam[a] * lam[b];
+    G[e] = d > 0 ? Graw[e] / d : 0.0;
+  }
+}
+
+__global__ void k_scale(float* __restrict__ U, int64_t I, int R, const double* __restrict__ lam) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= I * R) return;
+  double l = lam[e % R];
+  if (l > 0) U[e] = (float)((double)U[e] / l);
+}
+
+// part[c] = sum_{i in chunk c} sum_r lambda_r M[i,r] U[i,r]
+__global__ void k_inner_partial(const float* __restrict__ M, const float* __restrict__ U,
+                                const double* __restrict__ lam, int64_t I, int R, int64_t rows_per,
+                                double* __restrict__ part) {
+  __shared__ double sh[kCT];
+  const int64_t i0 = (int64_t)blockIdx.x * rows_per, i1 = min(I, i0 + rows_per);
+  double s = 0.0;
+  for (int64_t e = i0 * R + threadIdx.x; e < i1 * R; e += blockDim.x)
+    s += lam[e % R] * (double)M[e] * (double)U[e];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+__global__ void k_sumsq_partial(const float* __restrict__ v, int64_t n, int64_t per, double* __restrict__ part) {
+  __shared__ double sh[kCT];
+  const int64_t q0 = (int64_t)blockIdx.x * per, q1 = min(n, q0 + per);
+  double s = 0.0;
+  for (int64_t q = q0 + threadIdx.x; q < q1; q += blockDim.x) s += (double)v[q] * (double)v[q];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) part[blockIdx.x] = s;
+}
+
+// fit = 1 - sqrt(max(0, |X|^2 + |Xhat|^2 - 2 <X,Xhat>)) / |X|   (one CTA)
+__global__ void k_fit(const double* __restrict__ inner_part, int ninner, const double* __restrict__ xsq_part,
+                      int nxsq, GramPtrs G, int order, const double* __restrict__ lam, int R,
+                      double* __restrict__ out) {
+  __shared__ double sh[kCT];
+  double inner = 0.0, xsq = 0.0, xh = 0.0;
+  // fixed-order sums (thread-strided then tree): deterministic
+  for (int c = threadIdx.x; c < ninner; c += blockDim.x) inner += inner_part[c];
+  inner = block_sum(inner, sh);
+  for (int c = threadIdx.x; c < nxsq; c += blockDim.x) xsq += xsq_part[c];
+  xsq = block_sum(xsq, sh);
+  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
+    double h = lam[e / R] * lam[e % R];
+    for (int m = 0; m < order; ++m) h *= G.g[m][e];
+    xh += h;
+  }
+  xh = block_sum(xh, sh);
+  if (threadIdx.x == 0) {
+    double r2 = xsq + xh - 2.0 * inner;
+    out[0] = 1.0 - sqrt(r2 > 0 ? r2 : 0.0) / sqrt(xsq);
+  }
+}
+
+unsigned nblk(int64_t n, int t = kCT) { return (unsigned)((n + t - 1) / t); }
+
+}  // namespace
+
+fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* factors, float* lambda,
+                        double* fit_trace, int* iters_done, const fcoo_allocator* alloc, cudaStream_t s) {
+  if (!X || !o || !factors || !fit_trace) return fail(FCOO_ERR_ARG, "NULL argument");
+  const int N = X->order, R = o->R;
+  if (N < 2 || N > kMaxOrder) return fail(FCOO_ERR_ORDER, "order %d", N);
+  if (R < 1 || R > 256) return fail(FCOO_ERR_RANK, "R=%d outside [1,256]", R);
+  if (o->iters < 1) return fail(FCOO_ERR_ARG, "iters < 1");
+  for (int m = 0; m < N; ++m) if (!factors[m]) return fail(FCOO_ERR_ARG, "factors[%d] NULL", m);
+  if (iters_done) *iters_done = 0;
+  Alloc al;
+  if (alloc && alloc->alloc && alloc->free) { al.a = *alloc; al.custom = true; }
+
+  // F-COO for every mode, built once up front
+  std::vector<fcoo_t> H(N, nullptr);
+  auto cleanup = [&]() { for (auto h : H) fcoo_destroy(h); };
+  fcoo_build_opts bo{FCOO_OP_MTTKRP, o->tile_nnz > 0 ? o->tile_nnz : 256, 0u};
+  for (int n = 0; n < N; ++n) {
+    fcoo_status st = fcoo_build(X, n, &bo, alloc, (void*)s, &H[n]);
+    if (st) { cleanup(); return st; }
+    if (o->comm && o->nranks > 1) fcoo_set_shard(H[n], o->rank, o->nranks, o->comm);
+  }
+  int64_t Imax = 0;
+  for (int m = 0; m < N; ++m) Imax = std::max(Imax, X->dims[m]);
+  const int RR = R * R;
+  const int64_t maxchunks = 256;
+  Buf M(&al, sizeof(float) * Imax * R, s), Gs(&al, sizeof(double) * N * RR, s), Graw(&al, sizeof(double) * RR, s);
+  Buf A(&al, sizeof(double) * RR, s), Q(&al, sizeof(double) * RR, s), W(&al, sizeof(double) * RR, s);
+  Buf lam(&al, sizeof(double) * R, s), part(&al, sizeof(double) * maxchunks * RR, s);
+  Buf ipart(&al, sizeof(double) * maxchunks, s), xpart(&al, sizeof(double) * maxchunks, s);
+  Buf fitd(&al, sizeof(double) * 2, s), status(&al, sizeof(int) * 2, s);
+  if (!M.ok() || !Gs.ok() || !Graw.ok() || !A.ok() || !Q.ok() || !W.ok() || !lam.ok() || !part.ok() || !ipart.ok() ||
+      !xpart.ok() || !fitd.ok() || !status.ok()) {
+    cleanup();
+    return fail(FCOO_ERR_OOM, "cp_als scratch");
+  }
+  GramPtrs gp{};
+  for (int m = 0; m < N; ++m) gp.g[m] = Gs.as<double>() + (int64_t)m * RR;
+
+  auto chunks_for = [&](int64_t I) { return (int)std::min<int64_t>(maxchunks, std::max<int64_t>(1, (I + 255) / 256)); };
+  auto gram = [&](const float* U, int64_t I, double* out) -> fcoo_status {
+    int nc = chunks_for(I);
+    int64_t per = (I + nc - 1) / nc;
+    k_gram_partial<<<nc, kCT, 0, s>>>(U, I, R, per, part.as<double>());
+    FCOO_LAUNCH_CHECK();
+    k_gram_reduce<<<nblk(RR), kCT, 0, s>>>(part.as<double>(), nc, RR, out);
+    FCOO_LAUNCH_CHECK();
+    return FCOO_OK;
+  };
+  fcoo_status st = FCOO_OK;
+  // initial Grams of the given factors; |X|^2
+  for (int m = 0; m < N && !st; ++m) st = gram(factors[m], X->dims[m], Gs.as<double>() + (int64_t)m * RR);
+  int nx = (int)std::min<int64_t>(maxchunks, std::max<int64_t>(1, (X->nnz + 65535) / 65536));
+  int64_t xper = (X->nnz + nx - 1) / nx;
+  if (!st) {
+    k_sumsq_partial<<<nx, kCT, 0, s>>>(X->val, X->nnz, xper, xpart.as<double>());
+    fcoo::count_launch();
+    if (cudaGetLastError() != cudaSuccess) st = fail(FCOO_ERR_CUDA, "k_sumsq_partial");
+  }
+  double fit_prev = 0.0;
+  int it = 0;
+  for (; it < o->iters && !st; ++it) {
+    for (int n = 0; n < N && !st; ++n) {
+      const int64_t In = X->dims[n];
+      st = fcoo_mttkrp(H[n], factors, R, M.as<float>(), (void*)s);
+      if (st) break;
+      k_solve<<<1, kCT, 0, s>>>(gp, N, n, R, A.as<double>(), Q.as<double>(), W.as<double>(), status.as<int>());
+      FCOO_LAUNCH_CHECK();
+      k_apply<<<nblk(In * R), kCT, 0, s>>>(M.as<float>(), W.as<double>(), In, R, factors[n]);
+      FCOO_LAUNCH_CHECK();
+      st = gram(factors[n], In, Graw.as<double>());
+      if (st) break;
+      k_norm_stats<<<1, kCT, 0, s>>>(Graw.as<double>(), R, lam.as<double>(), lambda,
+                                     Gs.as<double>() + (int64_t)n * RR);
+      FCOO_LAUNCH_CHECK();
+      k_scale<<<nblk(In * R), kCT, 0, s>>>(factors[n], In, R, lam.as<double>());
+      FCOO_LAUNCH_CHECK();
+    }
+    if (st) break;
+    const int nl = N - 1;
+    const int64_t Il = X->dims[nl];
+    int nc = chunks_for(Il);
+    int64_t per = (Il + nc - 1) / nc;
+    k_inner_partial<<<nc, kCT, 0, s>>>(M.as<float>(), factors[nl], lam.as<double>(), Il, R, per, ipart.as<double>());
+    FCOO_LAUNCH_CHECK();
+    k_fit<<<1, kCT, 0, s>>>(ipart.as<double>(), nc, xpart.as<double>(), nx, gp, N, lam.as<double>(), R,
+                            fitd.as<double>());
+    FCOO_LAUNCH_CHECK();
+    double fit = 0.0;
+    cudaError_t ce = cudaMemcpyAsync(&fit, fitd.p, sizeof(double), cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+    if (ce != cudaSuccess) { st = fail(FCOO_ERR_CUDA, "fit readback: %s", cudaGetErrorString(ce)); break; }
+    fit_trace[it] = fit;
+    if (iters_done) *iters_done = it + 1;
+    if (o->tol > 0 && it > 0 && fabs(fit - fit_prev) < o->tol) { ++it; break; }
+    fit_prev = fit;
+  }
+  cleanup();
+  return st;
+}
+
+}  // namespace fcoo
+
+extern "C" fcoo_status cp_als(const fcoo_coo* tensor, const fcoo_cp_opts* opts, float* const* factors, float* lambda,
+                              double* fit_trace, int* iters_done, const fcoo_allocator* alloc, void* stream) {
+  return fcoo::cp_als_impl(tensor, opts, factors, lambda, fit_trace, iters_done, alloc, (cudaStream_t)stream);
+}

@@ -1,0 +1,92 @@
+// fcoo_internal.cuh — private declarations shared by the libfcoo translation units.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <atomic>
+#include <string>
+
+#include "fcoo.h"
+
+namespace fcoo {
+
+constexpr int kMaxOrder = 8;
+
+// Thread-local detail message for fcoo_last_error().
+void set_error(const char* fmt, ...);
+fcoo_status fail(fcoo_status s, const char* fmt, ...);
+
+extern std::atomic<uint64_t> g_launches;
+inline void count_launch(uint64_t n = 1) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+
+// Device memory through the caller's allocator (or stream-ordered cudaMallocAsync).
+struct Alloc {
+  fcoo_allocator a{};
+  bool custom = false;
+  void* get(size_t bytes, cudaStream_t s) const;
+  void put(void* p, size_t bytes, cudaStream_t s) const;
+};
+
+struct Buf {  // RAII temp buffer
+  const Alloc* al = nullptr;
+  void* p = nullptr;
+  size_t n = 0;
+  cudaStream_t s = nullptr;
+  Buf() = default;
+  Buf(const Alloc* a, size_t bytes, cudaStream_t st) : al(a), n(bytes), s(st) { p = bytes ? a->get(bytes, st) : nullptr; }
+  ~Buf() { if (p) al->put(p, n, s); }
+  Buf(const Buf&) = delete;
+  Buf& operator=(const Buf&) = delete;
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+  bool ok() const { return n == 0 || p != nullptr; }
+};
+
+}  // namespace fcoo
+
+// The F-COO handle (layout in DESIGN.md "Data layout in HBM").
+struct fcoo_s {
+  int order = 0, op = 0, mode = 0, n_idx = 0, n_prod = 0;
+  int idx_modes[fcoo::kMaxOrder] = {0}, prod_modes[fcoo::kMaxOrder] = {0};
+  int64_t dims[fcoo::kMaxOrder] = {0};
+  int64_t nnz = 0, nnz_pad = 0, ntiles = 0, nsegs = 0, T = 256;
+  int dense_rows = 0;
+  // device arrays
+  uint32_t* pidx = nullptr;      // n_prod x nnz_pad (row a = product mode prod_modes[a])
+  float* val = nullptr;          // nnz_pad
+  uint32_t* bf = nullptr;        // nnz_pad / 32 words, LSB-first
+  uint32_t* sf = nullptr;        // ceil(ntiles/32) words (+1)
+  uint32_t* seg_base = nullptr;  // ntiles + 1 (last = nsegs)
+  uint32_t* seg_coord = nullptr; // nsegs x n_idx
+  uint32_t* perm = nullptr;      // nnz (KEEP_PERM only)
+  size_t bytes_pidx = 0, bytes_val = 0, bytes_bf = 0, bytes_sf = 0, bytes_seg_base = 0, bytes_seg_coord = 0,
+         bytes_perm = 0;
+  // shard
+  int shard = 0, nshards = 1;
+  int64_t tile_begin = 0, tile_end = 0;
+  fcoo_comm_t comm = nullptr;
+  fcoo::Alloc alloc;
+  cudaStream_t build_stream = nullptr;
+  int device = 0;
+};
+
+namespace fcoo {
+// engine entry points (fcoo_engine.cu)
+fcoo_status run_mttkrp(fcoo_s* f, const float* const* factors, int R, float* out, cudaStream_t s);
+fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s);
+}  // namespace fcoo
+
+#define FCOO_CUDA_TRY(expr)                                                                         \
+  do {                                                                                              \
+    cudaError_t _e = (expr);                                                                        \
+    if (_e != cudaSuccess)                                                                          \
+      return fcoo::fail(FCOO_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+  } while (0)
+
+#define FCOO_LAUNCH_CHECK()                                                                         \
+  do {                                                                                              \
+    fcoo::count_launch();                                                                           \
+    cudaError_t _e = cudaGetLastError();                                                            \
+    if (_e != cudaSuccess)                                                                          \
+      return fcoo::fail(FCOO_ERR_CUDA, "%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(_e)); \
+  } while (0)

@@ -1,0 +1,358 @@
+"""Thin ctypes binding over libfcoo.so (include/fcoo.h) — argument marshalling only.
+
+Every step of the path runs in the library's CUDA kernels; PyTorch supplies device memory
+(the caching allocator, through fcoo_allocator callbacks), streams and torch.distributed (to
+broadcast the NCCL unique id).  There is no CPU fallback: if libfcoo.so is missing or no CUDA
+device is present, calls raise.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libfcoo.so")
+
+OK = 0
+ERR_ARG, ERR_ORDER, ERR_MODE, ERR_INDEX_RANGE, ERR_DUPLICATE, ERR_EMPTY, ERR_KEY_BITS, ERR_RANK, ERR_SHAPE, \
+    ERR_ALIGN, ERR_OOM, ERR_CUDA, ERR_NCCL, ERR_NOT_FINITE = range(1, 15)
+OP_MTTKRP, OP_TTM = 0, 1
+BUILD_KEEP_PERM = 1
+
+
+class FcooError(RuntimeError):
+    def __init__(self, code: int, where: str, detail: str):
+        super().__init__(f"{where}: status {code} ({detail})")
+        self.code = code
+
+
+class _Coo(ctypes.Structure):
+    _fields_ = [("order", ctypes.c_int), ("dims", ctypes.POINTER(ctypes.c_int64)), ("nnz", ctypes.c_int64),
+                ("idx", ctypes.POINTER(ctypes.c_void_p)), ("val", ctypes.c_void_p)]
+
+
+_ALLOC_FN = ctypes.CFUNCTYPE(ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+_FREE_FN = ctypes.CFUNCTYPE(None, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_void_p)
+
+
+class _Allocator(ctypes.Structure):
+    _fields_ = [("alloc", _ALLOC_FN), ("free", _FREE_FN), ("ctx", ctypes.c_void_p)]
+
+
+class _BuildOpts(ctypes.Structure):
+    _fields_ = [("op", ctypes.c_int), ("tile_nnz", ctypes.c_int), ("flags", ctypes.c_uint)]
+
+
+class _Info(ctypes.Structure):
+    _fields_ = [("order", ctypes.c_int), ("op", ctypes.c_int), ("mode", ctypes.c_int), ("n_idx", ctypes.c_int),
+                ("n_prod", ctypes.c_int), ("idx_modes", ctypes.c_int * 8), ("prod_modes", ctypes.c_int * 8),
+                ("dims", ctypes.c_int64 * 8), ("nnz", ctypes.c_int64), ("nsegs", ctypes.c_int64),
+                ("ntiles", ctypes.c_int64), ("tile_nnz", ctypes.c_int64), ("dense_rows", ctypes.c_int),
+                ("storage_bytes", ctypes.c_int64), ("seg_table_bytes", ctypes.c_int64),
+                ("device_bytes", ctypes.c_int64), ("shard", ctypes.c_int), ("nshards", ctypes.c_int),
+                ("tile_begin", ctypes.c_int64), ("tile_end", ctypes.c_int64)]
+
+
+class _HostView(ctypes.Structure):
+    _fields_ = [("perm", ctypes.c_void_p), ("bf", ctypes.c_void_p), ("sf", ctypes.c_void_p),
+                ("seg_base", ctypes.c_void_p), ("seg_coord", ctypes.c_void_p), ("pidx", ctypes.c_void_p),
+                ("val", ctypes.c_void_p)]
+
+
+class _CpOpts(ctypes.Structure):
+    _fields_ = [("R", ctypes.c_int), ("iters", ctypes.c_int), ("tol", ctypes.c_double), ("tile_nnz", ctypes.c_int),
+                ("comm", ctypes.c_void_p), ("rank", ctypes.c_int), ("nranks", ctypes.c_int)]
+
+
+# The exported symbols (every one declared in include/fcoo.h).
+SYMBOLS = ["fcoo_build", "fcoo_mttkrp", "fcoo_ttm", "fcoo_info", "fcoo_export", "fcoo_destroy",
+           "fcoo_comm_unique_id", "fcoo_comm_init", "fcoo_comm_destroy", "fcoo_allreduce_sum", "fcoo_set_shard",
+           "cp_als", "fcoo_status_str", "fcoo_last_error", "fcoo_launch_count"]
+
+_lib = None
+
+
+def load_library():
+    """Load libfcoo.so (raises if it was not built — there is no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+    L = ctypes.CDLL(LIB_PATH)
+    vp, ci, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
+    L.fcoo_build.argtypes = [ctypes.POINTER(_Coo), ci, ctypes.POINTER(_BuildOpts), ctypes.POINTER(_Allocator), vp,
+                             ctypes.POINTER(vp)]
+    L.fcoo_mttkrp.argtypes = [vp, ctypes.POINTER(vp), ci, vp, vp]
+    L.fcoo_ttm.argtypes = [vp, vp, ci, vp, vp]
+    L.fcoo_info.argtypes = [vp, ctypes.POINTER(_Info)]
+    L.fcoo_export.argtypes = [vp, ctypes.POINTER(_HostView), vp]
+    L.fcoo_destroy.argtypes = [vp]
+    L.fcoo_comm_unique_id.argtypes = [vp]
+    L.fcoo_comm_init.argtypes = [ci, ci, vp, ctypes.POINTER(vp)]
+    L.fcoo_comm_destroy.argtypes = [vp]
+    L.fcoo_allreduce_sum.argtypes = [vp, vp, ctypes.c_size_t, vp]
+    L.fcoo_set_shard.argtypes = [vp, ci, ci, vp]
+    L.cp_als.argtypes = [ctypes.POINTER(_Coo), ctypes.POINTER(_CpOpts), ctypes.POINTER(vp), vp,
+                         ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ci), ctypes.POINTER(_Allocator), vp]
+    L.fcoo_status_str.restype = ctypes.c_char_p
+    L.fcoo_status_str.argtypes = [ci]
+    L.fcoo_last_error.restype = ctypes.c_char_p
+    L.fcoo_launch_count.restype = ctypes.c_uint64
+    for name in SYMBOLS[:-3]:
+        getattr(L, name).restype = ci
+    _lib = L
+    return L
+
+
+def _check(rc: int, where: str):
+    if rc != OK:
+        L = load_library()
+        raise FcooError(rc, where, f"{L.fcoo_status_str(rc).decode()}: {L.fcoo_last_error().decode()}")
+
+
+def launch_count() -> int:
+    return int(load_library().fcoo_launch_count())
+
+
+# ---- torch caching allocator behind fcoo_allocator ----
+_live = {}
+
+
+@_ALLOC_FN
+def _torch_alloc(nbytes, stream, ctx):
+    try:
+        p = torch.cuda.caching_allocator_alloc(int(nbytes), torch.cuda.current_device(), stream or 0)
+        _live[p] = nbytes
+        return p
+    except Exception:  # surfaces as FCOO_ERR_OOM
+        return None
+
+
+@_FREE_FN
+def _torch_free(ptr, nbytes, stream, ctx):
+    if ptr:
+        _live.pop(ptr, None)
+        torch.cuda.caching_allocator_delete(ptr)
+
+
+_ALLOCATOR = _Allocator(_torch_alloc, _torch_free, None)
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return int(stream.cuda_stream) if hasattr(stream, "cuda_stream") else int(stream)
+
+
+def _require_cuda(t: torch.Tensor, dtype, name: str):
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise ValueError(f"{name} must be {dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+
+
+class Coo:
+    """Device COO tensor: idx (order, nnz) int32-viewed-as-uint32 CUDA tensor, val (nnz,) float32."""
+
+    def __init__(self, dims, idx: torch.Tensor, val: torch.Tensor):
+        _require_cuda(idx, torch.int32, "idx")
+        _require_cuda(val, torch.float32, "val")
+        self.dims = [int(d) for d in dims]
+        self.idx, self.val = idx, val
+        self._dims = (ctypes.c_int64 * len(self.dims))(*self.dims)
+        self._ptrs = (ctypes.c_void_p * len(self.dims))(*[idx[m].data_ptr() for m in range(len(self.dims))])
+        self.c = _Coo(len(self.dims), self._dims, int(val.shape[0]), self._ptrs, val.data_ptr())
+
+    @property
+    def order(self):
+        return len(self.dims)
+
+    @property
+    def nnz(self):
+        return int(self.val.shape[0])
+
+    @staticmethod
+    def from_numpy(dims, idx_np, val_np, device=None):
+        import numpy as np
+        idx = torch.from_numpy(np.ascontiguousarray(idx_np).view(np.int32)).to(device or "cuda")
+        val = torch.from_numpy(np.ascontiguousarray(val_np, dtype=np.float32)).to(device or "cuda")
+        return Coo(dims, idx, val)
+
+
+@dataclass
+class Info:
+    order: int
+    op: int
+    mode: int
+    n_idx: int
+    n_prod: int
+    idx_modes: list
+    prod_modes: list
+    dims: list
+    nnz: int
+    nsegs: int
+    ntiles: int
+    tile_nnz: int
+    dense_rows: bool
+    storage_bytes: int
+    seg_table_bytes: int
+    device_bytes: int
+    shard: int
+    nshards: int
+    tile_begin: int
+    tile_end: int
+
+
+class Fcoo:
+    """Owning wrapper of an fcoo_t handle (fcoo_build ... fcoo_destroy)."""
+
+    def __init__(self, handle: int, keep: Coo):
+        self.h = ctypes.c_void_p(handle)
+        self._coo = keep  # the build borrows the COO only until the build returns; kept for clarity
+        self.info = self._info()
+
+    def _info(self) -> Info:
+        inf = _Info()
+        _check(load_library().fcoo_info(self.h, ctypes.byref(inf)), "fcoo_info")
+        o = inf.order
+        return Info(o, inf.op, inf.mode, inf.n_idx, inf.n_prod, list(inf.idx_modes[: inf.n_idx]),
+                    list(inf.prod_modes[: inf.n_prod]), list(inf.dims[:o]), inf.nnz, inf.nsegs, inf.ntiles,
+                    inf.tile_nnz, bool(inf.dense_rows), inf.storage_bytes, inf.seg_table_bytes, inf.device_bytes,
+                    inf.shard, inf.nshards, inf.tile_begin, inf.tile_end)
+
+    def destroy(self):
+        if self.h:
+            load_library().fcoo_destroy(self.h)
+            self.h = ctypes.c_void_p(None)
+
+    def __del__(self):
+        try:
+            self.destroy()
+        except Exception:
+            pass
+
+
+def fcoo_build(coo: Coo, mode: int, op: int = OP_MTTKRP, tile_nnz: int = 256, keep_perm: bool = False,
+               stream=None) -> Fcoo:
+    L = load_library()
+    opts = _BuildOpts(op, tile_nnz, BUILD_KEEP_PERM if keep_perm else 0)
+    out = ctypes.c_void_p()
+    _check(L.fcoo_build(ctypes.byref(coo.c), mode, ctypes.byref(opts), ctypes.byref(_ALLOCATOR),
+                        ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out)), "fcoo_build")
+    return Fcoo(out.value, coo)
+
+
+def fcoo_mttkrp(f: Fcoo, factors, R: int, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """factors: list of `order` CUDA fp32 (I_m, R) tensors (entry [mode] may be None)."""
+    L = load_library()
+    ptrs = []
+    for m, U in enumerate(factors):
+        if U is None:
+            ptrs.append(None)
+            continue
+        _require_cuda(U, torch.float32, f"factors[{m}]")
+        ptrs.append(U.data_ptr())
+    _require_cuda(out, torch.float32, "out")
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    _check(L.fcoo_mttkrp(f.h, arr, R, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))),
+           "fcoo_mttkrp")
+    return out
+
+
+def fcoo_ttm(f: Fcoo, U: torch.Tensor, R: int, out: torch.Tensor, stream=None) -> torch.Tensor:
+    L = load_library()
+    _require_cuda(U, torch.float32, "U")
+    _require_cuda(out, torch.float32, "out")
+    _check(L.fcoo_ttm(f.h, ctypes.c_void_p(U.data_ptr()), R, ctypes.c_void_p(out.data_ptr()),
+                      ctypes.c_void_p(_stream_ptr(stream))), "fcoo_ttm")
+    return out
+
+
+def fcoo_export(f: Fcoo, perm: bool = False, stream=None) -> dict:
+    import numpy as np
+    i = f.info
+    nnz = i.nnz
+    d = {
+        "bf": np.zeros((nnz + 7) // 8, np.uint8),
+        "sf": np.zeros((i.ntiles + 31) // 32, np.uint32),
+        "seg_base": np.zeros(i.ntiles, np.uint32),
+        "seg_coord": np.zeros((i.nsegs, i.n_idx), np.uint32),
+        "pidx": np.zeros((i.n_prod, nnz), np.uint32),
+        "val": np.zeros(nnz, np.float32),
+    }
+    if perm:
+        d["perm"] = np.zeros(nnz, np.uint32)
+    v = _HostView(*(d[k].ctypes.data if k in d else None
+                    for k in ("perm", "bf", "sf", "seg_base", "seg_coord", "pidx", "val")))
+    _check(load_library().fcoo_export(f.h, ctypes.byref(v), ctypes.c_void_p(_stream_ptr(stream))), "fcoo_export")
+    return d
+
+
+class Comm:
+    def __init__(self, handle: int, rank: int, nranks: int):
+        self.h = ctypes.c_void_p(handle)
+        self.rank, self.nranks = rank, nranks
+
+    def destroy(self):
+        if self.h:
+            load_library().fcoo_comm_destroy(self.h)
+            self.h = ctypes.c_void_p(None)
+
+
+def fcoo_comm_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(load_library().fcoo_comm_unique_id(buf), "fcoo_comm_unique_id")
+    return buf.raw
+
+
+def fcoo_comm_init(rank: int, nranks: int, uid: bytes) -> Comm:
+    out = ctypes.c_void_p()
+    buf = ctypes.create_string_buffer(uid, 128)
+    _check(load_library().fcoo_comm_init(rank, nranks, buf, ctypes.byref(out)), "fcoo_comm_init")
+    return Comm(out.value, rank, nranks)
+
+
+def comm_from_process_group(group=None) -> Comm:
+    """NCCL communicator of the library, unique id broadcast over torch.distributed."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    obj = [fcoo_comm_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    return fcoo_comm_init(rank, world, obj[0])
+
+
+def fcoo_allreduce_sum(comm: Comm, buf: torch.Tensor, stream=None):
+    _require_cuda(buf, torch.float32, "buf")
+    _check(load_library().fcoo_allreduce_sum(comm.h, ctypes.c_void_p(buf.data_ptr()), buf.numel(),
+                                             ctypes.c_void_p(_stream_ptr(stream))), "fcoo_allreduce_sum")
+
+
+def fcoo_set_shard(f: Fcoo, shard: int, nshards: int, comm: Comm | None = None):
+    _check(load_library().fcoo_set_shard(f.h, shard, nshards, comm.h if comm else None), "fcoo_set_shard")
+    f.info = f._info()
+
+
+def cp_als(coo: Coo, R: int, iters: int, factors, tol: float = 0.0, tile_nnz: int = 256, comm: Comm | None = None,
+           stream=None):
+    """In-place CP-ALS: `factors` (list of CUDA fp32 (I_m, R)) hold the initial factors and receive
+    the result.  Returns (lambda CUDA fp32 (R,), fit_trace list)."""
+    import numpy as np
+    L = load_library()
+    for m, U in enumerate(factors):
+        _require_cuda(U, torch.float32, f"factors[{m}]")
+    lam = torch.empty(R, dtype=torch.float32, device=factors[0].device)
+    trace = np.zeros(iters, np.float64)
+    done = ctypes.c_int(0)
+    opts = _CpOpts(R, iters, tol, tile_nnz, comm.h if comm else None, comm.rank if comm else 0,
+                   comm.nranks if comm else 1)
+    arr = (ctypes.c_void_p * len(factors))(*[U.data_ptr() for U in factors])
+    _check(L.cp_als(ctypes.byref(coo.c), ctypes.byref(opts), arr, ctypes.c_void_p(lam.data_ptr()),
+                    trace.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(done),
+                    ctypes.byref(_ALLOCATOR), ctypes.c_void_p(_stream_ptr(stream))), "cp_als")
+    return lam, list(trace[: done.value])

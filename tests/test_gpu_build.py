@@ -1,0 +1,91 @@
+"""GPU: the device F-COO build is bit-exact against the oracle build (SURVEY §8(c) c1 acceptance),
+through the C ABI (fcoo_build + fcoo_export)."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def F():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_1705_09905_b200 as F
+    return F
+
+
+def _compare(F, dims, idx, val, op, mode, T):
+    coo = F.Coo.from_numpy(dims, idx, val)
+    h = F.fcoo_build(coo, mode, op=op, tile_nnz=T, keep_perm=True)
+    got = F.fcoo_export(h, perm=True)
+    ref = oracle.build_fcoo(dims, idx, val, op, mode, T)
+    assert h.info.nsegs == ref.nsegs
+    assert h.info.idx_modes == ref.index_modes and h.info.prod_modes == ref.product_modes
+    assert np.array_equal(got["perm"], ref.perm)
+    assert got["bf"].tobytes() == ref.bf.tobytes()
+    assert got["sf"].tobytes() == ref.sf.tobytes()
+    assert got["seg_base"].tobytes() == ref.seg_base.tobytes()
+    assert got["seg_coord"].tobytes() == ref.seg_coord.tobytes()
+    assert got["pidx"].tobytes() == ref.pidx.tobytes()
+    assert got["val"].tobytes() == ref.val.tobytes()
+    assert h.info.storage_bytes == oracle.storage_bytes(val.shape[0], len(ref.product_modes), T)
+    h.destroy()
+
+
+def test_build_tiny_all_modes(F):
+    w = gen.WORKLOADS["tiny"]
+    idx, val = gen.coo(w.dims, w.nnz, w.alpha, w.seed)
+    for mode in range(3):
+        for op in (F.OP_MTTKRP, F.OP_TTM):
+            _compare(F, w.dims, idx, val, op, mode, 32)
+
+
+@pytest.mark.parametrize("T", [32, 64, 256, 1024])
+def test_build_random(F, T):
+    for dims, alpha in (((300, 200, 500), (0.5, 0.5, 0.5)), ((40, 50, 30, 20), (0.8, 0.0, 0.5, 0.3)),
+                        ((3000, 7), (0.0, 0.0))):
+        idx, val = gen.coo(dims, 20000, alpha, 17)
+        for mode in range(len(dims)):
+            for op in (F.OP_MTTKRP, F.OP_TTM):
+                _compare(F, dims, idx, val, op, mode, T)
+
+
+def test_build_nell2_subset(F):
+    w = gen.WORKLOADS["nell2"]
+    idx, val = gen.coo(w.dims, 2_000_000, w.alpha, w.seed)
+    for mode in range(3):
+        _compare(F, w.dims, idx, val, F.OP_MTTKRP, mode, 256)
+
+
+def test_build_edge_cases(F):
+    # singleton tensor; all nonzeros in one slice (one giant segment); all singleton segments
+    _compare(F, (5, 6, 7), np.array([[3], [4], [5]], np.uint32), np.array([2.5], np.float32), F.OP_MTTKRP, 1, 32)
+    n = 5000
+    one = np.stack([np.zeros(n, np.uint32), (np.arange(n) % 100).astype(np.uint32),
+                    (np.arange(n) // 100).astype(np.uint32)])
+    v = gen.uniform((n,), 3, 0) + 0.5
+    _compare(F, (1, 100, 50), one, v, F.OP_MTTKRP, 0, 64)
+    single = np.stack([np.arange(n, dtype=np.uint32), (np.arange(n) * 7 % 13).astype(np.uint32),
+                       np.zeros(n, np.uint32)])
+    _compare(F, (n, 13, 1), single, v, F.OP_MTTKRP, 0, 32)
+    _compare(F, (n, 13, 1), single, v, F.OP_TTM, 2, 32)
+
+
+def test_build_errors(F):
+    dims = (10, 10, 10)
+    idx = np.array([[1, 2, 1], [1, 2, 1], [1, 2, 1]], np.uint32)  # duplicate (1,1,1)
+    val = np.ones(3, np.float32)
+    with pytest.raises(F.FcooError) as e:
+        F.fcoo_build(F.Coo.from_numpy(dims, idx, val), 0)
+    assert e.value.code == 5  # FCOO_ERR_DUPLICATE
+    bad = np.array([[1, 2], [1, 10], [1, 2]], np.uint32)
+    with pytest.raises(F.FcooError) as e:
+        F.fcoo_build(F.Coo.from_numpy(dims, bad, val[:2]), 0)
+    assert e.value.code == 4  # FCOO_ERR_INDEX_RANGE
+    big = (1 << 30, 1 << 30, 1 << 30)
+    with pytest.raises(F.FcooError) as e:
+        F.fcoo_build(F.Coo.from_numpy(big, idx[:, :2].copy(), val[:2]), 0)
+    assert e.value.code == 7  # FCOO_ERR_KEY_BITS

@@ -1,0 +1,132 @@
+"""GPU parity of fcoo_mttkrp (through the C ABI) against the fp64 oracle, element by element,
+normalised by the per-element sum of |contributions| (tolerance 1e-4, north_star)."""
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from parity import assert_parity
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def F():
+    import torch
+    assert torch.cuda.is_available()
+    import paper_1705_09905_b200 as F
+    return F
+
+
+def _run(F, dims, idx, val, mode, factors_np, R, T=256, shards=1):
+    import torch
+    coo = F.Coo.from_numpy(dims, idx, val)
+    h = F.fcoo_build(coo, mode, tile_nnz=T)
+    fs = [torch.from_numpy(f).cuda() for f in factors_np]
+    out = torch.full((dims[mode], R), float("nan"), device="cuda")
+    if shards == 1:
+        F.fcoo_mttkrp(h, fs, R, out)
+    else:  # fake multi-rank: shards run one after another, partials summed on device
+        acc = torch.zeros_like(out)
+        for g in range(shards):
+            F.fcoo_set_shard(h, g, shards)
+            F.fcoo_mttkrp(h, fs, R, out)
+            acc += out
+        out = acc
+    torch.cuda.synchronize()
+    res = out.cpu().numpy()
+    h.destroy()
+    return res
+
+
+def _check(F, dims, idx, val, mode, R, T=256, signed=False, shards=1, seed=5):
+    fs = gen.factors(dims, R, seed, signed=signed)
+    got = _run(F, dims, idx, val, mode, fs, R, T, shards)
+    M, D = oracle.mttkrp(dims, idx, val, mode, fs, nthreads=8)
+    return assert_parity(got, M, D, what=f"dims={dims} mode={mode} R={R} T={T} shards={shards}")
+
+
+def test_tiny_config_all_modes(F):
+    """BASELINE configs[0]: 50x40x30, 1000 nnz, R=8, all modes."""
+    w = gen.WORKLOADS["tiny"]
+    idx, val = gen.coo(w.dims, w.nnz, w.alpha, w.seed)
+    for mode in range(3):
+        _check(F, w.dims, idx, val, mode, 8, T=32)
+        _check(F, w.dims, idx, val, mode, 8, T=256, signed=True)
+
+
+@pytest.mark.parametrize("R", [1, 3, 4, 8, 16, 32, 64, 100, 128, 200, 256])
+def test_ranks(F, R):
+    dims = (300, 200, 500)
+    idx, val = gen.coo(dims, 30000, (0.5, 0.5, 0.5), 23)
+    for mode in range(3):
+        _check(F, dims, idx, val, mode, R, T=64, signed=True)
+
+
+@pytest.mark.parametrize("dims", [(40, 50, 30, 20), (12, 10, 8, 6, 5), (3000, 7), (9, 8, 7, 6, 5, 4, 3)])
+def test_orders(F, dims):
+    nnz = min(20000, int(np.prod(dims) * 0.3))
+    idx, val = gen.coo(dims, nnz, None, 29)
+    for mode in range(len(dims)):
+        for R in (16, 5):
+            _check(F, dims, idx, val, mode, R, T=32, signed=True)
+
+
+@pytest.mark.parametrize("T", [32, 96, 256, 1024, 4096])
+def test_tile_sizes_and_ragged_tail(F, T):
+    dims = (700, 500, 900)
+    idx, val = gen.coo(dims, 12345, (0.7, 0.3, 0.5), 31)
+    for mode in range(3):
+        _check(F, dims, idx, val, mode, 32, T=T)
+
+
+def test_adversarial_segments(F):
+    n = 20000
+    v = gen.uniform((n,), 3, 0) + 0.5
+    # one giant segment spanning many tiles
+    giant = np.stack([np.zeros(n, np.uint32), (np.arange(n) % 200).astype(np.uint32),
+                      (np.arange(n) // 200).astype(np.uint32)])
+    _check(F, (3, 200, 100), giant, v, 0, 32, T=32)
+    # all singleton segments (every nonzero its own row), plus empty rows
+    single = np.stack([(np.arange(n) * 2).astype(np.uint32), (np.arange(n) % 13).astype(np.uint32),
+                       (np.arange(n) % 5).astype(np.uint32)])
+    _check(F, (2 * n + 5, 13, 5), single, v, 0, 32, T=32)
+    # segment heads exactly on tile boundaries: every slice has exactly 64 nonzeros, T = 64
+    blk = np.stack([(np.arange(n) // 64).astype(np.uint32), (np.arange(n) % 64).astype(np.uint32),
+                    np.zeros(n, np.uint32)])
+    _check(F, (n // 64 + 1, 64, 1), blk, v, 0, 16, T=64)
+
+
+@pytest.mark.parametrize("shards", [2, 3, 8])
+def test_fake_multirank_shards(F, shards):
+    """Shard-boundary logic without NCCL: tile-aligned shards summed equal the whole."""
+    dims = (100, 900, 800)
+    idx, val = gen.coo(dims, 50000, (1.0, 0.5, 0.5), 37)
+    for mode in range(3):
+        _check(F, dims, idx, val, mode, 32, T=64, shards=shards)
+
+
+def test_deterministic_repeat(F):
+    """Stores + boundary-only atomics: repeated calls agree to the last bit except where
+    red.add ordering differs; rows fully owned by one tile are bitwise stable."""
+    dims = (2000, 300, 400)
+    idx, val = gen.coo(dims, 60000, None, 41)
+    fs = gen.factors(dims, 32, 42)
+    a = _run(F, dims, idx, val, 0, fs, 32)
+    b = _run(F, dims, idx, val, 0, fs, 32)
+    M, D = oracle.mttkrp(dims, idx, val, 0, fs)
+    assert_parity(a, M, D)
+    assert_parity(b, M, D)
+
+
+def test_nell2_shaped_full_size(F):
+    """BASELINE configs[1] at full size (76.9M nnz), R=32, every mode, launch configuration of
+    bench.py (T=256), compared element by element with the multi-threaded oracle."""
+    w = gen.WORKLOADS["nell2"]
+    idx, val = gen.coo(w.dims, w.nnz, w.alpha, w.seed)
+    import os
+    for mode in range(3):
+        fs = gen.factors(w.dims, 32, 7)
+        got = _run(F, w.dims, idx, val, mode, fs, 32, 256)
+        M, D = oracle.mttkrp(w.dims, idx, val, mode, fs, nthreads=os.cpu_count() or 8)
+        assert_parity(got, M, D, what=f"nell2 mode {mode}")
