@@ -22,6 +22,14 @@ fcoo_status comm_allreduce(fcoo_comm_t c, float* buf, size_t count, cudaStream_t
   return FCOO_OK;
 }
 
+fcoo_status comm_allreduce_f64(fcoo_comm_t c, double* buf, size_t count, cudaStream_t s) {
+  if (!c || c->nranks == 1) return FCOO_OK;
+  ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, s);
+  if (r != ncclSuccess) return fail(FCOO_ERR_NCCL, "ncclAllReduce(f64): %s", ncclGetErrorString(r));
+  count_launch();
+  return FCOO_OK;
+}
+
 }  // namespace fcoo
 
 extern "C" {

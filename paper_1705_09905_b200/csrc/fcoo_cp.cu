@@ -4,11 +4,13 @@
 // sharded); k_solve (one CTA): V = Hadamard_{m!=n} G_m, fp64 Cholesky, W = V^{-1}, falling back to
 // a Jacobi pseudo-inverse when V is not positive definite (reading Q14); k_apply: U_n = M W
 // (fp64 accumulation, fp32 store); k_gram_partial + k_gram_reduce: G_raw = U_n^T U_n (fp64,
-// deterministic two-stage sum); k_norm_stats: lambda = sqrt(diag G_raw), G_n = G_raw / (lambda
-// lambda^T); k_scale: U_n /= lambda (reading Q13).  After the last mode, k_inner_partial +
-// k_fit compute the fit from <X,Xhat> = sum_r lambda_r sum_i M(i,r) U_N(i,r) and
-// |Xhat|^2 = lambda^T (Hadamard G_m) lambda with no extra pass over X.  Every reduction has a
-// fixed order, so replicated ranks compute bit-identical factors from identical M.
+// deterministic two-stage sum); k_norm_stats: lambda = sqrt(diag G_raw); k_scale: U_n /= lambda
+// (reading Q13); then G_n = Gram of the stored normalised U_n.  After the last mode,
+// k_inner_partial + k_fit compute the fit from <X,Xhat> = sum_r lambda_r sum_i M(i,r) U_N(i,r)
+// and |Xhat|^2 = lambda^T (Hadamard G_m) lambda with no extra pass over X; the last mode's M is
+// accumulated in fp64 so the cancellation in |X|^2 + |Xhat|^2 - 2<X,Xhat> near fit = 1 does
+// not swamp the result.  Every reduction has a fixed order, so
+// replicated ranks compute bit-identical factors from identical M.
 // The paper runs the small matrix ops with CUBLAS on a second stream; here they are
 // microsecond-scale single-purpose kernels on the same stream.
 #include <math.h>
@@ -167,13 +169,14 @@ __global__ void k_solve(GramPtrs G, int order, int n, int R, double* __restrict_
 }
 
 // U[i, b] = sum_a M[i, a] W[a, b]  (fp64 accumulation)
-__global__ void k_apply(const float* __restrict__ M, const double* __restrict__ W, int64_t I, int R,
+template <class MT>
+__global__ void k_apply(const MT* __restrict__ M, const double* __restrict__ W, int64_t I, int R,
                         float* __restrict__ U) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= I * R) return;
   int64_t i = e / R;
   int b = (int)(e % R);
-  const float* m = M + i * R;
+  const MT* m = M + i * R;
   double s = 0.0;
   for (int a = 0; a < R; ++a) s += (double)m[a] * W[a * R + b];
   U[e] = (float)s;
@@ -201,19 +204,13 @@ __global__ void k_gram_reduce(const double* __restrict__ part, int nchunks, int 
   G[e] = s;
 }
 
-// lambda = sqrt(diag Graw); G = Graw / (lambda lambda^T) (0 where lambda == 0)
+// lambda = column 2-norms = sqrt(diag Graw)
 __global__ void k_norm_stats(const double* __restrict__ Graw, int R, double* __restrict__ lam,
-                             float* __restrict__ lam_f, double* __restrict__ G) {
+                             float* __restrict__ lam_f) {
   for (int r = threadIdx.x; r < R; r += blockDim.x) {
     double l = sqrt(Graw[r * R + r]);
     lam[r] = l;
     if (lam_f) lam_f[r] = (float)l;
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < R * R; e += blockDim.x) {
-    int a = e / R, b = e % R;
-    double d = lam[a] * lam[b];
-    G[e] = d > 0 ? Graw[e] / d : 0.0;
   }
 }
 
@@ -224,8 +221,8 @@ __global__ void k_scale(float* __restrict__ U, int64_t I, int R, const double* _
   if (l > 0) U[e] = (float)((double)U[e] / l);
 }
 
-// part[c] = sum_{i in chunk c} sum_r lambda_r M[i,r] U[i,r]
-__global__ void k_inner_partial(const float* __restrict__ M, const float* __restrict__ U,
+// part[c] = sum_{i in chunk c} sum_r lambda_r M[i,r] U[i,r]   (M accumulated in fp64)
+__global__ void k_inner_partial(const double* __restrict__ M, const float* __restrict__ U,
                                 const double* __restrict__ lam, int64_t I, int R, int64_t rows_per,
                                 double* __restrict__ part) {
   __shared__ double sh[kCT];
@@ -298,12 +295,13 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
   for (int m = 0; m < N; ++m) Imax = std::max(Imax, X->dims[m]);
   const int RR = R * R;
   const int64_t maxchunks = 256;
-  Buf M(&al, sizeof(float) * Imax * R, s), Gs(&al, sizeof(double) * N * RR, s), Graw(&al, sizeof(double) * RR, s);
+  Buf M(&al, sizeof(float) * Imax * R, s), M64(&al, sizeof(double) * X->dims[N - 1] * R, s);
+  Buf Gs(&al, sizeof(double) * N * RR, s), Graw(&al, sizeof(double) * RR, s);
   Buf A(&al, sizeof(double) * RR, s), Q(&al, sizeof(double) * RR, s), W(&al, sizeof(double) * RR, s);
   Buf lam(&al, sizeof(double) * R, s), part(&al, sizeof(double) * maxchunks * RR, s);
   Buf ipart(&al, sizeof(double) * maxchunks, s), xpart(&al, sizeof(double) * maxchunks, s);
   Buf fitd(&al, sizeof(double) * 2, s), status(&al, sizeof(int) * 2, s);
-  if (!M.ok() || !Gs.ok() || !Graw.ok() || !A.ok() || !Q.ok() || !W.ok() || !lam.ok() || !part.ok() || !ipart.ok() ||
+  if (!M.ok() || !M64.ok() || !Gs.ok() || !Graw.ok() || !A.ok() || !Q.ok() || !W.ok() || !lam.ok() || !part.ok() || !ipart.ok() ||
       !xpart.ok() || !fitd.ok() || !status.ok()) {
     cleanup();
     return fail(FCOO_ERR_OOM, "cp_als scratch");
@@ -336,26 +334,37 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
   for (; it < o->iters && !st; ++it) {
     for (int n = 0; n < N && !st; ++n) {
       const int64_t In = X->dims[n];
-      st = fcoo_mttkrp(H[n], factors, R, M.as<float>(), (void*)s);
+      const bool last = (n == N - 1);
+      // M = MTTKRP_n; the last mode accumulates in fp64 because the fit's <X, Xhat> is taken
+      // from it; all-reduced across ranks on sharded handles.
+      if (last) {
+        st = run_mttkrp_f64(H[n], factors, R, M64.as<double>(), s);
+        if (!st && o->comm && o->nranks > 1) st = comm_allreduce_f64(o->comm, M64.as<double>(), (size_t)In * R, s);
+      } else {
+        st = fcoo_mttkrp(H[n], factors, R, M.as<float>(), (void*)s);
+      }
       if (st) break;
       k_solve<<<1, kCT, 0, s>>>(gp, N, n, R, A.as<double>(), Q.as<double>(), W.as<double>(), status.as<int>());
       FCOO_LAUNCH_CHECK();
-      k_apply<<<nblk(In * R), kCT, 0, s>>>(M.as<float>(), W.as<double>(), In, R, factors[n]);
+      if (last) k_apply<double><<<nblk(In * R), kCT, 0, s>>>(M64.as<double>(), W.as<double>(), In, R, factors[n]);
+      else k_apply<float><<<nblk(In * R), kCT, 0, s>>>(M.as<float>(), W.as<double>(), In, R, factors[n]);
       FCOO_LAUNCH_CHECK();
       st = gram(factors[n], In, Graw.as<double>());
       if (st) break;
-      k_norm_stats<<<1, kCT, 0, s>>>(Graw.as<double>(), R, lam.as<double>(), lambda,
-                                     Gs.as<double>() + (int64_t)n * RR);
+      k_norm_stats<<<1, kCT, 0, s>>>(Graw.as<double>(), R, lam.as<double>(), lambda);
       FCOO_LAUNCH_CHECK();
       k_scale<<<nblk(In * R), kCT, 0, s>>>(factors[n], In, R, lam.as<double>());
       FCOO_LAUNCH_CHECK();
+      // Gram of the STORED (normalised, fp32) factor, so |Xhat|^2 and V describe exactly the
+      // model held in memory
+      st = gram(factors[n], In, Gs.as<double>() + (int64_t)n * RR);
     }
     if (st) break;
     const int nl = N - 1;
     const int64_t Il = X->dims[nl];
     int nc = chunks_for(Il);
     int64_t per = (Il + nc - 1) / nc;
-    k_inner_partial<<<nc, kCT, 0, s>>>(M.as<float>(), factors[nl], lam.as<double>(), Il, R, per, ipart.as<double>());
+    k_inner_partial<<<nc, kCT, 0, s>>>(M64.as<double>(), factors[nl], lam.as<double>(), Il, R, per, ipart.as<double>());
     FCOO_LAUNCH_CHECK();
     k_fit<<<1, kCT, 0, s>>>(ipart.as<double>(), nc, xpart.as<double>(), nx, gp, N, lam.as<double>(), R,
                             fitd.as<double>());

@@ -30,7 +30,7 @@ struct EngineParams {
   const uint32_t* seg_coord;       // row of segment s = seg_coord[s]; nullptr -> row = s
   int64_t nnz, ntiles, tile_begin, tile_end;
   int T, R;
-  float* out;
+  void* out;  // float* (fp32 accumulation) or double* (fp64 accumulation)
 };
 
 // Streaming loads of the read-once F-COO arrays: read-only path, no L1 allocation (L1 is kept
@@ -82,37 +82,101 @@ __device__ __forceinline__ void red_add_v4(float* p, float4 v) {
                : "memory");
 }
 
+// Per-lane column slot: VEC consecutive fp32 factor entries (float4 on the vector path) and an
+// accumulator of type ACC (fp32 for the product path; fp64 for the CP-ALS fit mode, where the
+// identity-based fit needs the inner product <X, Xhat> to ~1e-12).
 template <int VEC>
-struct Vec;
+struct Ld;
 template <>
-struct Vec<4> {
+struct Ld<4> {
   using T = float4;
   static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
   static __device__ __forceinline__ T load(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-  static __device__ __forceinline__ T mul(T a, T b) { return make_float4(a.x * b.x, a.y * b.y, a.z * b.z, a.w * b.w); }
-  static __device__ __forceinline__ T fma(float s, T a, T c) {
-    return make_float4(fmaf(s, a.x, c.x), fmaf(s, a.y, c.y), fmaf(s, a.z, c.z), fmaf(s, a.w, c.w));
+};
+template <>
+struct Ld<1> {
+  using T = float;
+  static __device__ __forceinline__ T zero() { return 0.f; }
+  static __device__ __forceinline__ T load(const float* p) { return __ldg(p); }
+};
+
+struct d4 {
+  double x, y, z, w;
+};
+
+template <int VEC, class ACC>
+struct Acc;
+template <>
+struct Acc<4, float> {
+  using T = float4;
+  static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
+  template <int NP>
+  static __device__ __forceinline__ void add(T& acc, float v, const float4 (&r)[NP]) {
+    float4 h = r[0];
+#pragma unroll
+    for (int a = 1; a < NP; ++a) h = make_float4(h.x * r[a].x, h.y * r[a].y, h.z * r[a].z, h.w * r[a].w);
+    acc = make_float4(fmaf(v, h.x, acc.x), fmaf(v, h.y, acc.y), fmaf(v, h.z, acc.z), fmaf(v, h.w, acc.w));
   }
   static __device__ __forceinline__ void store(float* p, T v) { *reinterpret_cast<float4*>(p) = v; }
   static __device__ __forceinline__ void red(float* p, T v) { red_add_v4(p, v); }
 };
 template <>
-struct Vec<1> {
+struct Acc<1, float> {
   using T = float;
   static __device__ __forceinline__ T zero() { return 0.f; }
-  static __device__ __forceinline__ T load(const float* p) { return __ldg(p); }
-  static __device__ __forceinline__ T mul(T a, T b) { return a * b; }
-  static __device__ __forceinline__ T fma(float s, T a, T c) { return fmaf(s, a, c); }
+  template <int NP>
+  static __device__ __forceinline__ void add(T& acc, float v, const float (&r)[NP]) {
+    float h = r[0];
+#pragma unroll
+    for (int a = 1; a < NP; ++a) h *= r[a];
+    acc = fmaf(v, h, acc);
+  }
   static __device__ __forceinline__ void store(float* p, T v) { *p = v; }
   static __device__ __forceinline__ void red(float* p, T v) { atomicAdd(p, v); }
+};
+template <>
+struct Acc<4, double> {
+  using T = d4;
+  static __device__ __forceinline__ T zero() { return d4{0.0, 0.0, 0.0, 0.0}; }
+  template <int NP>
+  static __device__ __forceinline__ void add(T& acc, float v, const float4 (&r)[NP]) {
+    double hx = r[0].x, hy = r[0].y, hz = r[0].z, hw = r[0].w;
+#pragma unroll
+    for (int a = 1; a < NP; ++a) { hx *= (double)r[a].x; hy *= (double)r[a].y; hz *= (double)r[a].z; hw *= (double)r[a].w; }
+    double dv = v;
+    acc.x = fma(dv, hx, acc.x); acc.y = fma(dv, hy, acc.y); acc.z = fma(dv, hz, acc.z); acc.w = fma(dv, hw, acc.w);
+  }
+  static __device__ __forceinline__ void store(double* p, T v) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(v.x, v.y);
+    reinterpret_cast<double2*>(p)[1] = make_double2(v.z, v.w);
+  }
+  static __device__ __forceinline__ void red(double* p, T v) {
+    atomicAdd(p, v.x); atomicAdd(p + 1, v.y); atomicAdd(p + 2, v.z); atomicAdd(p + 3, v.w);
+  }
+};
+template <>
+struct Acc<1, double> {
+  using T = double;
+  static __device__ __forceinline__ T zero() { return 0.0; }
+  template <int NP>
+  static __device__ __forceinline__ void add(T& acc, float v, const float (&r)[NP]) {
+    double h = r[0];
+#pragma unroll
+    for (int a = 1; a < NP; ++a) h *= (double)r[a];
+    acc = fma((double)v, h, acc);
+  }
+  static __device__ __forceinline__ void store(double* p, T v) { *p = v; }
+  static __device__ __forceinline__ void red(double* p, T v) { atomicAdd(p, v); }
 };
 
 // NP product modes; G lanes per group (divides 32); VEC floats per lane per column slot;
 // CPL column slots per lane (lane gl covers columns (gl + G*c)*VEC .. +VEC-1, c < CPL).
-template <int NP, int G, int VEC, int CPL>
+template <int NP, int G, int VEC, int CPL, class ACC>
 __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
-  using V = Vec<VEC>;
+  using V = Ld<VEC>;
   using VT = typename V::T;
+  using A = Acc<VEC, ACC>;
+  using AT = typename A::T;
   constexpr int B = batch_size<NP, VEC, CPL>();  // nonzeros per batch (divides 32)
   const int gl = threadIdx.x % G;
   const int64_t t = P.tile_begin + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
@@ -135,17 +199,17 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
   if (left_open) row = P.seg_coord ? (int64_t)P.seg_coord[s] : s;
   bool own = false;  // did the current segment start inside this tile?
 
-  VT acc[CPL];
+  AT acc[CPL];
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) acc[c] = V::zero();
+  for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
 
   auto flush = [&](bool store) {
-    float* o = P.out + row * (int64_t)R;
+    ACC* o = reinterpret_cast<ACC*>(P.out) + row * (int64_t)R;
 #pragma unroll
     for (int c = 0; c < CPL; ++c)
       if (cok[c]) {
-        if (store) V::store(o + col[c], acc[c]);
-        else V::red(o + col[c], acc[c]);
+        if (store) A::store(o + col[c], acc[c]);
+        else A::red(o + col[c], acc[c]);
       }
   };
 
@@ -161,14 +225,14 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
     const uint32_t heads = (bfw >> ((pb - p0) & 31)) & ((1u << B) - 1u);
     const int nb = (int)min((int64_t)B, p1 - pb);  // < B only in the tensor's last tile
     // ---- gathers: all factor rows of the batch in flight together ----
-    VT rows[B][NP][CPL];
+    VT rows[B][CPL][NP];
 #pragma unroll
     for (int e = 0; e < B; ++e)
 #pragma unroll
       for (int a = 0; a < NP; ++a)
 #pragma unroll
         for (int c = 0; c < CPL; ++c)
-          rows[e][a][c] = (cok[c] && e < nb) ? V::load(P.U[a] + (int64_t)ix[a][e] * R + col[c]) : V::zero();
+          rows[e][c][a] = (cok[c] && e < nb) ? V::load(P.U[a] + (int64_t)ix[a][e] * R + col[c]) : V::zero();
     // ---- segmented accumulation ----
 #pragma unroll
     for (int e = 0; e < B; ++e) {
@@ -176,18 +240,13 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
         if ((heads >> e) & 1u) {
           if (pb + e != p0) flush(own);
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) acc[c] = V::zero();
+          for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
           own = true;
           ++s;
           row = P.seg_coord ? (int64_t)P.seg_coord[s] : s;
         }
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          VT h = rows[e][0][c];
-#pragma unroll
-          for (int a = 1; a < NP; ++a) h = V::mul(h, rows[e][a][c]);
-          acc[c] = V::fma(__uint_as_float(vb[e]), h, acc[c]);
-        }
+        for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), rows[e][c]);
       }
     }
   }
@@ -197,25 +256,26 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
 
 // Zero the output rows of segments that cross a tile boundary (they are combined by atomics);
 // every other row is written exactly once by a plain store.
+template <class ACC>
 __global__ void k_zero_boundary_rows(const uint32_t* __restrict__ sf, const uint32_t* __restrict__ seg_base,
                                      const uint32_t* __restrict__ seg_coord, int64_t tile_begin, int64_t tile_end,
-                                     int R, float* __restrict__ out) {
+                                     int R, ACC* __restrict__ out) {
   int64_t t = tile_begin + blockIdx.x;
   if (t >= tile_end) return;
-  // tile t's first segment is shared with the left neighbour iff sf[t] == 0
+  // tile t's first segment is shared with the left neighbour iff sf[t] == 0 (a segment that is
+  // right-open in tile t-1 is left-open in tile t, so checking the left side covers both)
   bool left_open = !((sf[t >> 5] >> (t & 31)) & 1u);
-  // tile t's last segment is shared with the right neighbour iff sf[t+1] == 0 (checked by t+1)
   if (!left_open) return;
   int64_t s = (int64_t)seg_base[t] - 1;
   int64_t row = seg_coord ? (int64_t)seg_coord[s] : s;
-  for (int c = threadIdx.x; c < R; c += blockDim.x) out[row * (int64_t)R + c] = 0.f;
+  for (int c = threadIdx.x; c < R; c += blockDim.x) out[row * (int64_t)R + c] = ACC(0);
 }
 
 namespace {
 
-template <int NP, int G, int VEC, int CPL>
+template <int NP, int G, int VEC, int CPL, class ACC>
 cudaError_t launch_one(const EngineParams& P, cudaStream_t s) {
-  auto kern = k_segreduce<NP, G, VEC, CPL>;
+  auto kern = k_segreduce<NP, G, VEC, CPL, ACC>;
   static bool configured = false;
   if (!configured) {  // no shared memory: give the whole unified carveout to L1 (factor rows)
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
@@ -231,63 +291,64 @@ cudaError_t launch_one(const EngineParams& P, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-template <int NP, int VEC, int CPL>
+template <int NP, int VEC, int CPL, class ACC>
 cudaError_t launch_g(const EngineParams& P, int G, cudaStream_t s) {
   switch (G) {
-    case 1: return launch_one<NP, 1, VEC, CPL>(P, s);
-    case 2: return launch_one<NP, 2, VEC, CPL>(P, s);
-    case 4: return launch_one<NP, 4, VEC, CPL>(P, s);
-    case 8: return launch_one<NP, 8, VEC, CPL>(P, s);
-    case 16: return launch_one<NP, 16, VEC, CPL>(P, s);
-    default: return launch_one<NP, 32, VEC, CPL>(P, s);
+    case 1: return launch_one<NP, 1, VEC, CPL, ACC>(P, s);
+    case 2: return launch_one<NP, 2, VEC, CPL, ACC>(P, s);
+    case 4: return launch_one<NP, 4, VEC, CPL, ACC>(P, s);
+    case 8: return launch_one<NP, 8, VEC, CPL, ACC>(P, s);
+    case 16: return launch_one<NP, 16, VEC, CPL, ACC>(P, s);
+    default: return launch_one<NP, 32, VEC, CPL, ACC>(P, s);
   }
 }
 
-template <int NP>
+template <int NP, class ACC>
 cudaError_t launch_np(const EngineParams& P, bool vec_ok, cudaStream_t s) {
   const int R = P.R;
   if (vec_ok) {  // float4 per lane: G = next pow2 of R/4 (<= 32)
     int q = R / 4, G = 1;
     while (G < q) G <<= 1;
-    return launch_g<NP, 4, 1>(P, G, s);
+    return launch_g<NP, 4, 1, ACC>(P, G, s);
   }
   if (R <= 32) {
     int G = 1;
     while (G < R) G <<= 1;
-    return launch_g<NP, 1, 1>(P, G, s);
+    return launch_g<NP, 1, 1, ACC>(P, G, s);
   }
   int cpl = (R + 31) / 32;
-  if (cpl <= 2) return launch_one<NP, 32, 1, 2>(P, s);
-  if (cpl <= 4) return launch_one<NP, 32, 1, 4>(P, s);
-  return launch_one<NP, 32, 1, 8>(P, s);
+  if (cpl <= 2) return launch_one<NP, 32, 1, 2, ACC>(P, s);
+  if (cpl <= 4) return launch_one<NP, 32, 1, 4, ACC>(P, s);
+  return launch_one<NP, 32, 1, 8, ACC>(P, s);
 }
 
+template <class ACC>
 cudaError_t launch_engine(const EngineParams& P, int NP, bool vec_ok, cudaStream_t s) {
   switch (NP) {
-    case 1: return launch_np<1>(P, vec_ok, s);
-    case 2: return launch_np<2>(P, vec_ok, s);
-    case 3: return launch_np<3>(P, vec_ok, s);
-    case 4: return launch_np<4>(P, vec_ok, s);
-    case 5: return launch_np<5>(P, vec_ok, s);
-    case 6: return launch_np<6>(P, vec_ok, s);
-    default: return launch_np<7>(P, vec_ok, s);
+    case 1: return launch_np<1, ACC>(P, vec_ok, s);
+    case 2: return launch_np<2, ACC>(P, vec_ok, s);
+    case 3: return launch_np<3, ACC>(P, vec_ok, s);
+    case 4: return launch_np<4, ACC>(P, vec_ok, s);
+    case 5: return launch_np<5, ACC>(P, vec_ok, s);
+    case 6: return launch_np<6, ACC>(P, vec_ok, s);
+    default: return launch_np<7, ACC>(P, vec_ok, s);
   }
 }
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-fcoo_status prepare_output(fcoo_s* f, int R, float* out, int64_t rows, bool all_rows_are_segments, cudaStream_t s) {
+template <class ACC>
+fcoo_status prepare_output(fcoo_s* f, int R, ACC* out, int64_t rows, bool all_rows_are_segments, cudaStream_t s) {
   bool whole = (f->tile_begin == 0 && f->tile_end == f->ntiles);
   if (!all_rows_are_segments || !whole) {
     // empty rows (or rows owned by other shards) must read 0
-    FCOO_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)(rows * R), s));
+    FCOO_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(ACC) * (size_t)(rows * R), s));
     return FCOO_OK;
   }
   int64_t nt = f->tile_end - f->tile_begin;
   if (nt > 0) {
-    k_zero_boundary_rows<<<(unsigned)nt, 64, 0, s>>>(f->sf, f->seg_base,
-                                                    f->op == FCOO_OP_MTTKRP && !f->dense_rows ? f->seg_coord : nullptr,
-                                                    f->tile_begin, f->tile_end, R, out);
+    k_zero_boundary_rows<ACC><<<(unsigned)nt, 64, 0, s>>>(f->sf, f->seg_base, nullptr, f->tile_begin, f->tile_end, R,
+                                                          out);
     FCOO_LAUNCH_CHECK();
   }
   return FCOO_OK;
@@ -295,9 +356,8 @@ fcoo_status prepare_output(fcoo_s* f, int R, float* out, int64_t rows, bool all_
 
 }  // namespace
 
-fcoo_status comm_allreduce(fcoo_comm_t comm, float* buf, size_t count, cudaStream_t s);
-
-fcoo_status run_mttkrp(fcoo_s* f, const float* const* factors, int R, float* out, cudaStream_t s) {
+template <class ACC>
+fcoo_status mttkrp_t(fcoo_s* f, const float* const* factors, int R, ACC* out, cudaStream_t s) {
   EngineParams P{};
   bool vec_ok = (R % 4 == 0) && R <= 128 && aligned16(out);
   for (int a = 0; a < f->n_prod; ++a) {
@@ -311,12 +371,24 @@ fcoo_status run_mttkrp(fcoo_s* f, const float* const* factors, int R, float* out
   P.seg_coord = f->dense_rows ? nullptr : f->seg_coord;
   P.nnz = f->nnz; P.ntiles = f->ntiles; P.tile_begin = f->tile_begin; P.tile_end = f->tile_end;
   P.T = (int)f->T; P.R = R; P.out = out;
-  fcoo_status st = prepare_output(f, R, out, f->dims[f->mode], f->dense_rows != 0, s);
+  // all rows are segments (dense_rows): only tile-crossing rows need zeroing
+  fcoo_status st = prepare_output<ACC>(f, R, out, f->dims[f->mode], f->dense_rows != 0, s);
   if (st) return st;
-  cudaError_t e = launch_engine(P, f->n_prod, vec_ok, s);
+  cudaError_t e = launch_engine<ACC>(P, f->n_prod, vec_ok, s);
   if (e != cudaSuccess) return fail(FCOO_ERR_CUDA, "mttkrp launch: %s", cudaGetErrorString(e));
+  return FCOO_OK;
+}
+
+fcoo_status run_mttkrp(fcoo_s* f, const float* const* factors, int R, float* out, cudaStream_t s) {
+  fcoo_status st = mttkrp_t<float>(f, factors, R, out, s);
+  if (st) return st;
   if (f->comm) return comm_allreduce(f->comm, out, (size_t)f->dims[f->mode] * R, s);
   return FCOO_OK;
+}
+
+// fp64-accumulating MTTKRP (CP-ALS fit mode); sharded handles return the LOCAL partial.
+fcoo_status run_mttkrp_f64(fcoo_s* f, const float* const* factors, int R, double* out, cudaStream_t s) {
+  return mttkrp_t<double>(f, factors, R, out, s);
 }
 
 fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s) {
@@ -328,9 +400,9 @@ fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s
   P.seg_coord = nullptr;  // output row = fibre (segment) ordinal
   P.nnz = f->nnz; P.ntiles = f->ntiles; P.tile_begin = f->tile_begin; P.tile_end = f->tile_end;
   P.T = (int)f->T; P.R = R; P.out = out;
-  fcoo_status st = prepare_output(f, R, out, f->nsegs, true, s);
+  fcoo_status st = prepare_output<float>(f, R, out, f->nsegs, true, s);
   if (st) return st;
-  cudaError_t e = launch_engine(P, 1, vec_ok, s);
+  cudaError_t e = launch_engine<float>(P, 1, vec_ok, s);
   if (e != cudaSuccess) return fail(FCOO_ERR_CUDA, "ttm launch: %s", cudaGetErrorString(e));
   if (f->comm) return comm_allreduce(f->comm, out, (size_t)f->nsegs * R, s);
   return FCOO_OK;

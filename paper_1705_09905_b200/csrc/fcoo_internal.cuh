@@ -73,6 +73,10 @@ struct fcoo_s {
 namespace fcoo {
 // engine entry points (fcoo_engine.cu)
 fcoo_status run_mttkrp(fcoo_s* f, const float* const* factors, int R, float* out, cudaStream_t s);
+fcoo_status run_mttkrp_f64(fcoo_s* f, const float* const* factors, int R, double* out, cudaStream_t s);
+// comm (fcoo_comm.cu)
+fcoo_status comm_allreduce(fcoo_comm_t comm, float* buf, size_t count, cudaStream_t s);
+fcoo_status comm_allreduce_f64(fcoo_comm_t comm, double* buf, size_t count, cudaStream_t s);
 fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s);
 }  // namespace fcoo
 
