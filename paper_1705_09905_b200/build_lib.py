@@ -14,7 +14,8 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libfcoo.so")
 OBJ = os.path.join(PKG, "build")
-SOURCES = ["fcoo_api.cu", "fcoo_build.cu", "fcoo_engine.cu", "fcoo_cp.cu", "fcoo_comm.cu"]
+SOURCES = ["fcoo_api.cu", "fcoo_build.cu", "fcoo_engine.cu", "fcoo_cp.cu", "fcoo_comm.cu"] + [
+    f"fcoo_engine_np{k}.cu" for k in range(1, 8)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -34,7 +35,8 @@ def _flags():
 def _compile(src: str) -> str:
     obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
     path = os.path.join(CSRC, src)
-    deps = [path, os.path.join(CSRC, "fcoo_internal.cuh"), os.path.join(ROOT, "include", "fcoo.h")]
+    deps = [path, os.path.join(ROOT, "include", "fcoo.h")] + [
+        os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".cuh")]
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj
     cmd = [NVCC] + _flags() + ["-c", path, "-o", obj]
@@ -51,7 +53,7 @@ def build(force: bool = False) -> str:
     if force:
         for f in os.listdir(OBJ):
             os.remove(os.path.join(OBJ, f))
-    with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
+    with cf.ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 4)) as ex:
         objs = list(ex.map(_compile, SOURCES))
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
         _, libdir = nccl_dirs()

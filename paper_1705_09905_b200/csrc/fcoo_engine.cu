@@ -1,258 +1,9 @@
-// fcoo_engine.cu — the one-shot, flag-driven segmented-reduction engine (§IV-C/D)
-// shared by SpMTTKRP (Eq.(6)) and SpTTM (Eq.(3)).
-//
-// Work decomposition: the nonzero stream is cut into tiles of T nonzeros
-// (T = "threadlen", the sf granularity).  A lane-group of G lanes owns one tile; its
-// lanes split the R columns (float4 per lane on the vector path), so a warp processes 32/G
-// tiles side by side.  A group walks its tile in batches of 8 nonzeros: it loads 8 product
-// indices per product mode and 8 values (128-bit loads, broadcast within the group), issues all
-// factor-row gathers of the batch, then forms v * Hadamard(rows) and accumulates in registers.
-// A set bf bit (segment head) closes the running segment: a segment that started inside the
-// tile and ends inside it is STORED (no atomics, the common case); the at most two segments a
-// tile shares with its neighbours (left-open when sf[t] == 0, right-open when sf[t+1] == 0) are
-// combined with red.global.add.v4.f32 — "boundary-only atomics" (north_star).
-// This replaces the paper's Titan-X adjacent-synchronisation carry chain.
-#include <stdarg.h>
-
-#include "fcoo_internal.cuh"
+// fcoo_engine.cu — host side of the segmented-reduction engine (see fcoo_engine_kernels.cuh):
+// output preparation, kernel dispatch by (product-mode count, rank, accumulator type), and the
+// SpMTTKRP / SpTTM entry points behind the C ABI.
+#include "fcoo_engine.cuh"
 
 namespace fcoo {
-
-constexpr int kMaxProd = kMaxOrder - 1;
-
-struct EngineParams {
-  const uint32_t* pidx[kMaxProd];  // product index arrays, row stride nnz_pad
-  const float* U[kMaxProd];        // factor matrix for product position a (I x R, row-major)
-  const float* val;
-  const uint32_t* bf;
-  const uint32_t* sf;
-  const uint32_t* seg_base;
-  const uint32_t* seg_coord;       // row of segment s = seg_coord[s]; nullptr -> row = s
-  int64_t nnz, ntiles, tile_begin, tile_end;
-  int T, R;
-  void* out;  // float* (fp32 accumulation) or double* (fp64 accumulation)
-};
-
-// Streaming loads of the read-once F-COO arrays: read-only path, no L1 allocation (L1 is kept
-// for the gathered factor rows, "read-only data cache").
-__device__ __forceinline__ uint4 ld_stream16(const void* p) {
-  uint4 r;
-  asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-      : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-      : "l"(p));
-  return r;
-}
-__device__ __forceinline__ uint2 ld_stream8(const void* p) {
-  uint2 r;
-  asm("ld.global.nc.L1::no_allocate.v2.u32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-  return r;
-}
-__device__ __forceinline__ uint32_t ld_stream4(const void* p) {
-  uint32_t r;
-  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(r) : "l"(p));
-  return r;
-}
-
-// B consecutive 32-bit words starting at a B*4-byte aligned address.
-template <int B>
-__device__ __forceinline__ void ld_batch(const void* p, uint32_t (&w)[B]) {
-  if constexpr (B == 8) {
-    uint4 lo = ld_stream16(p), hi = ld_stream16(reinterpret_cast<const uint32_t*>(p) + 4);
-    w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w; w[4] = hi.x; w[5] = hi.y; w[6] = hi.z; w[7] = hi.w;
-  } else if constexpr (B == 4) {
-    uint4 q = ld_stream16(p);
-    w[0] = q.x; w[1] = q.y; w[2] = q.z; w[3] = q.w;
-  } else if constexpr (B == 2) {
-    uint2 q = ld_stream8(p);
-    w[0] = q.x; w[1] = q.y;
-  } else {
-    w[0] = ld_stream4(p);
-  }
-}
-
-// Nonzeros per batch: keep the batch's gathered rows within ~64 registers.
-template <int NP, int VEC, int CPL>
-constexpr int batch_size() {
-  constexpr int regs = NP * VEC * CPL;
-  return regs * 8 <= 64 ? 8 : regs * 4 <= 64 ? 4 : regs * 2 <= 64 ? 2 : 1;
-}
-
-__device__ __forceinline__ void red_add_v4(float* p, float4 v) {
-  asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
-               : "memory");
-}
-
-// Per-lane column slot: VEC consecutive fp32 factor entries (float4 on the vector path) and an
-// accumulator of type ACC (fp32 for the product path; fp64 for the CP-ALS fit mode, where the
-// identity-based fit needs the inner product <X, Xhat> to ~1e-12).
-template <int VEC>
-struct Ld;
-template <>
-struct Ld<4> {
-  using T = float4;
-  static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
-  static __device__ __forceinline__ T load(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-};
-template <>
-struct Ld<1> {
-  using T = float;
-  static __device__ __forceinline__ T zero() { return 0.f; }
-  static __device__ __forceinline__ T load(const float* p) { return __ldg(p); }
-};
-
-struct d4 {
-  double x, y, z, w;
-};
-
-template <int VEC, class ACC>
-struct Acc;
-template <>
-struct Acc<4, float> {
-  using T = float4;
-  static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
-  template <int NP>
-  static __device__ __forceinline__ void add(T& acc, float v, const float4 (&r)[NP]) {
-    float4 h = r[0];
-#pragma unroll
-    for (int a = 1; a < NP; ++a) h = make_float4(h.x * r[a].x, h.y * r[a].y, h.z * r[a].z, h.w * r[a].w);
-    acc = make_float4(fmaf(v, h.x, acc.x), fmaf(v, h.y, acc.y), fmaf(v, h.z, acc.z), fmaf(v, h.w, acc.w));
-  }
-  static __device__ __forceinline__ void store(float* p, T v) { *reinterpret_cast<float4*>(p) = v; }
-  static __device__ __forceinline__ void red(float* p, T v) { red_add_v4(p, v); }
-};
-template <>
-struct Acc<1, float> {
-  using T = float;
-  static __device__ __forceinline__ T zero() { return 0.f; }
-  template <int NP>
-  static __device__ __forceinline__ void add(T& acc, float v, const float (&r)[NP]) {
-    float h = r[0];
-#pragma unroll
-    for (int a = 1; a < NP; ++a) h *= r[a];
-    acc = fmaf(v, h, acc);
-  }
-  static __device__ __forceinline__ void store(float* p, T v) { *p = v; }
-  static __device__ __forceinline__ void red(float* p, T v) { atomicAdd(p, v); }
-};
-template <>
-struct Acc<4, double> {
-  using T = d4;
-  static __device__ __forceinline__ T zero() { return d4{0.0, 0.0, 0.0, 0.0}; }
-  template <int NP>
-  static __device__ __forceinline__ void add(T& acc, float v, const float4 (&r)[NP]) {
-    double hx = r[0].x, hy = r[0].y, hz = r[0].z, hw = r[0].w;
-#pragma unroll
-    for (int a = 1; a < NP; ++a) { hx *= (double)r[a].x; hy *= (double)r[a].y; hz *= (double)r[a].z; hw *= (double)r[a].w; }
-    double dv = v;
-    acc.x = fma(dv, hx, acc.x); acc.y = fma(dv, hy, acc.y); acc.z = fma(dv, hz, acc.z); acc.w = fma(dv, hw, acc.w);
-  }
-  static __device__ __forceinline__ void store(double* p, T v) {
-    reinterpret_cast<double2*>(p)[0] = make_double2(v.x, v.y);
-    reinterpret_cast<double2*>(p)[1] = make_double2(v.z, v.w);
-  }
-  static __device__ __forceinline__ void red(double* p, T v) {
-    atomicAdd(p, v.x); atomicAdd(p + 1, v.y); atomicAdd(p + 2, v.z); atomicAdd(p + 3, v.w);
-  }
-};
-template <>
-struct Acc<1, double> {
-  using T = double;
-  static __device__ __forceinline__ T zero() { return 0.0; }
-  template <int NP>
-  static __device__ __forceinline__ void add(T& acc, float v, const float (&r)[NP]) {
-    double h = r[0];
-#pragma unroll
-    for (int a = 1; a < NP; ++a) h *= (double)r[a];
-    acc = fma((double)v, h, acc);
-  }
-  static __device__ __forceinline__ void store(double* p, T v) { *p = v; }
-  static __device__ __forceinline__ void red(double* p, T v) { atomicAdd(p, v); }
-};
-
-// NP product modes; G lanes per group (divides 32); VEC floats per lane per column slot;
-// CPL column slots per lane (lane gl covers columns (gl + G*c)*VEC .. +VEC-1, c < CPL).
-template <int NP, int G, int VEC, int CPL, class ACC>
-__global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
-  using V = Ld<VEC>;
-  using VT = typename V::T;
-  using A = Acc<VEC, ACC>;
-  using AT = typename A::T;
-  constexpr int B = batch_size<NP, VEC, CPL>();  // nonzeros per batch (divides 32)
-  const int gl = threadIdx.x % G;
-  const int64_t t = P.tile_begin + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-  if (t >= P.tile_end) return;  // groups are lane-aligned: whole groups exit together
-
-  const int R = P.R;
-  int col[CPL];
-  bool cok[CPL];
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    col[c] = (gl + G * c) * VEC;
-    cok[c] = col[c] < R;
-  }
-  const int64_t p0 = t * (int64_t)P.T;
-  const int64_t p1 = min(p0 + (int64_t)P.T, P.nnz);
-
-  const bool left_open = !((P.sf[t >> 5] >> (t & 31)) & 1u);
-  int64_t s = (int64_t)P.seg_base[t] - 1;  // current segment ordinal (incremented at each head)
-  int64_t row = 0;
-  if (left_open) row = P.seg_coord ? (int64_t)P.seg_coord[s] : s;
-  bool own = false;  // did the current segment start inside this tile?
-
-  AT acc[CPL];
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
-
-  auto flush = [&](bool store) {
-    ACC* o = reinterpret_cast<ACC*>(P.out) + row * (int64_t)R;
-#pragma unroll
-    for (int c = 0; c < CPL; ++c)
-      if (cok[c]) {
-        if (store) A::store(o + col[c], acc[c]);
-        else A::red(o + col[c], acc[c]);
-      }
-  };
-
-  uint32_t bfw = 0;
-  for (int64_t pb = p0; pb < p1; pb += B) {
-    if (((pb - p0) & 31) == 0) bfw = ld_stream4(P.bf + (pb >> 5));
-    // ---- batch loads: indices and values (broadcast within the group) ----
-    uint32_t ix[NP][B];
-    uint32_t vb[B];
-#pragma unroll
-    for (int a = 0; a < NP; ++a) ld_batch<B>(P.pidx[a] + pb, ix[a]);
-    ld_batch<B>(P.val + pb, vb);
-    const uint32_t heads = (bfw >> ((pb - p0) & 31)) & ((1u << B) - 1u);
-    const int nb = (int)min((int64_t)B, p1 - pb);  // < B only in the tensor's last tile
-    // ---- gathers: all factor rows of the batch in flight together ----
-    VT rows[B][CPL][NP];
-#pragma unroll
-    for (int e = 0; e < B; ++e)
-#pragma unroll
-      for (int a = 0; a < NP; ++a)
-#pragma unroll
-        for (int c = 0; c < CPL; ++c)
-          rows[e][c][a] = (cok[c] && e < nb) ? V::load(P.U[a] + (int64_t)ix[a][e] * R + col[c]) : V::zero();
-    // ---- segmented accumulation ----
-#pragma unroll
-    for (int e = 0; e < B; ++e) {
-      if (e < nb) {
-        if ((heads >> e) & 1u) {
-          if (pb + e != p0) flush(own);
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
-          own = true;
-          ++s;
-          row = P.seg_coord ? (int64_t)P.seg_coord[s] : s;
-        }
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), rows[e][c]);
-      }
-    }
-  }
-  const bool right_open = (t + 1 < P.ntiles) && !((P.sf[(t + 1) >> 5] >> ((t + 1) & 31)) & 1u);
-  flush(own && !right_open);
-}
 
 // Zero the output rows of segments that cross a tile boundary (they are combined by atomics);
 // every other row is written exactly once by a plain store.
@@ -272,55 +23,6 @@ __global__ void k_zero_boundary_rows(const uint32_t* __restrict__ sf, const uint
 }
 
 namespace {
-
-template <int NP, int G, int VEC, int CPL, class ACC>
-cudaError_t launch_one(const EngineParams& P, cudaStream_t s) {
-  auto kern = k_segreduce<NP, G, VEC, CPL, ACC>;
-  static bool configured = false;
-  if (!configured) {  // no shared memory: give the whole unified carveout to L1 (factor rows)
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-    configured = true;
-  }
-  const int TB = 256;
-  int64_t groups = P.tile_end - P.tile_begin;
-  int64_t threads = groups * G;
-  unsigned blocks = (unsigned)((threads + TB - 1) / TB);
-  if (blocks == 0) return cudaSuccess;
-  kern<<<blocks, TB, 0, s>>>(P);
-  count_launch();
-  return cudaGetLastError();
-}
-
-template <int NP, int VEC, int CPL, class ACC>
-cudaError_t launch_g(const EngineParams& P, int G, cudaStream_t s) {
-  switch (G) {
-    case 1: return launch_one<NP, 1, VEC, CPL, ACC>(P, s);
-    case 2: return launch_one<NP, 2, VEC, CPL, ACC>(P, s);
-    case 4: return launch_one<NP, 4, VEC, CPL, ACC>(P, s);
-    case 8: return launch_one<NP, 8, VEC, CPL, ACC>(P, s);
-    case 16: return launch_one<NP, 16, VEC, CPL, ACC>(P, s);
-    default: return launch_one<NP, 32, VEC, CPL, ACC>(P, s);
-  }
-}
-
-template <int NP, class ACC>
-cudaError_t launch_np(const EngineParams& P, bool vec_ok, cudaStream_t s) {
-  const int R = P.R;
-  if (vec_ok) {  // float4 per lane: G = next pow2 of R/4 (<= 32)
-    int q = R / 4, G = 1;
-    while (G < q) G <<= 1;
-    return launch_g<NP, 4, 1, ACC>(P, G, s);
-  }
-  if (R <= 32) {
-    int G = 1;
-    while (G < R) G <<= 1;
-    return launch_g<NP, 1, 1, ACC>(P, G, s);
-  }
-  int cpl = (R + 31) / 32;
-  if (cpl <= 2) return launch_one<NP, 32, 1, 2, ACC>(P, s);
-  if (cpl <= 4) return launch_one<NP, 32, 1, 4, ACC>(P, s);
-  return launch_one<NP, 32, 1, 8, ACC>(P, s);
-}
 
 template <class ACC>
 cudaError_t launch_engine(const EngineParams& P, int NP, bool vec_ok, cudaStream_t s) {

@@ -1,0 +1,27 @@
+// fcoo_engine.cuh — declarations shared by the engine translation units.
+#pragma once
+#include "fcoo_internal.cuh"
+
+namespace fcoo {
+
+constexpr int kMaxProd = kMaxOrder - 1;
+
+struct EngineParams {
+  const uint32_t* pidx[kMaxProd];  // product index arrays, row stride nnz_pad
+  const float* U[kMaxProd];        // factor matrix for product position a (I x R, row-major)
+  const float* val;
+  const uint32_t* bf;
+  const uint32_t* sf;
+  const uint32_t* seg_base;
+  const uint32_t* seg_coord;       // row of segment s = seg_coord[s]; nullptr -> row = s
+  int64_t nnz, ntiles, tile_begin, tile_end;
+  int T, R;
+  void* out;  // float* (fp32 accumulation) or double* (fp64 accumulation)
+};
+
+// Launch the segmented-reduction kernel for NP product modes, accumulator type ACC (instantiated
+// in fcoo_engine_np<NP>.cu so the template instances compile in parallel).
+template <int NP, class ACC>
+cudaError_t launch_np(const EngineParams& P, bool vec_ok, cudaStream_t s);
+
+}  // namespace fcoo

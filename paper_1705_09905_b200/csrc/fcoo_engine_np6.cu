@@ -1,0 +1,7 @@
+// Instances of the engine kernels for 6 product mode(s).
+#include "fcoo_engine_kernels.cuh"
+
+namespace fcoo {
+template cudaError_t launch_np<6, float>(const EngineParams&, bool, cudaStream_t);
+template cudaError_t launch_np<6, double>(const EngineParams&, bool, cudaStream_t);
+}  // namespace fcoo
