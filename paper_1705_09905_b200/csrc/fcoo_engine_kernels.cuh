@@ -13,6 +13,8 @@
 // combined with red.global.add.v4.f32 — "boundary-only atomics" (north_star).
 // This replaces the paper's Titan-X adjacent-synchronisation carry chain.
 #pragma once
+#include <stdlib.h>
+
 #include "fcoo_engine.cuh"
 
 namespace fcoo {
@@ -101,6 +103,16 @@ struct Acc<4, float> {
     for (int a = 1; a < NP; ++a) h = make_float4(h.x * r[a].x, h.y * r[a].y, h.z * r[a].z, h.w * r[a].w);
     acc = make_float4(fmaf(v, h.x, acc.x), fmaf(v, h.y, acc.y), fmaf(v, h.z, acc.z), fmaf(v, h.w, acc.w));
   }
+  template <int NP>
+  static __device__ __forceinline__ void add_inner(T& t, float v, const float4 (&r)[NP]) {  // t += v*prod_{a>=1} r[a]
+    float4 h = r[1];
+#pragma unroll
+    for (int a = 2; a < NP; ++a) h = make_float4(h.x * r[a].x, h.y * r[a].y, h.z * r[a].z, h.w * r[a].w);
+    t = make_float4(fmaf(v, h.x, t.x), fmaf(v, h.y, t.y), fmaf(v, h.z, t.z), fmaf(v, h.w, t.w));
+  }
+  static __device__ __forceinline__ void fold(T& acc, const T& t, float4 r0) {  // acc += t * r0
+    acc = make_float4(fmaf(t.x, r0.x, acc.x), fmaf(t.y, r0.y, acc.y), fmaf(t.z, r0.z, acc.z), fmaf(t.w, r0.w, acc.w));
+  }
   static __device__ __forceinline__ void store(float* p, T v) { *reinterpret_cast<float4*>(p) = v; }
   static __device__ __forceinline__ void red(float* p, T v) { red_add_v4(p, v); }
 };
@@ -115,6 +127,14 @@ struct Acc<1, float> {
     for (int a = 1; a < NP; ++a) h *= r[a];
     acc = fmaf(v, h, acc);
   }
+  template <int NP>
+  static __device__ __forceinline__ void add_inner(T& t, float v, const float (&r)[NP]) {
+    float h = r[1];
+#pragma unroll
+    for (int a = 2; a < NP; ++a) h *= r[a];
+    t = fmaf(v, h, t);
+  }
+  static __device__ __forceinline__ void fold(T& acc, const T& t, float r0) { acc = fmaf(t, r0, acc); }
   static __device__ __forceinline__ void store(float* p, T v) { *p = v; }
   static __device__ __forceinline__ void red(float* p, T v) { atomicAdd(p, v); }
 };
@@ -129,6 +149,18 @@ struct Acc<4, double> {
     for (int a = 1; a < NP; ++a) { hx *= (double)r[a].x; hy *= (double)r[a].y; hz *= (double)r[a].z; hw *= (double)r[a].w; }
     double dv = v;
     acc.x = fma(dv, hx, acc.x); acc.y = fma(dv, hy, acc.y); acc.z = fma(dv, hz, acc.z); acc.w = fma(dv, hw, acc.w);
+  }
+  template <int NP>
+  static __device__ __forceinline__ void add_inner(T& t, float v, const float4 (&r)[NP]) {
+    double hx = r[1].x, hy = r[1].y, hz = r[1].z, hw = r[1].w;
+#pragma unroll
+    for (int a = 2; a < NP; ++a) { hx *= (double)r[a].x; hy *= (double)r[a].y; hz *= (double)r[a].z; hw *= (double)r[a].w; }
+    double dv = v;
+    t.x = fma(dv, hx, t.x); t.y = fma(dv, hy, t.y); t.z = fma(dv, hz, t.z); t.w = fma(dv, hw, t.w);
+  }
+  static __device__ __forceinline__ void fold(T& acc, const T& t, float4 r0) {
+    acc.x = fma(t.x, (double)r0.x, acc.x); acc.y = fma(t.y, (double)r0.y, acc.y);
+    acc.z = fma(t.z, (double)r0.z, acc.z); acc.w = fma(t.w, (double)r0.w, acc.w);
   }
   static __device__ __forceinline__ void store(double* p, T v) {
     reinterpret_cast<double2*>(p)[0] = make_double2(v.x, v.y);
@@ -149,6 +181,14 @@ struct Acc<1, double> {
     for (int a = 1; a < NP; ++a) h *= (double)r[a];
     acc = fma((double)v, h, acc);
   }
+  template <int NP>
+  static __device__ __forceinline__ void add_inner(T& t, float v, const float (&r)[NP]) {
+    double h = r[1];
+#pragma unroll
+    for (int a = 2; a < NP; ++a) h *= (double)r[a];
+    t = fma((double)v, h, t);
+  }
+  static __device__ __forceinline__ void fold(T& acc, const T& t, float r0) { acc = fma(t, (double)r0, acc); }
   static __device__ __forceinline__ void store(double* p, T v) { *p = v; }
   static __device__ __forceinline__ void red(double* p, T v) { atomicAdd(p, v); }
 };
@@ -273,15 +313,178 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
   flush(own && !right_open);
 }
 
+// Factored variant (NP >= 2): CSF-style reuse of the outer (first, sorted) product mode.  Within a
+// segment the nonzeros are ordered by the product modes (reading Q5), so consecutive nonzeros
+// often share the outer index j.  For such a run, acc += U_0(j,:) * sum_run v * prod_{a>=1} U_a:
+// the run accumulator t collects the inner products and is folded into acc (one FFMA per column)
+// when the outer index changes or a segment head arrives; the outer row is gathered once per run
+// instead of once per nonzero.  This is the "data reuse" the paper lists among its GPU
+// optimisations applied to the F-COO stream; same sum, regrouped (error bound
+// unchanged: |fl(sum) - sum| <= gamma_n * sum |contributions|).
+template <int NP, int G, int VEC, int CPL, class ACC, bool FULL>
+__global__ void __launch_bounds__(256) k_segreduce_fact(const EngineParams P) {
+  static_assert(NP >= 2, "factored variant needs an outer and an inner product mode");
+  using V = Ld<VEC>;
+  using VT = typename V::T;
+  using A = Acc<VEC, ACC>;
+  using AT = typename A::T;
+  constexpr int B = batch_size<NP, VEC, CPL>();
+  const int gl = threadIdx.x % G;
+  const int64_t t = P.tile_begin + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  if (t >= P.tile_end) return;
+
+  const int R = P.R;
+  const uint32_t rowb = (uint32_t)R * 4u;
+  int col[CPL];
+  bool cok[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    col[c] = (gl + G * c) * VEC;
+    cok[c] = FULL || col[c] < R;
+  }
+  const char* ub[NP][CPL];
+#pragma unroll
+  for (int a = 0; a < NP; ++a)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) ub[a][c] = reinterpret_cast<const char*>(P.U[a] + (cok[c] ? col[c] : 0));
+
+  const int64_t p0 = t * (int64_t)P.T;
+  const int64_t p1 = min(p0 + (int64_t)P.T, P.nnz);
+  const int64_t pfull = p0 + ((p1 - p0) / B) * B;
+
+  const bool left_open = !((P.sf[t >> 5] >> (t & 31)) & 1u);
+  int64_t s = (int64_t)P.seg_base[t] - 1;
+  int64_t row = 0;
+  if (left_open) row = P.seg_coord ? (int64_t)P.seg_coord[s] : s;
+  bool own = false;
+
+  AT acc[CPL], run[CPL];
+  VT bcur[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    acc[c] = A::zero();
+    run[c] = A::zero();
+    bcur[c] = V::zero();
+  }
+  uint32_t prev0 = 0xffffffffu;
+
+  auto flush = [&](bool store) {
+    ACC* o = reinterpret_cast<ACC*>(P.out) + row * (int64_t)R;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+      if (cok[c]) {
+        if (store) A::store(o + col[c], acc[c]);
+        else A::red(o + col[c], acc[c]);
+      }
+  };
+  auto open_segment = [&](int64_t p) {
+    if (p != p0) flush(own);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
+    own = true;
+    ++s;
+    row = P.seg_coord ? (int64_t)P.seg_coord[s] : s;
+  };
+
+  uint32_t bfw = 0;
+  for (int64_t pb = p0; pb < pfull; pb += B) {
+    if (((pb - p0) & 31) == 0) bfw = ld_stream4(P.bf + (pb >> 5));
+    uint32_t ix[NP][B];
+    uint32_t vb[B];
+#pragma unroll
+    for (int a = 0; a < NP; ++a) ld_batch<B>(P.pidx[a] + pb, ix[a]);
+    ld_batch<B>(P.val + pb, vb);
+    const uint32_t heads = (bfw >> ((pb - p0) & 31)) & ((1u << B) - 1u);
+    bool nr[B];  // a new run starts at e: outer index changes or a segment head
+#pragma unroll
+    for (int e = 0; e < B; ++e) nr[e] = (ix[0][e] != (e ? ix[0][e - 1] : prev0)) || ((heads >> e) & 1u);
+    prev0 = ix[0][B - 1];
+    VT r[B][CPL][NP];
+#pragma unroll
+    for (int e = 0; e < B; ++e)
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        r[e][c][0] = V::zero();
+        if (nr[e] && cok[c]) r[e][c][0] = V::load(reinterpret_cast<const float*>(ub[0][c] + (size_t)ix[0][e] * rowb));
+#pragma unroll
+        for (int a = 1; a < NP; ++a)
+          r[e][c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(ub[a][c] + (size_t)ix[a][e] * rowb)) : V::zero();
+      }
+#pragma unroll
+    for (int e = 0; e < B; ++e) {
+      if (nr[e]) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) {
+          A::fold(acc[c], run[c], bcur[c]);
+          run[c] = A::zero();
+        }
+      }
+      if (heads != 0 && ((heads >> e) & 1u)) open_segment(pb + e);
+      if (nr[e]) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) bcur[c] = r[e][c][0];
+      }
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) A::template add_inner<NP>(run[c], __uint_as_float(vb[e]), r[e][c]);
+    }
+  }
+  for (int64_t p = pfull; p < p1; ++p) {  // ragged tail of the last tile
+    if ((p & 31) == 0 || p == pfull) bfw = ld_stream4(P.bf + (p >> 5));
+    const bool head = (bfw >> (p & 31)) & 1u;
+    const float v = __uint_as_float(ld_stream4(P.val + p));
+    uint32_t i0 = ld_stream4(P.pidx[0] + p);
+    VT r1[CPL][NP];
+#pragma unroll
+    for (int a = 0; a < NP; ++a) {
+      uint32_t i = a ? ld_stream4(P.pidx[a] + p) : i0;
+#pragma unroll
+      for (int c = 0; c < CPL; ++c)
+        r1[c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(ub[a][c] + (size_t)i * rowb)) : V::zero();
+    }
+    if (head || i0 != prev0) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) {
+        A::fold(acc[c], run[c], bcur[c]);
+        run[c] = A::zero();
+        bcur[c] = r1[c][0];
+      }
+    }
+    prev0 = i0;
+    if (head) open_segment(p);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) A::template add_inner<NP>(run[c], v, r1[c]);
+  }
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) A::fold(acc[c], run[c], bcur[c]);
+  const bool right_open = (t + 1 < P.ntiles) && !((P.sf[(t + 1) >> 5] >> ((t + 1) & 31)) & 1u);
+  flush(own && !right_open);
+}
+
+// Engine variant (FCOO_ENGINE env var, read once): 0 = plain, 1 = factored outer mode (default).
+inline int engine_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FCOO_ENGINE");
+    v = e ? atoi(e) : 1;
+  }
+  return v;
+}
 
 template <int NP, int G, int VEC, int CPL, class ACC>
 cudaError_t launch_one(const EngineParams& P, cudaStream_t s) {
   const bool full = (P.R == G * VEC * CPL);
-  auto kern = full ? k_segreduce<NP, G, VEC, CPL, ACC, true> : k_segreduce<NP, G, VEC, CPL, ACC, false>;
-  static bool configured[2] = {false, false};
-  if (!configured[full]) {  // no shared memory: give the whole unified carveout to L1 (factor rows)
+  const bool fact = NP >= 2 && engine_variant() == 1;
+  void (*kern)(const EngineParams);
+  if constexpr (NP >= 2) {
+    if (fact) kern = full ? k_segreduce_fact<NP, G, VEC, CPL, ACC, true> : k_segreduce_fact<NP, G, VEC, CPL, ACC, false>;
+    else kern = full ? k_segreduce<NP, G, VEC, CPL, ACC, true> : k_segreduce<NP, G, VEC, CPL, ACC, false>;
+  } else {
+    kern = full ? k_segreduce<NP, G, VEC, CPL, ACC, true> : k_segreduce<NP, G, VEC, CPL, ACC, false>;
+  }
+  static bool configured[4] = {false, false, false, false};
+  if (!configured[full + 2 * fact]) {  // no shared memory: give the whole unified carveout to L1
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-    configured[full] = true;
+    configured[full + 2 * fact] = true;
   }
   const int TB = 256;
   int64_t groups = P.tile_end - P.tile_begin;

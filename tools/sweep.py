@@ -1,0 +1,65 @@
+"""Quick per-(R, mode) timing sweep of fcoo_mttkrp on a workload (engine A/B experiments).
+
+FCOO_ENGINE=0|1 python tools/sweep.py [--workload nell2] [--R 16,32,64] [--tile 256]
+Prints one JSON line per (R, mode): ms (CUDA events, 10 reps after 2 warm-up), G nnz/s, %HBM.
+"""
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--workload", default="nell2")
+    ap.add_argument("--R", default="16,32,64")
+    ap.add_argument("--tile", type=int, default=256)
+    ap.add_argument("--reps", type=int, default=10)
+    ap.add_argument("--op", default="mttkrp")
+    a = ap.parse_args()
+    import torch
+
+    import gen
+    import paper_1705_09905_b200 as P
+    from bench import compulsory_bytes, hbm_peak
+    w, idx, val = gen.workload(a.workload)
+    coo = P.Coo.from_numpy(w.dims, idx, val)
+    N = len(w.dims)
+    nnz = val.shape[0]
+    peak, _ = hbm_peak()
+    for n in range(N):
+        h = P.fcoo_build(coo, n, op=P.OP_TTM if a.op == "ttm" else P.OP_MTTKRP, tile_nnz=a.tile)
+        for R in [int(x) for x in a.R.split(",")]:
+            fs = [torch.from_numpy(f).cuda() for f in gen.factors(w.dims, R, 7)]
+            rows = h.info.nsegs if a.op == "ttm" else w.dims[n]
+            out = torch.empty((rows, R), device="cuda")
+
+            def call():
+                if a.op == "ttm":
+                    P.fcoo_ttm(h, fs[n], R, out)
+                else:
+                    P.fcoo_mttkrp(h, fs, R, out)
+
+            for _ in range(2):
+                call()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record()
+            for _ in range(a.reps):
+                call()
+            e1.record()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / a.reps
+            b = compulsory_bytes(w.dims, nnz, n, R, a.tile)
+            print(json.dumps({"engine": os.environ.get("FCOO_ENGINE", "default"), "workload": a.workload,
+                              "op": a.op, "mode": n, "R": R, "tile": a.tile, "ms": round(ms, 4),
+                              "gnnz_s": round(nnz / ms / 1e6, 2), "hbm_frac": round(b / (ms / 1e3) / 1e9 / peak, 4)}),
+                  flush=True)
+        h.destroy()
+
+
+if __name__ == "__main__":
+    main()
