@@ -78,12 +78,34 @@ struct Ld<4> {
   using T = float4;
   static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
   static __device__ __forceinline__ T load(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+  // Predicated gather into fresh registers (opaque to the compiler, so it cannot fold the
+  // "keep the previous row" select into a chain of moves that waits on earlier loads).
+  static __device__ __forceinline__ T load_if(bool pred, const float* p) {
+    T r;
+    asm volatile(
+        "{ .reg .pred q; setp.ne.b32 q, %4, 0;\n"
+        "  mov.b32 %0, 0; mov.b32 %1, 0; mov.b32 %2, 0; mov.b32 %3, 0;\n"
+        "  @q ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%5]; }"
+        : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+        : "r"((int)pred), "l"(p));
+    return r;
+  }
 };
 template <>
 struct Ld<1> {
   using T = float;
   static __device__ __forceinline__ T zero() { return 0.f; }
   static __device__ __forceinline__ T load(const float* p) { return __ldg(p); }
+  static __device__ __forceinline__ T load_if(bool pred, const float* p) {
+    T r;
+    asm volatile(
+        "{ .reg .pred q; setp.ne.b32 q, %1, 0;\n"
+        "  mov.b32 %0, 0;\n"
+        "  @q ld.global.nc.f32 %0, [%2]; }"
+        : "=f"(r)
+        : "r"((int)pred), "l"(p));
+    return r;
+  }
 };
 
 struct d4 {
@@ -404,28 +426,42 @@ __global__ void __launch_bounds__(256) k_segreduce_fact(const EngineParams P) {
     for (int e = 0; e < B; ++e)
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
-        r[e][c][0] = V::zero();
-        if (nr[e] && cok[c]) r[e][c][0] = V::load(reinterpret_cast<const float*>(ub[0][c] + (size_t)ix[0][e] * rowb));
+        r[e][c][0] = V::load_if(nr[e] && cok[c], reinterpret_cast<const float*>(ub[0][c] + (size_t)ix[0][e] * rowb));
 #pragma unroll
         for (int a = 1; a < NP; ++a)
           r[e][c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(ub[a][c] + (size_t)ix[a][e] * rowb)) : V::zero();
       }
+    if (heads == 0) {  // common case: no segment boundary in the batch, straight-line code
 #pragma unroll
-    for (int e = 0; e < B; ++e) {
-      if (nr[e]) {
+      for (int e = 0; e < B; ++e) {
 #pragma unroll
         for (int c = 0; c < CPL; ++c) {
-          A::fold(acc[c], run[c], bcur[c]);
-          run[c] = A::zero();
+          if (nr[e]) {
+            A::fold(acc[c], run[c], bcur[c]);
+            run[c] = A::zero();
+            bcur[c] = r[e][c][0];
+          }
+          A::template add_inner<NP>(run[c], __uint_as_float(vb[e]), r[e][c]);
         }
       }
-      if (heads != 0 && ((heads >> e) & 1u)) open_segment(pb + e);
-      if (nr[e]) {
+    } else {
 #pragma unroll
-        for (int c = 0; c < CPL; ++c) bcur[c] = r[e][c][0];
+      for (int e = 0; e < B; ++e) {
+        if (nr[e]) {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            A::fold(acc[c], run[c], bcur[c]);
+            run[c] = A::zero();
+          }
+        }
+        if ((heads >> e) & 1u) open_segment(pb + e);
+        if (nr[e]) {
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) bcur[c] = r[e][c][0];
+        }
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) A::template add_inner<NP>(run[c], __uint_as_float(vb[e]), r[e][c]);
       }
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) A::template add_inner<NP>(run[c], __uint_as_float(vb[e]), r[e][c]);
     }
   }
   for (int64_t p = pfull; p < p1; ++p) {  // ragged tail of the last tile
