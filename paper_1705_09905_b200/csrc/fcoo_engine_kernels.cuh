@@ -496,12 +496,197 @@ __global__ void __launch_bounds__(256) k_segreduce_fact(const EngineParams P) {
   flush(own && !right_open);
 }
 
-// Engine variant (FCOO_ENGINE env var, read once): 0 = plain, 1 = factored outer mode (default).
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+  const uint32_t d = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+// B consecutive words from shared memory (broadcast within the group).
+template <int B>
+__device__ __forceinline__ void lds_batch(const uint32_t* p, uint32_t (&w)[B]) {
+  if constexpr (B == 8) {
+    uint4 lo = reinterpret_cast<const uint4*>(p)[0], hi = reinterpret_cast<const uint4*>(p)[1];
+    w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w; w[4] = hi.x; w[5] = hi.y; w[6] = hi.z; w[7] = hi.w;
+  } else if constexpr (B == 4) {
+    uint4 q = reinterpret_cast<const uint4*>(p)[0];
+    w[0] = q.x; w[1] = q.y; w[2] = q.z; w[3] = q.w;
+  } else if constexpr (B == 2) {
+    uint2 q = reinterpret_cast<const uint2*>(p)[0];
+    w[0] = q.x; w[1] = q.y;
+  } else {
+    w[0] = p[0];
+  }
+}
+
+// Shared-memory staging geometry of k_segreduce_staged: per lane-group, NST stages of one
+// 32-nonzero chunk each: NP index rows + the values + the bf word (16-byte padded); the
+// per-group stride is padded to 4 (mod 32) words so the groups of a warp hit distinct banks.
+template <int NP>
+struct Stage {
+  static constexpr int CH = 32;
+  static constexpr int NST = 2;
+  static constexpr int WORDS = (NP + 1) * CH + 4;
+  static constexpr int STRIDE_RAW = NST * WORDS;
+  static constexpr int STRIDE = STRIDE_RAW + ((4 - STRIDE_RAW % 32) + 32) % 32;
+};
+
+// Staged variant: the same segmented reduction, with the nonzero stream (indices, values, bf)
+// double-buffered through shared memory by cp.async (LDGSTS) one 32-nonzero chunk ahead, so the
+// HBM latency of the stream is off the critical path; only the L2-resident factor gathers remain
+// exposed.  This is the "shared-memory staging of the nonzero stream" of the north star; the
+// factor rows still go through L1 (most of the unified carveout stays L1).
+template <int NP, int G, int VEC, int CPL, class ACC, bool FULL>
+__global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) {
+  using V = Ld<VEC>;
+  using VT = typename V::T;
+  using A = Acc<VEC, ACC>;
+  using AT = typename A::T;
+  using S = Stage<NP>;
+  constexpr int B = batch_size<NP, VEC, CPL>();
+  constexpr int CH = S::CH;
+  extern __shared__ uint4 smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int gl = threadIdx.x % G;
+  const int64_t t = P.tile_begin + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  if (t >= P.tile_end) return;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
+  uint32_t* my = reinterpret_cast<uint32_t*>(smem_raw) + (threadIdx.x / G) * S::STRIDE;
+
+  const int R = P.R;
+  const uint32_t rowb = (uint32_t)R * 4u;
+  int col[CPL];
+  bool cok[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) {
+    col[c] = (gl + G * c) * VEC;
+    cok[c] = FULL || col[c] < R;
+  }
+  const char* ub[NP][CPL];
+#pragma unroll
+  for (int a = 0; a < NP; ++a)
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) ub[a][c] = reinterpret_cast<const char*>(P.U[a] + (cok[c] ? col[c] : 0));
+
+  const int64_t p0 = t * (int64_t)P.T;
+  const int64_t p1 = min(p0 + (int64_t)P.T, P.nnz);
+  const int nchunk = (int)((p1 - p0) / CH);  // full chunks (all of them except in the last tile)
+
+  const bool left_open = !((P.sf[t >> 5] >> (t & 31)) & 1u);
+  int64_t s = (int64_t)P.seg_base[t] - 1;
+  int64_t row = 0;
+  if (left_open) row = P.seg_coord ? (int64_t)P.seg_coord[s] : s;
+  bool own = false;
+
+  AT acc[CPL];
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
+  auto flush = [&](bool store) {
+    ACC* o = reinterpret_cast<ACC*>(P.out) + row * (int64_t)R;
+#pragma unroll
+    for (int c = 0; c < CPL; ++c)
+      if (cok[c]) {
+        if (store) A::store(o + col[c], acc[c]);
+        else A::red(o + col[c], acc[c]);
+      }
+  };
+  auto open_segment = [&](int64_t p) {
+    if (p != p0) flush(own);
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
+    own = true;
+    ++s;
+    row = P.seg_coord ? (int64_t)P.seg_coord[s] : s;
+  };
+  auto issue = [&](int64_t pc, int st) {  // group-cooperative copy of chunk [pc, pc+32) into stage st
+    uint32_t* dst = my + st * S::WORDS;
+#pragma unroll
+    for (int a = 0; a <= NP; ++a) {
+      const uint32_t* base = a < NP ? P.pidx[a] : reinterpret_cast<const uint32_t*>(P.val);
+#pragma unroll
+      for (int k = 0; k < (8 + G - 1) / G; ++k) {
+        const int q = gl + k * G;
+        if (q < 8) cp_async16(dst + a * CH + q * 4, base + pc + q * 4);
+      }
+    }
+    if (gl == 0) cp_async4(dst + (NP + 1) * CH, P.bf + (pc >> 5));
+  };
+
+  if (nchunk > 0) issue(p0, 0);
+  cp_async_commit();
+  for (int ci = 0; ci < nchunk; ++ci) {
+    if (ci + 1 < nchunk) issue(p0 + (int64_t)(ci + 1) * CH, (ci + 1) & 1);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncwarp(gmask);
+    const uint32_t* stg = my + (ci & 1) * S::WORDS;
+    const uint32_t bfw = stg[(NP + 1) * CH];
+#pragma unroll
+    for (int bi = 0; bi < CH / B; ++bi) {
+      const int64_t pb = p0 + (int64_t)ci * CH + bi * B;
+      uint32_t ix[NP][B];
+      uint32_t vb[B];
+#pragma unroll
+      for (int a = 0; a < NP; ++a) lds_batch<B>(stg + a * CH + bi * B, ix[a]);
+      lds_batch<B>(stg + NP * CH + bi * B, vb);
+      const uint32_t heads = (bfw >> (bi * B)) & ((1u << B) - 1u);
+      VT r[B][CPL][NP];
+#pragma unroll
+      for (int e = 0; e < B; ++e)
+#pragma unroll
+        for (int a = 0; a < NP; ++a)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c)
+            r[e][c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(ub[a][c] + (size_t)ix[a][e] * rowb)) : V::zero();
+      if (heads == 0) {
+#pragma unroll
+        for (int e = 0; e < B; ++e)
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), r[e][c]);
+      } else {
+#pragma unroll
+        for (int e = 0; e < B; ++e) {
+          if ((heads >> e) & 1u) open_segment(pb + e);
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), r[e][c]);
+        }
+      }
+    }
+    __syncwarp(gmask);  // every lane is done with this stage before it is refilled
+  }
+  uint32_t bfw = 0;
+  for (int64_t p = p0 + (int64_t)nchunk * CH; p < p1; ++p) {  // ragged tail of the last tile
+    if ((p & 31) == 0 || p == p0 + (int64_t)nchunk * CH) bfw = ld_stream4(P.bf + (p >> 5));
+    if ((bfw >> (p & 31)) & 1u) open_segment(p);
+    const float v = __uint_as_float(ld_stream4(P.val + p));
+    VT r1[CPL][NP];
+#pragma unroll
+    for (int a = 0; a < NP; ++a) {
+      uint32_t i = ld_stream4(P.pidx[a] + p);
+#pragma unroll
+      for (int c = 0; c < CPL; ++c)
+        r1[c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(ub[a][c] + (size_t)i * rowb)) : V::zero();
+    }
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], v, r1[c]);
+  }
+  const bool right_open = (t + 1 < P.ntiles) && !((P.sf[(t + 1) >> 5] >> ((t + 1) & 31)) & 1u);
+  flush(own && !right_open);
+}
+
+// Engine variant (FCOO_ENGINE env var, read once): 0 = plain, 1 = factored outer mode,
+// 2 = shared-memory-staged stream (default; used when a lane-group has >= 4 lanes).
 inline int engine_variant() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("FCOO_ENGINE");
-    v = e ? atoi(e) : 1;
+    v = e ? atoi(e) : 2;
   }
   return v;
 }
@@ -509,25 +694,38 @@ inline int engine_variant() {
 template <int NP, int G, int VEC, int CPL, class ACC>
 cudaError_t launch_one(const EngineParams& P, cudaStream_t s) {
   const bool full = (P.R == G * VEC * CPL);
-  const bool fact = NP >= 2 && engine_variant() == 1;
+  const int variant = engine_variant();
+  const bool fact = NP >= 2 && variant == 1;
+  const bool staged = variant == 2 && G >= 4;
+  const int TB = 256;
   void (*kern)(const EngineParams);
-  if constexpr (NP >= 2) {
+  size_t smem = 0;
+  if (staged) {
+    kern = full ? k_segreduce_staged<NP, G, VEC, CPL, ACC, true> : k_segreduce_staged<NP, G, VEC, CPL, ACC, false>;
+    smem = sizeof(uint32_t) * (size_t)(TB / G) * Stage<NP>::STRIDE;
+  } else if constexpr (NP >= 2) {
     if (fact) kern = full ? k_segreduce_fact<NP, G, VEC, CPL, ACC, true> : k_segreduce_fact<NP, G, VEC, CPL, ACC, false>;
     else kern = full ? k_segreduce<NP, G, VEC, CPL, ACC, true> : k_segreduce<NP, G, VEC, CPL, ACC, false>;
   } else {
     kern = full ? k_segreduce<NP, G, VEC, CPL, ACC, true> : k_segreduce<NP, G, VEC, CPL, ACC, false>;
   }
-  static bool configured[4] = {false, false, false, false};
-  if (!configured[full + 2 * fact]) {  // no shared memory: give the whole unified carveout to L1
-    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
-    configured[full + 2 * fact] = true;
+  static bool configured[2][3] = {{false, false, false}, {false, false, false}};
+  const int ci = staged ? 2 : fact ? 1 : 0;
+  if (!configured[full][ci]) {
+    if (staged) {  // small staging buffers: ask for just enough carveout, keep the rest as L1
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      int pct = (int)((2 * smem * 100 + 228 * 1024 - 1) / (228 * 1024)) + 1;
+      cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
+    } else {  // no shared memory: give the whole unified carveout to L1 (factor rows)
+      cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
+    }
+    configured[full][ci] = true;
   }
-  const int TB = 256;
   int64_t groups = P.tile_end - P.tile_begin;
   int64_t threads = groups * G;
   unsigned blocks = (unsigned)((threads + TB - 1) / TB);
   if (blocks == 0) return cudaSuccess;
-  kern<<<blocks, TB, 0, s>>>(P);
+  kern<<<blocks, TB, smem, s>>>(P);
   count_launch();
   return cudaGetLastError();
 }
