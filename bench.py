@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--impl", default="fcoo", choices=["fcoo", "reference"])
     ap.add_argument("--workload", default="nell2")
     ap.add_argument("--R", type=int, default=32)
-    ap.add_argument("--tile", type=int, default=256)
+    ap.add_argument("--tile", type=int, default=2048)
     ap.add_argument("--nnz", type=int, default=None, help="override nnz (debug only; not a bench number)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")

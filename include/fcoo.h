@@ -70,7 +70,7 @@ typedef struct {
 
 #define FCOO_BUILD_KEEP_PERM 1u /* keep the sorted->input permutation for fcoo_export */
 
-/* Build options.  NULL -> {FCOO_OP_MTTKRP, 256, 0}.
+/* Build options.  NULL -> {FCOO_OP_MTTKRP, 2048, 0}.
  * tile_nnz = T, the partition length ("threadlen", P:L272 / P:L426): a multiple of 32 in
  * [32, 8192].  sf has one bit per tile; one GPU lane-group processes one tile. */
 typedef struct {
@@ -177,6 +177,10 @@ fcoo_status fcoo_allreduce_sum(fcoo_comm_t comm, float* buf, size_t count, void*
  * nshards == 1 restores the whole handle. */
 fcoo_status fcoo_set_shard(fcoo_t f, int shard, int nshards, fcoo_comm_t comm);
 
+/* fcoo_shard_range — the tile range fcoo_set_shard uses (pure host arithmetic, no device):
+ * [*begin, *end) = [floor(shard*ntiles/nshards), floor((shard+1)*ntiles/nshards)). */
+fcoo_status fcoo_shard_range(int64_t ntiles, int shard, int nshards, int64_t* begin, int64_t* end);
+
 /* ---- CP-ALS (Algorithm 1, generalised to order N) ----
  * Per iteration, for n = 0..N-1: M = MTTKRP_n (fcoo_mttkrp, one F-COO handle per mode built up
  * front); V = Hadamard_{m != n} U_m^T U_m (fp64); U_n = M V^{-1} (fp64 Cholesky, with a
@@ -191,7 +195,7 @@ typedef struct {
   int R;            /* 1..256 */
   int iters;        /* >= 1 */
   double tol;       /* 0 = run all iterations */
-  int tile_nnz;     /* 0 -> 256 */
+  int tile_nnz;     /* 0 -> 2048 */
   fcoo_comm_t comm; /* NULL = single GPU */
   int rank, nranks; /* shard of this process (ignored when comm == NULL) */
 } fcoo_cp_opts;

@@ -143,12 +143,23 @@ fcoo_status fcoo_destroy(fcoo_t f) {
   return FCOO_OK;
 }
 
+fcoo_status fcoo_shard_range(int64_t ntiles, int shard, int nshards, int64_t* begin, int64_t* end) {
+  if (!begin || !end || ntiles < 0 || nshards < 1 || shard < 0 || shard >= nshards)
+    return fcoo::fail(FCOO_ERR_ARG, "bad shard %d/%d of %lld tiles", shard, nshards, (long long)ntiles);
+  *begin = ntiles * shard / nshards;
+  *end = ntiles * (shard + 1) / nshards;
+  return FCOO_OK;
+}
+
 fcoo_status fcoo_set_shard(fcoo_t f, int shard, int nshards, fcoo_comm_t comm) {
-  if (!f || nshards < 1 || shard < 0 || shard >= nshards) return fcoo::fail(FCOO_ERR_ARG, "bad shard %d/%d", shard, nshards);
+  if (!f) return fcoo::fail(FCOO_ERR_ARG, "NULL handle");
+  int64_t b = 0, e = 0;
+  fcoo_status st = fcoo_shard_range(f->ntiles, shard, nshards, &b, &e);
+  if (st) return st;
   f->shard = shard;
   f->nshards = nshards;
-  f->tile_begin = f->ntiles * shard / nshards;
-  f->tile_end = f->ntiles * (shard + 1) / nshards;
+  f->tile_begin = b;
+  f->tile_end = e;
   f->comm = nshards > 1 ? comm : nullptr;
   return FCOO_OK;
 }

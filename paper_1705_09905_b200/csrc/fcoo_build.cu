@@ -183,7 +183,7 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
   if (!coo || !out) return fail(FCOO_ERR_ARG, "NULL coo/out");
   *out = nullptr;
   int op = opts ? opts->op : FCOO_OP_MTTKRP;
-  int T = opts ? opts->tile_nnz : 256;
+  int T = opts ? opts->tile_nnz : 2048;
   unsigned flags = opts ? opts->flags : 0u;
   if (T < 32 || T > 8192 || (T % 32) != 0) return fail(FCOO_ERR_ARG, "tile_nnz %d must be a multiple of 32 in [32,8192]", T);
   if (!coo->dims || !coo->idx || !coo->val) return fail(FCOO_ERR_ARG, "NULL dims/idx/val");

@@ -70,7 +70,7 @@ class _CpOpts(ctypes.Structure):
 # The exported symbols (every one declared in include/fcoo.h).
 SYMBOLS = ["fcoo_build", "fcoo_mttkrp", "fcoo_ttm", "fcoo_info", "fcoo_export", "fcoo_destroy",
            "fcoo_comm_unique_id", "fcoo_comm_init", "fcoo_comm_destroy", "fcoo_allreduce_sum", "fcoo_set_shard",
-           "cp_als", "fcoo_status_str", "fcoo_last_error", "fcoo_launch_count"]
+           "fcoo_shard_range", "cp_als", "fcoo_status_str", "fcoo_last_error", "fcoo_launch_count"]
 
 _lib = None
 
@@ -96,6 +96,7 @@ def load_library():
     L.fcoo_comm_destroy.argtypes = [vp]
     L.fcoo_allreduce_sum.argtypes = [vp, vp, ctypes.c_size_t, vp]
     L.fcoo_set_shard.argtypes = [vp, ci, ci, vp]
+    L.fcoo_shard_range.argtypes = [i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.cp_als.argtypes = [ctypes.POINTER(_Coo), ctypes.POINTER(_CpOpts), ctypes.POINTER(vp), vp,
                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ci), ctypes.POINTER(_Allocator), vp]
     L.fcoo_status_str.restype = ctypes.c_char_p
@@ -238,7 +239,7 @@ class Fcoo:
             pass
 
 
-def fcoo_build(coo: Coo, mode: int, op: int = OP_MTTKRP, tile_nnz: int = 256, keep_perm: bool = False,
+def fcoo_build(coo: Coo, mode: int, op: int = OP_MTTKRP, tile_nnz: int = 2048, keep_perm: bool = False,
                stream=None) -> Fcoo:
     L = load_library()
     opts = _BuildOpts(op, tile_nnz, BUILD_KEEP_PERM if keep_perm else 0)
@@ -333,12 +334,20 @@ def fcoo_allreduce_sum(comm: Comm, buf: torch.Tensor, stream=None):
                                              ctypes.c_void_p(_stream_ptr(stream))), "fcoo_allreduce_sum")
 
 
+def fcoo_shard_range(ntiles: int, shard: int, nshards: int):
+    """Tile range [begin, end) of shard `shard` (host arithmetic in the library, no device)."""
+    b, e = ctypes.c_int64(0), ctypes.c_int64(0)
+    _check(load_library().fcoo_shard_range(ntiles, shard, nshards, ctypes.byref(b), ctypes.byref(e)),
+           "fcoo_shard_range")
+    return b.value, e.value
+
+
 def fcoo_set_shard(f: Fcoo, shard: int, nshards: int, comm: Comm | None = None):
     _check(load_library().fcoo_set_shard(f.h, shard, nshards, comm.h if comm else None), "fcoo_set_shard")
     f.info = f._info()
 
 
-def cp_als(coo: Coo, R: int, iters: int, factors, tol: float = 0.0, tile_nnz: int = 256, comm: Comm | None = None,
+def cp_als(coo: Coo, R: int, iters: int, factors, tol: float = 0.0, tile_nnz: int = 2048, comm: Comm | None = None,
            stream=None):
     """In-place CP-ALS: `factors` (list of CUDA fp32 (I_m, R)) hold the initial factors and receive
     the result.  Returns (lambda CUDA fp32 (R,), fit_trace list)."""

@@ -121,12 +121,12 @@ def test_deterministic_repeat(F):
 
 def test_nell2_shaped_full_size(F):
     """BASELINE configs[1] at full size (76.9M nnz), R=32, every mode, launch configuration of
-    bench.py (T=256), compared element by element with the multi-threaded oracle."""
+    bench.py (T=2048), compared element by element with the multi-threaded oracle."""
     w = gen.WORKLOADS["nell2"]
     idx, val = gen.coo(w.dims, w.nnz, w.alpha, w.seed)
     import os
     for mode in range(3):
         fs = gen.factors(w.dims, 32, 7)
-        got = _run(F, w.dims, idx, val, mode, fs, 32, 256)
+        got = _run(F, w.dims, idx, val, mode, fs, 32, 2048)
         M, D = oracle.mttkrp(w.dims, idx, val, mode, fs, nthreads=os.cpu_count() or 8)
         assert_parity(got, M, D, what=f"nell2 mode {mode}")

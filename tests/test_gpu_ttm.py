@@ -76,4 +76,4 @@ def test_brainq_shaped_full_size(F):
     w = gen.WORKLOADS["brainq"]
     idx, val = gen.coo(w.dims, w.nnz, w.alpha, w.seed)
     for mode in range(3):
-        _check(F, w.dims, idx, val, mode, 16, T=256)
+        _check(F, w.dims, idx, val, mode, 16, T=2048)

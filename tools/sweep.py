@@ -16,7 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="nell2")
     ap.add_argument("--R", default="16,32,64")
-    ap.add_argument("--tile", type=int, default=256)
+    ap.add_argument("--tile", type=int, default=2048)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--op", default="mttkrp")
     a = ap.parse_args()
