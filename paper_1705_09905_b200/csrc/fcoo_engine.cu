@@ -6,20 +6,18 @@
 namespace fcoo {
 
 // Zero the output rows of segments that cross a tile boundary (they are combined by atomics);
-// every other row is written exactly once by a plain store.
+// every other row is written exactly once by a plain store.  One thread per tile t: the segment
+// seg_base[t]-1 crosses into t iff sf[t] == 0; it is zeroed only by the first tile it crosses
+// into, i.e. when its head lies in tile t-1 (seg_base[t-1] != seg_base[t]).
 template <class ACC>
 __global__ void k_zero_boundary_rows(const uint32_t* __restrict__ sf, const uint32_t* __restrict__ seg_base,
-                                     const uint32_t* __restrict__ seg_coord, int64_t tile_begin, int64_t tile_end,
-                                     int R, ACC* __restrict__ out) {
-  int64_t t = tile_begin + blockIdx.x;
-  if (t >= tile_end) return;
-  // tile t's first segment is shared with the left neighbour iff sf[t] == 0 (a segment that is
-  // right-open in tile t-1 is left-open in tile t, so checking the left side covers both)
-  bool left_open = !((sf[t >> 5] >> (t & 31)) & 1u);
-  if (!left_open) return;
-  int64_t s = (int64_t)seg_base[t] - 1;
-  int64_t row = seg_coord ? (int64_t)seg_coord[s] : s;
-  for (int c = threadIdx.x; c < R; c += blockDim.x) out[row * (int64_t)R + c] = ACC(0);
+                                     int64_t tile_begin, int64_t tile_end, int R, ACC* __restrict__ out) {
+  int64_t t = tile_begin + (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= tile_end || t == 0) return;
+  const bool left_open = !((sf[t >> 5] >> (t & 31)) & 1u);
+  if (!left_open || seg_base[t - 1] == seg_base[t]) return;
+  ACC* o = out + ((int64_t)seg_base[t] - 1) * R;
+  for (int c = 0; c < R; ++c) o[c] = ACC(0);
 }
 
 namespace {
@@ -48,9 +46,9 @@ fcoo_status prepare_output(fcoo_s* f, int R, ACC* out, int64_t rows, bool all_ro
     return FCOO_OK;
   }
   int64_t nt = f->tile_end - f->tile_begin;
-  if (nt > 0) {
-    k_zero_boundary_rows<ACC><<<(unsigned)nt, 64, 0, s>>>(f->sf, f->seg_base, nullptr, f->tile_begin, f->tile_end, R,
-                                                          out);
+  if (nt > 0) {  // rows are segment ordinals here (TTM, or MTTKRP with every slice non-empty)
+    k_zero_boundary_rows<ACC><<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(f->sf, f->seg_base, f->tile_begin,
+                                                                         f->tile_end, R, out);
     FCOO_LAUNCH_CHECK();
   }
   return FCOO_OK;
