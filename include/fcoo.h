@@ -69,6 +69,10 @@ typedef struct {
 } fcoo_allocator;
 
 #define FCOO_BUILD_KEEP_PERM 1u /* keep the sorted->input permutation for fcoo_export */
+/* Order the product modes of an MTTKRP handle by DESCENDING extent (ties by mode id) instead of
+ * the default ascending order of reading Q5: the last (per-nonzero random) product mode is then
+ * the smallest factor.  Same segments, same sum, another canonical permutation. */
+#define FCOO_BUILD_PRODUCT_DESC 2u
 
 /* Build options.  NULL -> {FCOO_OP_MTTKRP, 2048, 0}.
  * tile_nnz = T, the partition length ("threadlen", P:L272 / P:L426): a multiple of 32 in

@@ -45,6 +45,8 @@ def _load():
         L.orc_storage_bytes.restype = i64
         L.orc_storage_bytes.argtypes = [i64, ci, i64]
         L.orc_build.argtypes = [ci, vp, i64, vp, vp, ci, ci, i64, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_build_ex.argtypes = [ci, vp, i64, vp, vp, ci, ci, i64, ci, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_mode_spec_ex.argtypes = [ci, vp, ci, ci, ci, vp, vp, vp, vp]
         L.orc_mttkrp.argtypes = [ci, vp, i64, vp, vp, ci, vp, ci, vp, vp, ci]
         L.orc_ttm.argtypes = [ci, vp, i64, vp, vp, ci, vp, ci, vp, vp, vp, vp]
         L.orc_gram.argtypes = [i64, ci, vp, vp]
@@ -67,12 +69,13 @@ def _coo(dims, idx, val):
     return d, idx, val
 
 
-def mode_spec(dims, op: int, mode: int):
+def mode_spec(dims, op: int, mode: int, desc: bool = False):
     L = _load()
     d = np.ascontiguousarray(dims, dtype=np.int64)
     im, pm = np.zeros(8, np.int32), np.zeros(8, np.int32)
     ni, npr = ctypes.c_int(0), ctypes.c_int(0)
-    rc = L.orc_mode_spec(len(d), _ptr(d), op, mode, _ptr(im), ctypes.byref(ni), _ptr(pm), ctypes.byref(npr))
+    rc = L.orc_mode_spec_ex(len(d), _ptr(d), op, mode, int(desc), _ptr(im), ctypes.byref(ni), _ptr(pm),
+                            ctypes.byref(npr))
     if rc:
         raise OracleError(rc, "mode_spec")
     return list(im[: ni.value]), list(pm[: npr.value])
@@ -101,14 +104,14 @@ class Fcoo:
         return np.unpackbits(self.bf, bitorder="little")[: self.val.shape[0]]
 
 
-def build_fcoo(dims, idx, val, op: int, mode: int, T: int) -> Fcoo:
+def build_fcoo(dims, idx, val, op: int, mode: int, T: int, desc: bool = False) -> Fcoo:
     L = _load()
     d, idx, val = _coo(dims, idx, val)
     nnz = val.shape[0]
     order = len(d)
     if order < 2 or order > 8:
         raise OracleError(ERR_ORDER, "build")
-    im, pm = mode_spec(d, op, mode)
+    im, pm = mode_spec(d, op, mode, desc)
     ntiles = max(1, (nnz + T - 1) // T)
     perm = np.zeros(nnz, np.uint32)
     bf = np.zeros(max(1, (nnz + 7) // 8), np.uint8)
@@ -118,7 +121,7 @@ def build_fcoo(dims, idx, val, op: int, mode: int, T: int) -> Fcoo:
     pidx = np.zeros((len(pm), nnz), np.uint32)
     pval = np.zeros(nnz, np.float32)
     ns = ctypes.c_int64(0)
-    rc = L.orc_build(order, _ptr(d), nnz, _ptr(idx), _ptr(val), op, mode, T, _ptr(perm), _ptr(bf), _ptr(sf),
+    rc = L.orc_build_ex(order, _ptr(d), nnz, _ptr(idx), _ptr(val), op, mode, T, int(desc), _ptr(perm), _ptr(bf), _ptr(sf),
                      _ptr(seg_base), _ptr(seg_coord), _ptr(pidx), _ptr(pval), ctypes.byref(ns))
     if rc:
         raise OracleError(rc, "build")

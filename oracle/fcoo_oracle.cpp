@@ -53,8 +53,8 @@ enum { ORC_OP_MTTKRP = 0, ORC_OP_TTM = 1 };
  *   SpTTM on mode n:    product mode {n}; index modes = all others, ascending.
  *   Q5: product modes of MTTKRP ordered by ascending extent I_m, ties by mode id.
  * Writes index modes to idx_modes[0..n_idx), product modes to prod_modes[0..n_prod). */
-int orc_mode_spec(int order, const int64_t* dims, int op, int mode, int* idx_modes, int* n_idx, int* prod_modes,
-                  int* n_prod) {
+int orc_mode_spec_ex(int order, const int64_t* dims, int op, int mode, int desc, int* idx_modes, int* n_idx,
+                     int* prod_modes, int* n_prod) {
   if (order < 2 || order > 8) return ORC_ERR_ORDER;
   if (mode < 0 || mode >= order) return ORC_ERR_MODE;
   int ni = 0, np = 0;
@@ -62,9 +62,12 @@ int orc_mode_spec(int order, const int64_t* dims, int op, int mode, int* idx_mod
     idx_modes[ni++] = mode;
     for (int m = 0; m < order; ++m)
       if (m != mode) prod_modes[np++] = m;
-    /* Q5: ascending extent, ties by mode id (stable insertion sort) */
+    /* Q5: ascending extent, ties by mode id (stable insertion sort); desc != 0: the build
+     * option that orders the product modes by descending extent instead */
     for (int a = 1; a < np; ++a)
-      for (int b = a; b > 0 && dims[prod_modes[b]] < dims[prod_modes[b - 1]]; --b) std::swap(prod_modes[b], prod_modes[b - 1]);
+      for (int b = a; b > 0 && (desc ? dims[prod_modes[b]] > dims[prod_modes[b - 1]]
+                                     : dims[prod_modes[b]] < dims[prod_modes[b - 1]]); --b)
+        std::swap(prod_modes[b], prod_modes[b - 1]);
   } else if (op == ORC_OP_TTM) {
     for (int m = 0; m < order; ++m)
       if (m != mode) idx_modes[ni++] = m;
@@ -75,6 +78,11 @@ int orc_mode_spec(int order, const int64_t* dims, int op, int mode, int* idx_mod
   *n_idx = ni;
   *n_prod = np;
   return ORC_OK;
+}
+
+int orc_mode_spec(int order, const int64_t* dims, int op, int mode, int* idx_modes, int* n_idx, int* prod_modes,
+                  int* n_prod) {
+  return orc_mode_spec_ex(order, dims, op, mode, 0, idx_modes, n_idx, prod_modes, n_prod);
 }
 
 /* Table II generalised to |product modes| (Q17), S:L201:
@@ -99,11 +107,11 @@ int64_t orc_storage_bytes(int64_t nnz, int n_prod, int64_t T) {
  *   pval[nnz]             values in sorted order (bitwise copies)
  *   nsegs_out
  * Returns ORC_ERR_* on invalid input: ORDER, MODE, EMPTY (nnz==0), INDEX_RANGE, DUPLICATE (Q6). */
-int orc_build(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, const float* val, int op, int mode,
-              int64_t T, uint32_t* perm, uint8_t* bf, uint32_t* sf, uint32_t* seg_base, uint32_t* seg_coord,
-              uint32_t* pidx, float* pval, int64_t* nsegs_out) {
+int orc_build_ex(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, const float* val, int op, int mode,
+                 int64_t T, int desc, uint32_t* perm, uint8_t* bf, uint32_t* sf, uint32_t* seg_base,
+                 uint32_t* seg_coord, uint32_t* pidx, float* pval, int64_t* nsegs_out) {
   int idx_modes[8], prod_modes[8], n_idx = 0, n_prod = 0;
-  int rc = orc_mode_spec(order, dims, op, mode, idx_modes, &n_idx, prod_modes, &n_prod);
+  int rc = orc_mode_spec_ex(order, dims, op, mode, desc, idx_modes, &n_idx, prod_modes, &n_prod);
   if (rc) return rc;
   if (T < 1) return ORC_ERR_ARG;
   if (nnz <= 0) return ORC_ERR_EMPTY;
@@ -154,6 +162,13 @@ int orc_build(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, 
   }
   *nsegs_out = nsegs;
   return ORC_OK;
+}
+
+int orc_build(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, const float* val, int op, int mode,
+              int64_t T, uint32_t* perm, uint8_t* bf, uint32_t* sf, uint32_t* seg_base, uint32_t* seg_coord,
+              uint32_t* pidx, float* pval, int64_t* nsegs_out) {
+  return orc_build_ex(order, dims, nnz, idx, val, op, mode, T, 0, perm, bf, sf, seg_base, seg_coord, pidx, pval,
+                      nsegs_out);
 }
 
 /* ------------------------------------------------------------------------- */

@@ -153,7 +153,7 @@ void free_handle_arrays(fcoo_s* f) {
 }  // namespace
 
 // Host-side mode taxonomy (Table I) and key layout; used by fcoo_build.
-fcoo_status plan_modes(fcoo_s* f, int order, const int64_t* dims, int op, int mode) {
+fcoo_status plan_modes(fcoo_s* f, int order, const int64_t* dims, int op, int mode, bool desc = false) {
   if (order < 2 || order > kMaxOrder) return fail(FCOO_ERR_ORDER, "order %d outside [2,8]", order);
   if (mode < 0 || mode >= order) return fail(FCOO_ERR_MODE, "mode %d outside [0,%d)", mode, order);
   if (op != FCOO_OP_MTTKRP && op != FCOO_OP_TTM) return fail(FCOO_ERR_ARG, "unknown op %d", op);
@@ -166,8 +166,10 @@ fcoo_status plan_modes(fcoo_s* f, int order, const int64_t* dims, int op, int mo
   if (op == FCOO_OP_MTTKRP) {
     f->idx_modes[ni++] = mode;
     for (int m = 0; m < order; ++m) if (m != mode) f->prod_modes[np++] = m;
-    for (int a = 1; a < np; ++a)  // reading Q5: ascending extent, ties by mode id (stable)
-      for (int b = a; b > 0 && dims[f->prod_modes[b]] < dims[f->prod_modes[b - 1]]; --b) {
+    // reading Q5: ascending extent, ties by mode id (stable); FCOO_BUILD_PRODUCT_DESC: descending
+    auto before = [&](int x, int y) { return desc ? dims[x] > dims[y] : dims[x] < dims[y]; };
+    for (int a = 1; a < np; ++a)
+      for (int b = a; b > 0 && before(f->prod_modes[b], f->prod_modes[b - 1]); --b) {
         int t = f->prod_modes[b]; f->prod_modes[b] = f->prod_modes[b - 1]; f->prod_modes[b - 1] = t;
       }
   } else {
@@ -188,7 +190,7 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
   if (T < 32 || T > 8192 || (T % 32) != 0) return fail(FCOO_ERR_ARG, "tile_nnz %d must be a multiple of 32 in [32,8192]", T);
   if (!coo->dims || !coo->idx || !coo->val) return fail(FCOO_ERR_ARG, "NULL dims/idx/val");
   fcoo_s tmp;
-  fcoo_status st = plan_modes(&tmp, coo->order, coo->dims, op, mode);
+  fcoo_status st = plan_modes(&tmp, coo->order, coo->dims, op, mode, (flags & FCOO_BUILD_PRODUCT_DESC) != 0);
   if (st) return st;
   if (coo->nnz <= 0) return fail(FCOO_ERR_EMPTY, "nnz == 0");
   if (coo->nnz >= 4294967295LL) return fail(FCOO_ERR_ARG, "nnz must be < 2^32");

@@ -17,11 +17,11 @@ def F():
     return F
 
 
-def _compare(F, dims, idx, val, op, mode, T):
+def _compare(F, dims, idx, val, op, mode, T, desc=False):
     coo = F.Coo.from_numpy(dims, idx, val)
-    h = F.fcoo_build(coo, mode, op=op, tile_nnz=T, keep_perm=True)
+    h = F.fcoo_build(coo, mode, op=op, tile_nnz=T, keep_perm=True, product_desc=desc)
     got = F.fcoo_export(h, perm=True)
-    ref = oracle.build_fcoo(dims, idx, val, op, mode, T)
+    ref = oracle.build_fcoo(dims, idx, val, op, mode, T, desc=desc)
     assert h.info.nsegs == ref.nsegs
     assert h.info.idx_modes == ref.index_modes and h.info.prod_modes == ref.product_modes
     assert np.array_equal(got["perm"], ref.perm)
@@ -51,6 +51,13 @@ def test_build_random(F, T):
         for mode in range(len(dims)):
             for op in (F.OP_MTTKRP, F.OP_TTM):
                 _compare(F, dims, idx, val, op, mode, T)
+
+
+def test_build_product_desc_option(F):
+    for dims in ((300, 200, 500), (40, 50, 30, 20)):
+        idx, val = gen.coo(dims, 20000, None, 19)
+        for mode in range(len(dims)):
+            _compare(F, dims, idx, val, F.OP_MTTKRP, mode, 64, desc=True)
 
 
 def test_build_nell2_subset(F):

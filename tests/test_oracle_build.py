@@ -154,3 +154,17 @@ def test_toggle_reading_equivalence():
     tog = np.cumsum(heads) & 1
     back = np.concatenate([[1], tog[1:] ^ tog[:-1]])
     assert np.array_equal(back, heads)
+
+
+def test_product_desc_option_invariants():
+    """FCOO_BUILD_PRODUCT_DESC: same index modes and segments, product modes by descending extent."""
+    dims = (7, 5, 9, 4)
+    idx, val = gen.coo(dims, 300, None, 23)
+    assert oracle.mode_spec(dims, oracle.OP_MTTKRP, 0, desc=True)[1] == [2, 1, 3]
+    for mode in range(4):
+        a = oracle.build_fcoo(dims, idx, val, oracle.OP_MTTKRP, mode, 32)
+        b = oracle.build_fcoo(dims, idx, val, oracle.OP_MTTKRP, mode, 32, desc=True)
+        assert a.nsegs == b.nsegs and np.array_equal(a.bf, b.bf) and np.array_equal(a.seg_coord, b.seg_coord)
+        keys = np.stack([idx[m][b.perm] for m in b.index_modes + b.product_modes]).astype(np.int64)
+        for p in range(1, val.shape[0]):
+            assert tuple(keys[:, p - 1]) < tuple(keys[:, p])

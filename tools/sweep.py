@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--tile", type=int, default=2048)
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--op", default="mttkrp")
+    ap.add_argument("--desc", action="store_true", help="FCOO_BUILD_PRODUCT_DESC")
     a = ap.parse_args()
     import torch
 
@@ -31,7 +32,7 @@ def main():
     nnz = val.shape[0]
     peak, _ = hbm_peak()
     for n in range(N):
-        h = P.fcoo_build(coo, n, op=P.OP_TTM if a.op == "ttm" else P.OP_MTTKRP, tile_nnz=a.tile)
+        h = P.fcoo_build(coo, n, op=P.OP_TTM if a.op == "ttm" else P.OP_MTTKRP, tile_nnz=a.tile, product_desc=a.desc)
         for R in [int(x) for x in a.R.split(",")]:
             fs = [torch.from_numpy(f).cuda() for f in gen.factors(w.dims, R, 7)]
             rows = h.info.nsegs if a.op == "ttm" else w.dims[n]
@@ -53,9 +54,13 @@ def main():
             e1.record()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / a.reps
-            b = compulsory_bytes(w.dims, nnz, n, R, a.tile)
+            if a.op == "ttm":  # stream (index + value + bf + sf) + U + semi-sparse output
+                ntl = (nnz + a.tile - 1) // a.tile
+                b = nnz * 8 + (nnz + 7) // 8 + 4 * ((ntl + 31) // 32) + 4 * w.dims[n] * R + 4 * h.info.nsegs * R
+            else:
+                b = compulsory_bytes(w.dims, nnz, n, R, a.tile)
             print(json.dumps({"engine": os.environ.get("FCOO_ENGINE", "default"), "workload": a.workload,
-                              "op": a.op, "mode": n, "R": R, "tile": a.tile, "ms": round(ms, 4),
+                              "op": a.op, "desc": a.desc, "mode": n, "R": R, "tile": a.tile, "ms": round(ms, 4),
                               "gnnz_s": round(nnz / ms / 1e6, 2), "hbm_frac": round(b / (ms / 1e3) / 1e9 / peak, 4)}),
                   flush=True)
         h.destroy()
