@@ -1,0 +1,42 @@
+"""Small end-to-end run that reaches every engine specialisation used at scale (staged float4 path at
+R=16/32/64, scalar path, TTM, fp64 CP fit mode, sharded handles) — the workload for
+compute-sanitizer memcheck / racecheck / synccheck.
+
+compute-sanitizer --tool racecheck python tools/sanitize_run.py
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    import torch
+
+    import gen
+    import paper_1705_09905_b200 as P
+    dims = (300, 200, 250)
+    idx, val = gen.coo(dims, 30000, (0.8, 0.5, 0.5), 3)
+    coo = P.Coo.from_numpy(dims, idx, val)
+    for R in (16, 32, 64, 5):
+        fs = [torch.from_numpy(f).cuda() for f in gen.factors(dims, R, 4)]
+        for n in range(3):
+            h = P.fcoo_build(coo, n, tile_nnz=128)
+            out = torch.empty((dims[n], R), device="cuda")
+            P.fcoo_mttkrp(h, fs, R, out)
+            P.fcoo_set_shard(h, 1, 3)
+            P.fcoo_mttkrp(h, fs, R, out)
+            h.destroy()
+            t = P.fcoo_build(coo, n, op=P.OP_TTM, tile_nnz=64)
+            yo = torch.empty((t.info.nsegs, R), device="cuda")
+            P.fcoo_ttm(t, fs[n], R, yo)
+            t.destroy()
+    fs = [torch.from_numpy(f).cuda() for f in gen.factors(dims, 8, 5)]
+    P.cp_als(coo, 8, 3, fs, tile_nnz=64)
+    torch.cuda.synchronize()
+    print("sanitize_run OK")
+
+
+if __name__ == "__main__":
+    main()
