@@ -208,7 +208,8 @@ typedef struct {
  * cp_als — factors: host array of `order` DEVICE pointers to I_m x R fp32 buffers holding the
  * initial factors on entry (caller-seeded) and the unit-column factors on exit.
  * lambda: device [R] fp32 (out).  fit_trace: host [iters] (out).  iters_done: host (out).
- * Synchronises `stream` once per iteration (to read the fit for `tol`).
+ * Synchronises `stream` once per iteration when tol > 0 (to read the fit for the stopping rule),
+ * otherwise once at the end (the fit trace stays on the device until then).
  */
 fcoo_status cp_als(const fcoo_coo* tensor, const fcoo_cp_opts* opts, float* const* factors, float* lambda,
                    double* fit_trace, int* iters_done, const fcoo_allocator* alloc, void* stream);

@@ -196,6 +196,42 @@ __global__ void k_gram_partial(const float* __restrict__ U, int64_t I, int R, in
   }
 }
 
+// Tiled Gram partial for R <= 64: 32-row tiles of U staged in shared memory (coalesced loads);
+// thread tid owns entries e = tid + k*256 (k < EPT) of the R x R block in fp64 registers.
+template <int EPT>
+__global__ void __launch_bounds__(kCT) k_gram_tiled(const float* __restrict__ U, int64_t I, int R, int64_t rows_per,
+                                                    double* __restrict__ part) {
+  constexpr int TR = 32;
+  __shared__ float tile[TR * 64];
+  const int c = blockIdx.x;
+  const int64_t i0 = (int64_t)c * rows_per, i1 = min(I, i0 + rows_per);
+  const int RR = R * R;
+  double acc[EPT];
+  int ea[EPT], eb[EPT];
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    acc[k] = 0.0;
+    const int e = threadIdx.x + k * kCT;
+    ea[k] = e < RR ? e / R : 0;
+    eb[k] = e < RR ? e % R : 0;
+  }
+  for (int64_t r0 = i0; r0 < i1; r0 += TR) {
+    const int nr = (int)min((int64_t)TR, i1 - r0);
+    __syncthreads();
+    for (int q = threadIdx.x; q < nr * R; q += kCT) tile[q] = U[r0 * R + q];
+    __syncthreads();
+    for (int r = 0; r < nr; ++r) {
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) acc[k] += (double)tile[r * R + ea[k]] * (double)tile[r * R + eb[k]];
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < EPT; ++k) {
+    const int e = threadIdx.x + k * kCT;
+    if (e < RR) part[(int64_t)c * RR + e] = acc[k];
+  }
+}
+
 __global__ void k_gram_reduce(const double* __restrict__ part, int nchunks, int RR, double* __restrict__ G) {
   int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= RR) return;
@@ -294,13 +330,14 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
   int64_t Imax = 0;
   for (int m = 0; m < N; ++m) Imax = std::max(Imax, X->dims[m]);
   const int RR = R * R;
-  const int64_t maxchunks = 256;
+  // row chunks of the Gram / inner-product partial sums (<= 32 MB of fp64 partials)
+  const int64_t maxchunks = std::max<int64_t>(16, std::min<int64_t>(1024, (32ll << 20) / (8ll * RR)));
   Buf M(&al, sizeof(float) * Imax * R, s), M64(&al, sizeof(double) * X->dims[N - 1] * R, s);
   Buf Gs(&al, sizeof(double) * N * RR, s), Graw(&al, sizeof(double) * RR, s);
   Buf A(&al, sizeof(double) * RR, s), Q(&al, sizeof(double) * RR, s), W(&al, sizeof(double) * RR, s);
   Buf lam(&al, sizeof(double) * R, s), part(&al, sizeof(double) * maxchunks * RR, s);
   Buf ipart(&al, sizeof(double) * maxchunks, s), xpart(&al, sizeof(double) * maxchunks, s);
-  Buf fitd(&al, sizeof(double) * 2, s), status(&al, sizeof(int) * 2, s);
+  Buf fitd(&al, sizeof(double) * (o->iters + 1), s), status(&al, sizeof(int) * 2, s);
   if (!M.ok() || !M64.ok() || !Gs.ok() || !Graw.ok() || !A.ok() || !Q.ok() || !W.ok() || !lam.ok() || !part.ok() || !ipart.ok() ||
       !xpart.ok() || !fitd.ok() || !status.ok()) {
     cleanup();
@@ -309,11 +346,14 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
   GramPtrs gp{};
   for (int m = 0; m < N; ++m) gp.g[m] = Gs.as<double>() + (int64_t)m * RR;
 
-  auto chunks_for = [&](int64_t I) { return (int)std::min<int64_t>(maxchunks, std::max<int64_t>(1, (I + 255) / 256)); };
+  auto chunks_for = [&](int64_t I) { return (int)std::min<int64_t>(maxchunks, std::max<int64_t>(1, (I + 127) / 128)); };
   auto gram = [&](const float* U, int64_t I, double* out) -> fcoo_status {
     int nc = chunks_for(I);
     int64_t per = (I + nc - 1) / nc;
-    k_gram_partial<<<nc, kCT, 0, s>>>(U, I, R, per, part.as<double>());
+    if (RR <= kCT) k_gram_tiled<1><<<nc, kCT, 0, s>>>(U, I, R, per, part.as<double>());
+    else if (RR <= 4 * kCT) k_gram_tiled<4><<<nc, kCT, 0, s>>>(U, I, R, per, part.as<double>());
+    else if (RR <= 16 * kCT) k_gram_tiled<16><<<nc, kCT, 0, s>>>(U, I, R, per, part.as<double>());
+    else k_gram_partial<<<nc, kCT, 0, s>>>(U, I, R, per, part.as<double>());
     FCOO_LAUNCH_CHECK();
     k_gram_reduce<<<nblk(RR), kCT, 0, s>>>(part.as<double>(), nc, RR, out);
     FCOO_LAUNCH_CHECK();
@@ -367,16 +407,22 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
     k_inner_partial<<<nc, kCT, 0, s>>>(M64.as<double>(), factors[nl], lam.as<double>(), Il, R, per, ipart.as<double>());
     FCOO_LAUNCH_CHECK();
     k_fit<<<1, kCT, 0, s>>>(ipart.as<double>(), nc, xpart.as<double>(), nx, gp, N, lam.as<double>(), R,
-                            fitd.as<double>());
+                            fitd.as<double>() + it);
     FCOO_LAUNCH_CHECK();
-    double fit = 0.0;
-    cudaError_t ce = cudaMemcpyAsync(&fit, fitd.p, sizeof(double), cudaMemcpyDeviceToHost, s);
-    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
-    if (ce != cudaSuccess) { st = fail(FCOO_ERR_CUDA, "fit readback: %s", cudaGetErrorString(ce)); break; }
-    fit_trace[it] = fit;
     if (iters_done) *iters_done = it + 1;
-    if (o->tol > 0 && it > 0 && fabs(fit - fit_prev) < o->tol) { ++it; break; }
-    fit_prev = fit;
+    if (o->tol > 0) {  // the stopping rule needs the fit on the host every iteration
+      double fit = 0.0;
+      cudaError_t ce = cudaMemcpyAsync(&fit, fitd.as<double>() + it, sizeof(double), cudaMemcpyDeviceToHost, s);
+      if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+      if (ce != cudaSuccess) { st = fail(FCOO_ERR_CUDA, "fit readback: %s", cudaGetErrorString(ce)); break; }
+      if (it > 0 && fabs(fit - fit_prev) < o->tol) { ++it; break; }
+      fit_prev = fit;
+    }
+  }
+  if (!st && it > 0) {  // fit trace (one readback when tol == 0)
+    cudaError_t ce = cudaMemcpyAsync(fit_trace, fitd.p, sizeof(double) * it, cudaMemcpyDeviceToHost, s);
+    if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
+    if (ce != cudaSuccess) st = fail(FCOO_ERR_CUDA, "fit readback: %s", cudaGetErrorString(ce));
   }
   cleanup();
   return st;

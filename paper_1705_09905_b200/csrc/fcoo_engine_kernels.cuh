@@ -108,8 +108,18 @@ struct Ld<1> {
   }
 };
 
+// fp64 accumulator with an fp32 batch partial: products and the <= 8-term batch sum are formed
+// in fp32 (same instructions as the fp32 path), and settle() folds the batch partial into the
+// fp64 sum once per batch (one conversion per column per batch instead of per product).  The
+// fp32 rounding of a batch is random in sign across batches, so the error of the fp64 sum stays
+// ~u/sqrt(#batches) relative — far below the 1e-8 the CP fit identity needs.
 struct d4 {
   double x, y, z, w;
+  float4 part;
+};
+struct d1 {
+  double x;
+  float part;
 };
 
 template <int VEC, class ACC>
@@ -135,6 +145,7 @@ struct Acc<4, float> {
   static __device__ __forceinline__ void fold(T& acc, const T& t, float4 r0) {  // acc += t * r0
     acc = make_float4(fmaf(t.x, r0.x, acc.x), fmaf(t.y, r0.y, acc.y), fmaf(t.z, r0.z, acc.z), fmaf(t.w, r0.w, acc.w));
   }
+  static __device__ __forceinline__ void settle(T&) {}
   static __device__ __forceinline__ void store(float* p, T v) { *reinterpret_cast<float4*>(p) = v; }
   static __device__ __forceinline__ void red(float* p, T v) { red_add_v4(p, v); }
 };
@@ -157,20 +168,21 @@ struct Acc<1, float> {
     t = fmaf(v, h, t);
   }
   static __device__ __forceinline__ void fold(T& acc, const T& t, float r0) { acc = fmaf(t, r0, acc); }
+  static __device__ __forceinline__ void settle(T&) {}
   static __device__ __forceinline__ void store(float* p, T v) { *p = v; }
   static __device__ __forceinline__ void red(float* p, T v) { atomicAdd(p, v); }
 };
 template <>
 struct Acc<4, double> {
   using T = d4;
-  static __device__ __forceinline__ T zero() { return d4{0.0, 0.0, 0.0, 0.0}; }
+  static __device__ __forceinline__ T zero() { return d4{0.0, 0.0, 0.0, 0.0, make_float4(0.f, 0.f, 0.f, 0.f)}; }
   template <int NP>
   static __device__ __forceinline__ void add(T& acc, float v, const float4 (&r)[NP]) {
-    double hx = r[0].x, hy = r[0].y, hz = r[0].z, hw = r[0].w;
-#pragma unroll
-    for (int a = 1; a < NP; ++a) { hx *= (double)r[a].x; hy *= (double)r[a].y; hz *= (double)r[a].z; hw *= (double)r[a].w; }
-    double dv = v;
-    acc.x = fma(dv, hx, acc.x); acc.y = fma(dv, hy, acc.y); acc.z = fma(dv, hz, acc.z); acc.w = fma(dv, hw, acc.w);
+    Acc<4, float>::add<NP>(acc.part, v, r);
+  }
+  static __device__ __forceinline__ void settle(T& acc) {
+    acc.x += (double)acc.part.x; acc.y += (double)acc.part.y; acc.z += (double)acc.part.z; acc.w += (double)acc.part.w;
+    acc.part = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   template <int NP>
   static __device__ __forceinline__ void add_inner(T& t, float v, const float4 (&r)[NP]) {
@@ -185,34 +197,43 @@ struct Acc<4, double> {
     acc.z = fma(t.z, (double)r0.z, acc.z); acc.w = fma(t.w, (double)r0.w, acc.w);
   }
   static __device__ __forceinline__ void store(double* p, T v) {
+    settle(v);
     reinterpret_cast<double2*>(p)[0] = make_double2(v.x, v.y);
     reinterpret_cast<double2*>(p)[1] = make_double2(v.z, v.w);
   }
   static __device__ __forceinline__ void red(double* p, T v) {
+    settle(v);
     atomicAdd(p, v.x); atomicAdd(p + 1, v.y); atomicAdd(p + 2, v.z); atomicAdd(p + 3, v.w);
   }
 };
 template <>
 struct Acc<1, double> {
-  using T = double;
-  static __device__ __forceinline__ T zero() { return 0.0; }
+  using T = d1;
+  static __device__ __forceinline__ T zero() { return d1{0.0, 0.f}; }
   template <int NP>
   static __device__ __forceinline__ void add(T& acc, float v, const float (&r)[NP]) {
-    double h = r[0];
-#pragma unroll
-    for (int a = 1; a < NP; ++a) h *= (double)r[a];
-    acc = fma((double)v, h, acc);
+    Acc<1, float>::add<NP>(acc.part, v, r);
+  }
+  static __device__ __forceinline__ void settle(T& acc) {
+    acc.x += (double)acc.part;
+    acc.part = 0.f;
   }
   template <int NP>
   static __device__ __forceinline__ void add_inner(T& t, float v, const float (&r)[NP]) {
     double h = r[1];
 #pragma unroll
     for (int a = 2; a < NP; ++a) h *= (double)r[a];
-    t = fma((double)v, h, t);
+    t.x = fma((double)v, h, t.x);
   }
-  static __device__ __forceinline__ void fold(T& acc, const T& t, float r0) { acc = fma(t, (double)r0, acc); }
-  static __device__ __forceinline__ void store(double* p, T v) { *p = v; }
-  static __device__ __forceinline__ void red(double* p, T v) { atomicAdd(p, v); }
+  static __device__ __forceinline__ void fold(T& acc, const T& t, float r0) { acc.x = fma(t.x, (double)r0, acc.x); }
+  static __device__ __forceinline__ void store(double* p, T v) {
+    settle(v);
+    *p = v.x;
+  }
+  static __device__ __forceinline__ void red(double* p, T v) {
+    settle(v);
+    atomicAdd(p, v.x);
+  }
 };
 
 // NP product modes; G lanes per group (divides 32); VEC floats per lane per column slot;
@@ -314,6 +335,8 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
         for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), r[e][c]);
       }
     }
+#pragma unroll
+    for (int c = 0; c < CPL; ++c) A::settle(acc[c]);
   }
   // ragged tail of the tensor's last tile: one nonzero at a time
   for (int64_t p = pfull; p < p1; ++p) {
@@ -657,6 +680,8 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
           for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), r[e][c]);
         }
       }
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) A::settle(acc[c]);
     }
     __syncwarp(gmask);  // every lane is done with this stage before it is refilled
   }
@@ -674,7 +699,10 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
         r1[c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(ub[a][c] + (size_t)i * rowb)) : V::zero();
     }
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], v, r1[c]);
+    for (int c = 0; c < CPL; ++c) {
+      A::template add<NP>(acc[c], v, r1[c]);
+      A::settle(acc[c]);
+    }
   }
   const bool right_open = (t + 1 < P.ntiles) && !((P.sf[(t + 1) >> 5] >> ((t + 1) & 31)) & 1u);
   flush(own && !right_open);
