@@ -44,10 +44,74 @@ __device__ double block_sum(double v, double* sh) {
   return r;
 }
 
+// One CTA, R <= 48, everything in shared memory: V = Hadamard_{m != n} G_m; Cholesky V = L L^T;
+// L^{-1} column-parallel by forward substitution; W = V^{-1} = L^{-T} L^{-1}.  If a pivot is not
+// positive (V not positive definite) it writes status[0] = 1 and leaves W to k_solve (launched
+// next with only_if_failed), which redoes the solve with the Jacobi pseudo-inverse fallback.
+constexpr int kSmallR = 48;
+__global__ void __launch_bounds__(kCT) k_solve_small(GramPtrs G, int order, int n, int R, double* __restrict__ W,
+                                                     int* __restrict__ status) {
+  __shared__ double L[kSmallR * kSmallR], Li[kSmallR * kSmallR];
+  __shared__ double sh[kCT];
+  __shared__ int fail;
+  const int tid = threadIdx.x, nt = blockDim.x, RR = R * R;
+  double tr = 0.0;
+  for (int e = tid; e < RR; e += nt) {
+    double v = 1.0;
+    for (int m = 0; m < order; ++m)
+      if (m != n) v *= G.g[m][e];
+    L[e] = v;
+    Li[e] = 0.0;
+    if (e / R == e % R) tr += v;
+  }
+  if (tid == 0) fail = 0;
+  tr = block_sum(tr, sh);  // (contains __syncthreads)
+  const double tiny = 1e-12 * (tr > 0 ? tr / R : 1.0);
+  for (int j = 0; j < R; ++j) {  // right-looking Cholesky, column j
+    if (tid == 0) {
+      double d = L[j * R + j];
+      if (!(d > tiny)) fail = 1;
+      L[j * R + j] = d > 0 ? sqrt(d) : 1.0;
+    }
+    __syncthreads();
+    if (fail) break;
+    const double ljj = L[j * R + j];
+    for (int i = j + 1 + tid; i < R; i += nt) L[i * R + j] /= ljj;
+    __syncthreads();
+    // trailing update of the lower triangle: L[i][k] -= L[i][j] * L[k][j], j < k <= i
+    for (int e = tid; e < RR; e += nt) {
+      const int i = e / R, k = e % R;
+      if (k > j && k <= i) L[i * R + k] -= L[i * R + j] * L[k * R + j];
+    }
+    __syncthreads();
+  }
+  if (fail) {
+    if (tid == 0) status[0] = 1;
+    return;
+  }
+  for (int c = tid; c < R; c += nt) {  // column c of L^{-1}
+    for (int i = c; i < R; ++i) {
+      double s = (i == c) ? 1.0 : 0.0;
+      for (int k = c; k < i; ++k) s -= L[i * R + k] * Li[k * R + c];
+      Li[i * R + c] = s / L[i * R + i];
+    }
+  }
+  __syncthreads();
+  for (int e = tid; e < RR; e += nt) {  // W = Li^T Li
+    const int a = e / R, b = e % R;
+    double s = 0.0;
+    for (int k = a > b ? a : b; k < R; ++k) s += Li[k * R + a] * Li[k * R + b];
+    W[e] = s;
+  }
+  if (tid == 0) status[0] = 0;
+}
+
 // One CTA.  V = Hadamard_{m != n} G_m; W = V^{-1} by Cholesky, else Jacobi pinv (tau = R*eps*max|lambda|).
 // Scratch A, Q: R x R doubles each.  status[0] = 0 Cholesky, 1 Jacobi fallback.
+// only_if_failed: return at once unless k_solve_small reported a non-positive pivot.
 __global__ void k_solve(GramPtrs G, int order, int n, int R, double* __restrict__ A, double* __restrict__ Q,
-                        double* __restrict__ W, int* __restrict__ status) {
+                        double* __restrict__ W, int* __restrict__ status, int only_if_failed) {
+  if (only_if_failed && status[0] == 0) return;
   __shared__ double sh[kCT];
   __shared__ int fail;
   __shared__ double cs[2];
@@ -384,7 +448,12 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
         st = fcoo_mttkrp(H[n], factors, R, M.as<float>(), (void*)s);
       }
       if (st) break;
-      k_solve<<<1, kCT, 0, s>>>(gp, N, n, R, A.as<double>(), Q.as<double>(), W.as<double>(), status.as<int>());
+      if (R <= kSmallR) {
+        k_solve_small<<<1, kCT, 0, s>>>(gp, N, n, R, W.as<double>(), status.as<int>());
+        FCOO_LAUNCH_CHECK();
+      }
+      k_solve<<<1, kCT, 0, s>>>(gp, N, n, R, A.as<double>(), Q.as<double>(), W.as<double>(), status.as<int>(),
+                                R <= kSmallR ? 1 : 0);
       FCOO_LAUNCH_CHECK();
       if (last) k_apply<double><<<nblk(In * R), kCT, 0, s>>>(M64.as<double>(), W.as<double>(), In, R, factors[n]);
       else k_apply<float><<<nblk(In * R), kCT, 0, s>>>(M.as<float>(), W.as<double>(), In, R, factors[n]);
