@@ -108,11 +108,10 @@ struct Ld<1> {
   }
 };
 
-// fp64 accumulator with an fp32 batch partial: products and the <= 8-term batch sum are formed
-// in fp32 (same instructions as the fp32 path), and settle() folds the batch partial into the
-// fp64 sum once per batch (one conversion per column per batch instead of per product).  The
-// fp32 rounding of a batch is random in sign across batches, so the error of the fp64 sum stays
-// ~u/sqrt(#batches) relative — far below the 1e-8 the CP fit identity needs.
+// fp64 accumulator (CP fit mode).  Products are formed in fp64 (exact for two fp32 factors)
+// because the fit identity needs <X, Xhat> to ~1e-10 relative near fit = 1: an fp32 product
+// rounding (2^-24 per term) left a ~1e-4 jitter in the fit of small converged problems.  The
+// `part` slot (settle()) is an fp32 staging partial kept for experiments; add() does not use it.
 struct d4 {
   double x, y, z, w;
   float4 part;
@@ -178,7 +177,12 @@ struct Acc<4, double> {
   static __device__ __forceinline__ T zero() { return d4{0.0, 0.0, 0.0, 0.0, make_float4(0.f, 0.f, 0.f, 0.f)}; }
   template <int NP>
   static __device__ __forceinline__ void add(T& acc, float v, const float4 (&r)[NP]) {
-    Acc<4, float>::add<NP>(acc.part, v, r);
+    // products in fp64: r0*r1 of two fp32 values is exact, v*(r0*r1) rounds once at 2^-53
+    double hx = r[0].x, hy = r[0].y, hz = r[0].z, hw = r[0].w;
+#pragma unroll
+    for (int a = 1; a < NP; ++a) { hx *= (double)r[a].x; hy *= (double)r[a].y; hz *= (double)r[a].z; hw *= (double)r[a].w; }
+    const double dv = v;
+    acc.x = fma(dv, hx, acc.x); acc.y = fma(dv, hy, acc.y); acc.z = fma(dv, hz, acc.z); acc.w = fma(dv, hw, acc.w);
   }
   static __device__ __forceinline__ void settle(T& acc) {
     acc.x += (double)acc.part.x; acc.y += (double)acc.part.y; acc.z += (double)acc.part.z; acc.w += (double)acc.part.w;
@@ -212,7 +216,10 @@ struct Acc<1, double> {
   static __device__ __forceinline__ T zero() { return d1{0.0, 0.f}; }
   template <int NP>
   static __device__ __forceinline__ void add(T& acc, float v, const float (&r)[NP]) {
-    Acc<1, float>::add<NP>(acc.part, v, r);
+    double h = r[0];
+#pragma unroll
+    for (int a = 1; a < NP; ++a) h *= (double)r[a];
+    acc.x = fma((double)v, h, acc.x);
   }
   static __device__ __forceinline__ void settle(T& acc) {
     acc.x += (double)acc.part;
