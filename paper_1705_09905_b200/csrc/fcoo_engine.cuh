@@ -24,10 +24,7 @@ struct EngineParams {
 };
 
 __device__ __forceinline__ const float* replica(const EngineParams& P, int a) {
-  if (P.nrep <= 1) return P.U[a];
-  uint32_t smid;
-  asm("mov.u32 %0, %%smid;" : "=r"(smid));  // one replica per SM keeps the SM's L1 reuse intact
-  return P.U[a] + (int64_t)(smid % (uint32_t)P.nrep) * P.rep_stride[a];
+  return P.nrep > 1 ? P.U[a] + (int64_t)(blockIdx.x % P.nrep) * P.rep_stride[a] : P.U[a];
 }
 
 // Launch the segmented-reduction kernel for NP product modes, accumulator type ACC (instantiated
