@@ -146,8 +146,6 @@ void free_handle_arrays(fcoo_s* f) {
   if (f->seg_base) f->alloc.put(f->seg_base, f->bytes_seg_base, s);
   if (f->seg_coord) f->alloc.put(f->seg_coord, f->bytes_seg_coord, s);
   if (f->perm) f->alloc.put(f->perm, f->bytes_perm, s);
-  if (f->rep) f->alloc.put(f->rep, f->bytes_rep, s);
-  f->rep = nullptr;
   f->pidx = nullptr; f->val = nullptr; f->bf = nullptr; f->sf = nullptr;
   f->seg_base = nullptr; f->seg_coord = nullptr; f->perm = nullptr;
 }

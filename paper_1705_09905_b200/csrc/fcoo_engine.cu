@@ -37,18 +37,6 @@ cudaError_t launch_engine(const EngineParams& P, int NP, bool vec_ok, cudaStream
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// Number of factor replicas (FCOO_REPLICAS env var, read once; default 1 = none).
-int replicas() {
-  static int k = -1;
-  if (k < 0) {
-    const char* e = getenv("FCOO_REPLICAS");
-    k = e ? atoi(e) : 1;
-    if (k < 1) k = 1;
-    if (k > 16) k = 16;
-  }
-  return k;
-}
-
 template <class ACC>
 fcoo_status prepare_output(fcoo_s* f, int R, ACC* out, int64_t rows, bool all_rows_are_segments, cudaStream_t s) {
   bool whole = (f->tile_begin == 0 && f->tile_end == f->ntiles);
@@ -83,28 +71,6 @@ fcoo_status mttkrp_t(fcoo_s* f, const float* const* factors, int R, ACC* out, cu
   P.seg_coord = f->dense_rows ? nullptr : f->seg_coord;
   P.nnz = f->nnz; P.ntiles = f->ntiles; P.tile_begin = f->tile_begin; P.tile_end = f->tile_end;
   P.T = (int)f->T; P.R = R; P.out = out;
-  P.nrep = 1;
-  const int nrep = replicas();
-  if (nrep > 1) {  // K identical copies of each product factor, read by different CTAs
-    size_t need = 0;
-    for (int a = 0; a < f->n_prod; ++a) need += sizeof(float) * (size_t)nrep * f->dims[f->prod_modes[a]] * R;
-    if (need > f->bytes_rep) {
-      if (f->rep) f->alloc.put(f->rep, f->bytes_rep, s);
-      f->rep = reinterpret_cast<float*>(f->alloc.get(need, s));
-      f->bytes_rep = f->rep ? need : 0;
-      if (!f->rep) return fail(FCOO_ERR_OOM, "factor replicas");
-    }
-    float* dst = f->rep;
-    for (int a = 0; a < f->n_prod; ++a) {
-      const int64_t n = f->dims[f->prod_modes[a]] * R;
-      for (int k = 0; k < nrep; ++k)
-        FCOO_CUDA_TRY(cudaMemcpyAsync(dst + k * n, P.U[a], sizeof(float) * n, cudaMemcpyDeviceToDevice, s));
-      P.U[a] = dst;
-      P.rep_stride[a] = n;
-      dst += nrep * n;
-    }
-    P.nrep = nrep;
-  }
   // all rows are segments (dense_rows): only tile-crossing rows need zeroing
   fcoo_status st = prepare_output<ACC>(f, R, out, f->dims[f->mode], f->dense_rows != 0, s);
   if (st) return st;

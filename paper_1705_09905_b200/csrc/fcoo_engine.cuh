@@ -17,15 +17,7 @@ struct EngineParams {
   int64_t nnz, ntiles, tile_begin, tile_end;
   int T, R;
   void* out;  // float* (fp32 accumulation) or double* (fp64 accumulation)
-  // factor replicas: U[a] + k * rep_stride[a] (k < nrep) hold identical copies; CTA b reads copy
-  // b % nrep, so a hot row's L2 traffic is spread over nrep different L2 slices
-  int64_t rep_stride[kMaxProd];
-  int nrep;
 };
-
-__device__ __forceinline__ const float* replica(const EngineParams& P, int a) {
-  return P.nrep > 1 ? P.U[a] + (int64_t)(blockIdx.x % P.nrep) * P.rep_stride[a] : P.U[a];
-}
 
 // Launch the segmented-reduction kernel for NP product modes, accumulator type ACC (instantiated
 // in fcoo_engine_np<NP>.cu so the template instances compile in parallel).

@@ -279,7 +279,7 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
 #pragma unroll
   for (int a = 0; a < NP; ++a)
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) ub[a][c] = reinterpret_cast<const char*>(replica(P, a) + (cok[c] ? col[c] : 0));
+    for (int c = 0; c < CPL; ++c) ub[a][c] = reinterpret_cast<const char*>(P.U[a] + (cok[c] ? col[c] : 0));
 
   const int64_t p0 = t * (int64_t)P.T;
   const int64_t p1 = min(p0 + (int64_t)P.T, P.nnz);
@@ -398,7 +398,7 @@ __global__ void __launch_bounds__(256) k_segreduce_fact(const EngineParams P) {
 #pragma unroll
   for (int a = 0; a < NP; ++a)
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) ub[a][c] = reinterpret_cast<const char*>(replica(P, a) + (cok[c] ? col[c] : 0));
+    for (int c = 0; c < CPL; ++c) ub[a][c] = reinterpret_cast<const char*>(P.U[a] + (cok[c] ? col[c] : 0));
 
   const int64_t p0 = t * (int64_t)P.T;
   const int64_t p1 = min(p0 + (int64_t)P.T, P.nnz);
@@ -573,10 +573,7 @@ struct Stage {
 // exposed.  This is the "shared-memory staging of the nonzero stream" of the north star; the
 // factor rows still go through L1 (most of the unified carveout stays L1).
 template <int NP, int G, int VEC, int CPL, class ACC, bool FULL>
-#ifndef FCOO_STAGED_MINB
-#define FCOO_STAGED_MINB 1
-#endif
-__global__ void __launch_bounds__(256, FCOO_STAGED_MINB) k_segreduce_staged(const EngineParams P) {
+__global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) {
   using V = Ld<VEC>;
   using VT = typename V::T;
   using A = Acc<VEC, ACC>;
@@ -605,7 +602,7 @@ __global__ void __launch_bounds__(256, FCOO_STAGED_MINB) k_segreduce_staged(cons
 #pragma unroll
   for (int a = 0; a < NP; ++a)
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) ub[a][c] = reinterpret_cast<const char*>(replica(P, a) + (cok[c] ? col[c] : 0));
+    for (int c = 0; c < CPL; ++c) ub[a][c] = reinterpret_cast<const char*>(P.U[a] + (cok[c] ? col[c] : 0));
 
   const int64_t p0 = t * (int64_t)P.T;
   const int64_t p1 = min(p0 + (int64_t)P.T, P.nnz);

@@ -59,8 +59,6 @@ struct fcoo_s {
   uint32_t* seg_base = nullptr;  // ntiles + 1 (last = nsegs)
   uint32_t* seg_coord = nullptr; // nsegs x n_idx
   uint32_t* perm = nullptr;      // nnz (KEEP_PERM only)
-  float* rep = nullptr;          // factor replicas (FCOO_REPLICAS > 1), grown on demand
-  size_t bytes_rep = 0;
   size_t bytes_pidx = 0, bytes_val = 0, bytes_bf = 0, bytes_sf = 0, bytes_seg_base = 0, bytes_seg_coord = 0,
          bytes_perm = 0;
   // shard
