@@ -12,8 +12,12 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-LIB = os.path.join(PKG, "libfcoo.so")
-OBJ = os.path.join(PKG, "build")
+# FCOO_BUILD_TAG / FCOO_NVCC_EXTRA: experiment builds (e.g. -DFCOO_L1POL_INNER=1) go to
+# libfcoo_<tag>.so with their own object dir; the binding loads them when FCOO_LIB points there.
+TAG = os.environ.get("FCOO_BUILD_TAG", "")
+EXTRA = os.environ.get("FCOO_NVCC_EXTRA", "").split()
+LIB = os.path.join(PKG, f"libfcoo_{TAG}.so" if TAG else "libfcoo.so")
+OBJ = os.path.join(PKG, f"build_{TAG}" if TAG else "build")
 SOURCES = ["fcoo_api.cu", "fcoo_build.cu", "fcoo_engine.cu", "fcoo_cp.cu", "fcoo_comm.cu"] + [
     f"fcoo_engine_np{k}.cu" for k in range(1, 8)]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -29,7 +33,8 @@ def nccl_dirs():
 def _flags():
     inc, _ = nccl_dirs()
     return ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-I", os.path.join(ROOT, "include"),
-                   "-I", inc, "--expt-relaxed-constexpr", "-Xptxas", "-v" if os.environ.get("FCOO_PTXAS_V") else "-O3"]
+                   "-I", inc, "--expt-relaxed-constexpr", "-Xptxas", "-v" if os.environ.get("FCOO_PTXAS_V") else "-O3"
+                   ] + EXTRA
 
 
 def _compile(src: str) -> str:

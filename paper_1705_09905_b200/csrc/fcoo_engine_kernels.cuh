@@ -78,6 +78,22 @@ struct Ld<4> {
   using T = float4;
   static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
   static __device__ __forceinline__ T load(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
+  // Gather with an L1 eviction policy: 0 default, 1 no_allocate, 2 evict_first, 3 evict_last.
+  template <int POL>
+  static __device__ __forceinline__ T load_pol(const float* p) {
+    if constexpr (POL == 0) {
+      return load(p);
+    } else {
+      T r;
+      if constexpr (POL == 1)
+        asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+      else if constexpr (POL == 2)
+        asm("ld.global.nc.L1::evict_first.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+      else
+        asm("ld.global.nc.L1::evict_last.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+      return r;
+    }
+  }
   // Predicated gather into fresh registers (opaque to the compiler, so it cannot fold the
   // "keep the previous row" select into a chain of moves that waits on earlier loads).
   static __device__ __forceinline__ T load_if(bool pred, const float* p) {
@@ -96,6 +112,8 @@ struct Ld<1> {
   using T = float;
   static __device__ __forceinline__ T zero() { return 0.f; }
   static __device__ __forceinline__ T load(const float* p) { return __ldg(p); }
+  template <int POL>
+  static __device__ __forceinline__ T load_pol(const float* p) { return load(p); }
   static __device__ __forceinline__ T load_if(bool pred, const float* p) {
     T r;
     asm volatile(
@@ -573,6 +591,14 @@ struct Stage {
 // exposed.  This is the "shared-memory staging of the nonzero stream" of the north star; the
 // factor rows still go through L1 (most of the unified carveout stays L1).
 template <int NP, int G, int VEC, int CPL, class ACC, bool FULL>
+// L1 policy of the factor-row gathers in the staged kernel (see Ld<4>::load_pol): the last
+// product position is the per-nonzero random gather, the others are sorted within a segment.
+#ifndef FCOO_L1POL_INNER
+#define FCOO_L1POL_INNER 0
+#endif
+#ifndef FCOO_L1POL_OUTER
+#define FCOO_L1POL_OUTER 0
+#endif
 __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) {
   using V = Ld<VEC>;
   using VT = typename V::T;
@@ -672,8 +698,12 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
 #pragma unroll
         for (int a = 0; a < NP; ++a)
 #pragma unroll
-          for (int c = 0; c < CPL; ++c)
-            r[e][c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(ub[a][c] + (size_t)ix[a][e] * rowb)) : V::zero();
+          for (int c = 0; c < CPL; ++c) {
+            const float* gp = reinterpret_cast<const float*>(ub[a][c] + (size_t)ix[a][e] * rowb);
+            r[e][c][a] = !cok[c] ? V::zero()
+                         : (a == NP - 1) ? V::template load_pol<FCOO_L1POL_INNER>(gp)
+                                         : V::template load_pol<FCOO_L1POL_OUTER>(gp);
+          }
       if (heads == 0) {
 #pragma unroll
         for (int e = 0; e < B; ++e)

@@ -14,7 +14,7 @@ from dataclasses import dataclass
 import torch
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libfcoo.so")
+LIB_PATH = os.environ.get("FCOO_LIB") or os.path.join(_PKG, "libfcoo.so")  # FCOO_LIB: experiment builds
 
 OK = 0
 ERR_ARG, ERR_ORDER, ERR_MODE, ERR_INDEX_RANGE, ERR_DUPLICATE, ERR_EMPTY, ERR_KEY_BITS, ERR_RANK, ERR_SHAPE, \
