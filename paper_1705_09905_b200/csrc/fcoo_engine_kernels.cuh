@@ -15,6 +15,8 @@
 #pragma once
 #include <stdlib.h>
 
+#include <type_traits>
+
 #include "fcoo_engine.cuh"
 
 namespace fcoo {
@@ -67,6 +69,29 @@ __device__ __forceinline__ void red_add_v4(float* p, float4 v) {
   asm volatile("red.global.add.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
                : "memory");
 }
+
+// Predicated segment flushes (no branch): store when the segment is owned by the tile, red.add when
+// it is shared with a neighbour tile; a false predicate issues nothing to memory.
+__device__ __forceinline__ void flush_if(bool st, bool rd, float* p, float4 v) {
+  asm volatile(
+      "{ .reg .pred ps, pr; setp.ne.b32 ps, %0, 0; setp.ne.b32 pr, %1, 0;\n"
+      "  @ps st.global.v4.f32 [%2], {%3,%4,%5,%6};\n"
+      "  @pr red.global.add.v4.f32 [%2], {%3,%4,%5,%6}; }" ::"r"((int)st),
+      "r"((int)rd), "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+      : "memory");
+}
+__device__ __forceinline__ void flush_if(bool st, bool rd, float* p, float v) {
+  asm volatile(
+      "{ .reg .pred ps, pr; setp.ne.b32 ps, %0, 0; setp.ne.b32 pr, %1, 0;\n"
+      "  @ps st.global.f32 [%2], %3;\n"
+      "  @pr red.global.add.f32 [%2], %3; }" ::"r"((int)st),
+      "r"((int)rd), "l"(p), "f"(v)
+      : "memory");
+}
+__device__ __forceinline__ float4 zero_if(bool z, float4 a) {
+  return z ? make_float4(0.f, 0.f, 0.f, 0.f) : a;
+}
+__device__ __forceinline__ float zero_if(bool z, float a) { return z ? 0.f : a; }
 
 // Per-lane column slot: VEC consecutive fp32 factor entries (float4 on the vector path) and an
 // accumulator of type ACC (fp32 for the product path; fp64 for the CP-ALS fit mode, where the
@@ -635,16 +660,19 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
   const int nchunk = (int)((p1 - p0) / CH);  // full chunks (all of them except in the last tile)
 
   const bool left_open = !((P.sf[t >> 5] >> (t & 31)) & 1u);
-  int64_t s = (int64_t)P.seg_base[t] - 1;
-  int64_t row = 0;
-  if (left_open) row = P.seg_coord ? (int64_t)P.seg_coord[s] : s;
+  // segment ordinal and output row in 32 bits (nsegs and every extent are < 2^32); s wraps to
+  // 0xffffffff before the first head of tile 0 and is never used as a row there
+  uint32_t s = P.seg_base[t] - 1u;
+  uint32_t row = 0;
+  if (left_open) row = P.seg_coord ? P.seg_coord[s] : s;
   bool own = false;
+  ACC* const outp = reinterpret_cast<ACC*>(P.out);
 
   AT acc[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
   auto flush = [&](bool store) {
-    ACC* o = reinterpret_cast<ACC*>(P.out) + row * (int64_t)R;
+    ACC* o = outp + (size_t)row * (uint32_t)R;
 #pragma unroll
     for (int c = 0; c < CPL; ++c)
       if (cok[c]) {
@@ -658,7 +686,7 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
     for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
     own = true;
     ++s;
-    row = P.seg_coord ? (int64_t)P.seg_coord[s] : s;
+    row = P.seg_coord ? P.seg_coord[s] : s;
   };
   auto issue = [&](int64_t pc, int st) {  // group-cooperative copy of chunk [pc, pc+32) into stage st
     uint32_t* dst = my + st * S::WORDS;
@@ -709,6 +737,27 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
         for (int e = 0; e < B; ++e)
 #pragma unroll
           for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), r[e][c]);
+      } else if constexpr (std::is_same<ACC, float>::value) {
+        // branch-free segment handling (short segments, e.g. SpTTM fibres): at a head the running
+        // segment is flushed by a predicated store (owned) or red.add (shared with the left tile),
+        // the accumulator is reset by select and the segment ordinal advances by the head bit
+        const bool first = (ci == 0 && bi == 0);  // the tile's first nonzero opens, never closes
+#pragma unroll
+        for (int e = 0; e < B; ++e) {
+          const bool hd = (heads >> e) & 1u;
+          const bool cl = hd && (e != 0 || !first);
+          ACC* o = outp + (size_t)row * (uint32_t)R;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) {
+            if (cok[c]) flush_if(cl && own, cl && !own, o + col[c], acc[c]);
+            acc[c] = zero_if(hd, acc[c]);
+          }
+          own = own || hd;
+          s += hd ? 1u : 0u;
+          if (hd) row = P.seg_coord ? P.seg_coord[s] : s;
+#pragma unroll
+          for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), r[e][c]);
+        }
       } else {
 #pragma unroll
         for (int e = 0; e < B; ++e) {
