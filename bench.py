@@ -38,7 +38,7 @@ def parse():
     ap.add_argument("--impl", default="fcoo", choices=["fcoo", "reference"])
     ap.add_argument("--workload", default="nell2")
     ap.add_argument("--R", type=int, default=32)
-    ap.add_argument("--tile", type=int, default=2048)
+    ap.add_argument("--tile", type=int, default=0, help="tile_nnz; 0 = the library's automatic choice")
     ap.add_argument("--nnz", type=int, default=None, help="override nnz (debug only; not a bench number)")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
@@ -232,6 +232,7 @@ def main():
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     H = [P.fcoo_build(coo, n, tile_nnz=T) for n in range(N)]
+    T = H[0].info.tile_nnz  # the tile actually used (0 = automatic)
     torch.cuda.synchronize()
     build_ms = (time.perf_counter() - t0) * 1e3
     if world > 1:

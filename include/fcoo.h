@@ -74,9 +74,11 @@ typedef struct {
  * the smallest factor.  Same segments, same sum, another canonical permutation. */
 #define FCOO_BUILD_PRODUCT_DESC 2u
 
-/* Build options.  NULL -> {FCOO_OP_MTTKRP, 2048, 0}.
+/* Build options.  NULL -> {FCOO_OP_MTTKRP, 0 (automatic), 0}.
  * tile_nnz = T, the partition length ("threadlen", P:L272 / P:L426): a multiple of 32 in
- * [32, 8192].  sf has one bit per tile; one GPU lane-group processes one tile. */
+ * [32, 8192], or 0 = automatic (enough tiles to fill the GPU ~4x at R=32: about nnz/37888,
+ * rounded to a multiple of 32 and clamped to [32, 2048]; fcoo_info reports the value used).
+ * sf has one bit per tile; one GPU lane-group processes one tile. */
 typedef struct {
   int op;          /* fcoo_op */
   int tile_nnz;    /* T */
@@ -199,7 +201,7 @@ typedef struct {
   int R;            /* 1..256 */
   int iters;        /* >= 1 */
   double tol;       /* 0 = run all iterations */
-  int tile_nnz;     /* 0 -> 2048 */
+  int tile_nnz;     /* 0 -> automatic (see fcoo_build_opts) */
   fcoo_comm_t comm; /* NULL = single GPU */
   int rank, nranks; /* shard of this process (ignored when comm == NULL) */
 } fcoo_cp_opts;

@@ -152,6 +152,16 @@ void free_handle_arrays(fcoo_s* f) {
 
 }  // namespace
 
+// Automatic tile length (tile_nnz == 0): enough tiles that the MTTKRP/TTM launch fills the GPU
+// about four times over at R=32 (148 SMs x 16 resident warps x 4 lane-groups per warp x 4 waves),
+// rounded to a multiple of 32 in [32, 2048].  Large tensors get T = 2048 (the measured optimum for
+// nell-2, profiles/round1/README.md); brainq-sized ones ~256, where short fibres need more groups.
+int auto_tile(int64_t nnz) {
+  const int64_t groups = 148LL * 16 * 4 * 4;
+  int64_t t = (nnz / groups + 16) / 32 * 32;
+  return (int)std::min<int64_t>(2048, std::max<int64_t>(32, t));
+}
+
 // Host-side mode taxonomy (Table I) and key layout; used by fcoo_build.
 fcoo_status plan_modes(fcoo_s* f, int order, const int64_t* dims, int op, int mode, bool desc = false) {
   if (order < 2 || order > kMaxOrder) return fail(FCOO_ERR_ORDER, "order %d outside [2,8]", order);
@@ -185,8 +195,9 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
   if (!coo || !out) return fail(FCOO_ERR_ARG, "NULL coo/out");
   *out = nullptr;
   int op = opts ? opts->op : FCOO_OP_MTTKRP;
-  int T = opts ? opts->tile_nnz : 2048;
+  int T = opts ? opts->tile_nnz : 0;
   unsigned flags = opts ? opts->flags : 0u;
+  if (T == 0 && coo->nnz > 0) T = auto_tile(coo->nnz);
   if (T < 32 || T > 8192 || (T % 32) != 0) return fail(FCOO_ERR_ARG, "tile_nnz %d must be a multiple of 32 in [32,8192]", T);
   if (!coo->dims || !coo->idx || !coo->val) return fail(FCOO_ERR_ARG, "NULL dims/idx/val");
   fcoo_s tmp;

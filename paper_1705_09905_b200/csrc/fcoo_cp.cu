@@ -385,7 +385,7 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
   // F-COO for every mode, built once up front
   std::vector<fcoo_t> H(N, nullptr);
   auto cleanup = [&]() { for (auto h : H) fcoo_destroy(h); };
-  fcoo_build_opts bo{FCOO_OP_MTTKRP, o->tile_nnz > 0 ? o->tile_nnz : 2048, 0u};
+  fcoo_build_opts bo{FCOO_OP_MTTKRP, o->tile_nnz > 0 ? o->tile_nnz : 0, 0u};
   for (int n = 0; n < N; ++n) {
     fcoo_status st = fcoo_build(X, n, &bo, alloc, (void*)s, &H[n]);
     if (st) { cleanup(); return st; }

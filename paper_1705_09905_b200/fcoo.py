@@ -240,7 +240,7 @@ class Fcoo:
             pass
 
 
-def fcoo_build(coo: Coo, mode: int, op: int = OP_MTTKRP, tile_nnz: int = 2048, keep_perm: bool = False,
+def fcoo_build(coo: Coo, mode: int, op: int = OP_MTTKRP, tile_nnz: int = 0, keep_perm: bool = False,
                product_desc: bool = False, stream=None) -> Fcoo:
     L = load_library()
     opts = _BuildOpts(op, tile_nnz, (BUILD_KEEP_PERM if keep_perm else 0) | (BUILD_PRODUCT_DESC if product_desc else 0))
@@ -348,7 +348,7 @@ def fcoo_set_shard(f: Fcoo, shard: int, nshards: int, comm: Comm | None = None):
     f.info = f._info()
 
 
-def cp_als(coo: Coo, R: int, iters: int, factors, tol: float = 0.0, tile_nnz: int = 2048, comm: Comm | None = None,
+def cp_als(coo: Coo, R: int, iters: int, factors, tol: float = 0.0, tile_nnz: int = 0, comm: Comm | None = None,
            stream=None):
     """In-place CP-ALS: `factors` (list of CUDA fp32 (I_m, R)) hold the initial factors and receive
     the result.  Returns (lambda CUDA fp32 (R,), fit_trace list)."""

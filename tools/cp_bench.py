@@ -18,7 +18,7 @@ def main():
     ap.add_argument("--workload", default="order4")
     ap.add_argument("--R", type=int, default=32)
     ap.add_argument("--iters", type=int, default=20)
-    ap.add_argument("--tile", type=int, default=2048)
+    ap.add_argument("--tile", type=int, default=0)
     a = ap.parse_args()
     import torch
 

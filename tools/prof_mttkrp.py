@@ -17,7 +17,7 @@ def main():
     ap.add_argument("--R", type=int, default=32)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--modes", default=None)
-    ap.add_argument("--tile", type=int, default=2048)
+    ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--op", default="mttkrp")
     a = ap.parse_args()
     import torch

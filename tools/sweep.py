@@ -16,7 +16,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--workload", default="nell2")
     ap.add_argument("--R", default="16,32,64")
-    ap.add_argument("--tile", type=int, default=2048)
+    ap.add_argument("--tile", type=int, default=0, help="0 = automatic")
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--op", default="mttkrp")
     ap.add_argument("--desc", action="store_true", help="FCOO_BUILD_PRODUCT_DESC")
@@ -55,12 +55,12 @@ def main():
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / a.reps
             if a.op == "ttm":  # stream (index + value + bf + sf) + U + semi-sparse output
-                ntl = (nnz + a.tile - 1) // a.tile
+                ntl = h.info.ntiles
                 b = nnz * 8 + (nnz + 7) // 8 + 4 * ((ntl + 31) // 32) + 4 * w.dims[n] * R + 4 * h.info.nsegs * R
             else:
-                b = compulsory_bytes(w.dims, nnz, n, R, a.tile)
+                b = compulsory_bytes(w.dims, nnz, n, R, h.info.tile_nnz)
             print(json.dumps({"engine": os.environ.get("FCOO_ENGINE", "default"), "workload": a.workload,
-                              "op": a.op, "desc": a.desc, "mode": n, "R": R, "tile": a.tile, "ms": round(ms, 4),
+                              "op": a.op, "desc": a.desc, "mode": n, "R": R, "tile": h.info.tile_nnz, "ms": round(ms, 4),
                               "gnnz_s": round(nnz / ms / 1e6, 2), "hbm_frac": round(b / (ms / 1e3) / 1e9 / peak, 4)}),
                   flush=True)
         h.destroy()
