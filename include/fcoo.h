@@ -77,7 +77,7 @@ typedef struct {
 /* Build options.  NULL -> {FCOO_OP_MTTKRP, 0 (automatic), 0}.
  * tile_nnz = T, the partition length ("threadlen", P:L272 / P:L426): a multiple of 32 in
  * [32, 8192], or 0 = automatic (enough tiles to fill the GPU ~4x at R=32: about nnz/37888,
- * rounded to a multiple of 32 and clamped to [32, 2048]; fcoo_info reports the value used).
+ * rounded to the nearest power of two in [32, 2048]; fcoo_info reports the value used).
  * sf has one bit per tile; one GPU lane-group processes one tile. */
 typedef struct {
   int op;          /* fcoo_op */

@@ -154,12 +154,14 @@ void free_handle_arrays(fcoo_s* f) {
 
 // Automatic tile length (tile_nnz == 0): enough tiles that the MTTKRP/TTM launch fills the GPU
 // about four times over at R=32 (148 SMs x 16 resident warps x 4 lane-groups per warp x 4 waves),
-// rounded to a multiple of 32 in [32, 2048].  Large tensors get T = 2048 (the measured optimum for
-// nell-2, profiles/round1/README.md); brainq-sized ones ~256, where short fibres need more groups.
+// rounded to the nearest power of two in [32, 2048] (power-of-two tiles measured 5-12% faster than
+// neighbouring multiples of 32, profiles/round1/README.md).  Large tensors get T = 2048 (nell-2);
+// brainq-sized ones 256, where short fibres need more lane-groups in flight.
 int auto_tile(int64_t nnz) {
-  const int64_t groups = 148LL * 16 * 4 * 4;
-  int64_t t = (nnz / groups + 16) / 32 * 32;
-  return (int)std::min<int64_t>(2048, std::max<int64_t>(32, t));
+  const double x = (double)nnz / (148.0 * 16 * 4 * 4);
+  int t = 32;
+  while (t < 2048 && (double)t * 1.41421356 < x) t <<= 1;
+  return t;
 }
 
 // Host-side mode taxonomy (Table I) and key layout; used by fcoo_build.
