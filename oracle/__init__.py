@@ -49,6 +49,7 @@ def _load():
         L.orc_mode_spec_ex.argtypes = [ci, vp, ci, ci, ci, vp, vp, vp, vp]
         L.orc_mttkrp.argtypes = [ci, vp, i64, vp, vp, ci, vp, ci, vp, vp, ci]
         L.orc_ttm.argtypes = [ci, vp, i64, vp, vp, ci, vp, ci, vp, vp, vp, vp]
+        L.orc_ttmc.argtypes = [ci, vp, i64, vp, vp, ci, vp, vp, vp, vp]
         L.orc_gram.argtypes = [i64, ci, vp, vp]
         L.orc_pinv_sym.argtypes = [ci, vp, vp]
         L.orc_normalize.argtypes = [i64, ci, vp, vp]
@@ -164,6 +165,26 @@ def ttm(dims, idx, val, mode: int, U):
         raise OracleError(rc, "ttm")
     n = nf.value
     return coords[:n].copy(), Y[:n].copy(), D[:n].copy()
+
+
+def ttmc(dims, idx, val, mode: int, factors, with_D: bool = True):
+    """SpTTMc, Eq.(4): returns (Y, D) fp64 I_mode x prod_{m != mode} R_m (Kronecker of the other
+    modes' rows in ascending mode order; factors[mode] may be None)."""
+    L = _load()
+    d, idx, val = _coo(dims, idx, val)
+    order = len(d)
+    fs = [np.ascontiguousarray(f, dtype=np.float32) if f is not None else np.zeros((1, 1), np.float32)
+          for f in factors]
+    ranks = np.array([f.shape[1] for f in fs], np.int32)
+    W = int(np.prod([ranks[m] for m in range(order) if m != mode]))
+    ptrs = (ctypes.c_void_p * order)(*[_ptr(f) for f in fs])
+    Y = np.zeros((int(d[mode]), W), np.float64)
+    D = np.zeros_like(Y) if with_D else None
+    rc = L.orc_ttmc(order, _ptr(d), val.shape[0], _ptr(idx), _ptr(val), mode, ptrs, _ptr(ranks), _ptr(Y),
+                    _ptr(D) if with_D else None)
+    if rc:
+        raise OracleError(rc, "ttmc")
+    return Y, D
 
 
 def gram(A):

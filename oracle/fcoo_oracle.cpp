@@ -278,6 +278,53 @@ int orc_ttm(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, co
 }
 
 /* ------------------------------------------------------------------------- */
+/* SpTTMc, Eq.(4), Table I row 3: for mode n,
+ *   Y_(n)(i_n, :) += X(i) * (U_{m1}(i_{m1}, :) (x) U_{m2}(i_{m2}, :) (x) ...)
+ * over the other modes m1 < m2 < ... in ascending mode order (Eq.(4) writes U_2(j,:) (x) U_3(k,:)
+ * for mode 1; Kronecker of row vectors per Eq.(1): the first factor varies slowest).
+ * U[m] is fp32 I_m x ranks[m]; Y, D: fp64 I_n x W, W = prod_{m != n} ranks[m]; D may be NULL. */
+int orc_ttmc(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, const float* val, int mode,
+             const float* const* U, const int* ranks, double* Y, double* D) {
+  if (order < 2 || order > 8) return ORC_ERR_ORDER;
+  if (mode < 0 || mode >= order) return ORC_ERR_MODE;
+  int64_t W = 1;
+  int others[8], no = 0;
+  for (int m = 0; m < order; ++m)
+    if (m != mode) {
+      if (ranks[m] < 1) return ORC_ERR_ARG;
+      others[no++] = m;
+      W *= ranks[m];
+    }
+  for (int m = 0; m < order; ++m)
+    for (int64_t q = 0; q < nnz; ++q)
+      if ((int64_t)idx[(int64_t)m * nnz + q] >= dims[m]) return ORC_ERR_INDEX_RANGE;
+  int64_t In = dims[mode];
+  memset(Y, 0, sizeof(double) * (size_t)(In * W));
+  if (D) memset(D, 0, sizeof(double) * (size_t)(In * W));
+  std::vector<double> krow((size_t)W);
+  for (int64_t q = 0; q < nnz; ++q) {
+    /* Kronecker row: entry e = sum_a p_a * prod_{b > a} ranks[others[b]] (last factor fastest) */
+    for (int64_t e = 0; e < W; ++e) {
+      int64_t rem = e;
+      double t = (double)val[q];
+      for (int a = no - 1; a >= 0; --a) {
+        int m = others[a];
+        int64_t p = rem % ranks[m];
+        rem /= ranks[m];
+        t *= (double)U[m][(int64_t)idx[(int64_t)m * nnz + q] * ranks[m] + p];
+      }
+      krow[e] = t;
+    }
+    int64_t i = idx[(int64_t)mode * nnz + q];
+    for (int64_t e = 0; e < W; ++e) {
+      Y[i * W + e] += krow[e];
+      if (D) D[i * W + e] += fabs(krow[e]);
+    }
+  }
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
 /* c4. CP-ALS helpers (Alg. 1). */
 
 /* G = A^T A for A (I x R, fp64 row-major). */
