@@ -131,6 +131,19 @@ fcoo_status fcoo_mttkrp(fcoo_t f, const float* const* factors, int R, float* out
  */
 fcoo_status fcoo_ttm(fcoo_t f, const float* U, int R, float* out, void* stream);
 
+/*
+ * fcoo_ttmc — SpTTMc (tensor times matrix chain, the Tucker/HOOI kernel) on the handle's mode n,
+ * Eq.(4) (Table I row 3): same index-mode segments as SpMTTKRP, Kronecker
+ * instead of Hadamard product of the product-mode rows:
+ *   out(i_n, :) = sum_{nonzeros q of slice i_n} v_q * (U_a(i_a(q), :) (x) U_b(i_b(q), :)),
+ * a < b the two other modes in ascending mode order (Eq.(1) Kronecker layout: column p*R_b + q).
+ *   f: a handle built with FCOO_OP_MTTKRP on an order-3 tensor (else SHAPE / ORDER).
+ *   factors: host array of `order` DEVICE pointers, factors[m] is I_m x ranks[m] fp32 row-major
+ *   (factors[n] ignored).  ranks: host [order]; R_a * R_b <= 1024 (else RANK).
+ *   out: device, I_n x (R_a*R_b) fp32 row-major, overwritten.  Asynchronous.
+ */
+fcoo_status fcoo_ttmc(fcoo_t f, const float* const* factors, const int* ranks, float* out, void* stream);
+
 typedef struct {
   int order, op, mode;
   int n_idx, n_prod;

@@ -96,6 +96,12 @@ fcoo_status fcoo_ttm(fcoo_t f, const float* U, int R, float* out, void* stream) 
   return fcoo::run_ttm(f, U, R, out, (cudaStream_t)stream);
 }
 
+fcoo_status fcoo_ttmc(fcoo_t f, const float* const* factors, const int* ranks, float* out, void* stream) {
+  if (!f || !factors || !ranks || !out) return fcoo::fail(FCOO_ERR_ARG, "NULL handle/factors/ranks/out");
+  if (f->op != FCOO_OP_MTTKRP) return fcoo::fail(FCOO_ERR_SHAPE, "SpTTMc needs a handle built for FCOO_OP_MTTKRP");
+  return fcoo::run_ttmc(f, factors, ranks, out, (cudaStream_t)stream);
+}
+
 fcoo_status fcoo_info(fcoo_t f, fcoo_info_t* info) {
   if (!f || !info) return fcoo::fail(FCOO_ERR_ARG, "NULL handle/info");
   memset(info, 0, sizeof(*info));

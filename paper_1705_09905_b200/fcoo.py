@@ -69,7 +69,7 @@ class _CpOpts(ctypes.Structure):
 
 
 # The exported symbols (every one declared in include/fcoo.h).
-SYMBOLS = ["fcoo_build", "fcoo_mttkrp", "fcoo_ttm", "fcoo_info", "fcoo_export", "fcoo_destroy",
+SYMBOLS = ["fcoo_build", "fcoo_mttkrp", "fcoo_ttm", "fcoo_ttmc", "fcoo_info", "fcoo_export", "fcoo_destroy",
            "fcoo_comm_unique_id", "fcoo_comm_init", "fcoo_comm_destroy", "fcoo_allreduce_sum", "fcoo_set_shard",
            "fcoo_shard_range", "cp_als", "fcoo_status_str", "fcoo_last_error", "fcoo_launch_count"]
 
@@ -89,6 +89,7 @@ def load_library():
                              ctypes.POINTER(vp)]
     L.fcoo_mttkrp.argtypes = [vp, ctypes.POINTER(vp), ci, vp, vp]
     L.fcoo_ttm.argtypes = [vp, vp, ci, vp, vp]
+    L.fcoo_ttmc.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(ci), vp, vp]
     L.fcoo_info.argtypes = [vp, ctypes.POINTER(_Info)]
     L.fcoo_export.argtypes = [vp, ctypes.POINTER(_HostView), vp]
     L.fcoo_destroy.argtypes = [vp]
@@ -273,6 +274,27 @@ def fcoo_ttm(f: Fcoo, U: torch.Tensor, R: int, out: torch.Tensor, stream=None) -
     _require_cuda(out, torch.float32, "out")
     _check(L.fcoo_ttm(f.h, ctypes.c_void_p(U.data_ptr()), R, ctypes.c_void_p(out.data_ptr()),
                       ctypes.c_void_p(_stream_ptr(stream))), "fcoo_ttm")
+    return out
+
+
+def fcoo_ttmc(f: Fcoo, factors, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """SpTTMc (Eq.(4)) on an MTTKRP handle of an order-3 tensor.  factors: list of `order` CUDA fp32
+    (I_m, R_m) tensors (entry [mode] may be None); out: (I_mode, prod of the other R_m)."""
+    L = load_library()
+    ptrs, ranks = [], []
+    for m, U in enumerate(factors):
+        if U is None:
+            ptrs.append(None)
+            ranks.append(0)
+            continue
+        _require_cuda(U, torch.float32, f"factors[{m}]")
+        ptrs.append(U.data_ptr())
+        ranks.append(int(U.shape[1]))
+    _require_cuda(out, torch.float32, "out")
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    rk = (ctypes.c_int * len(ranks))(*ranks)
+    _check(L.fcoo_ttmc(f.h, arr, rk, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))),
+           "fcoo_ttmc")
     return out
 
 
