@@ -36,11 +36,14 @@ def main():
         for R in [int(x) for x in a.R.split(",")]:
             fs = [torch.from_numpy(f).cuda() for f in gen.factors(w.dims, R, 7)]
             rows = h.info.nsegs if a.op == "ttm" else w.dims[n]
-            out = torch.empty((rows, R), device="cuda")
+            width = R * R if a.op == "ttmc" else R  # SpTTMc: R per mode, Kronecker width R^2
+            out = torch.empty((rows, width), device="cuda")
 
             def call():
                 if a.op == "ttm":
                     P.fcoo_ttm(h, fs[n], R, out)
+                elif a.op == "ttmc":
+                    P.fcoo_ttmc(h, fs, out)
                 else:
                     P.fcoo_mttkrp(h, fs, R, out)
 
@@ -57,11 +60,15 @@ def main():
             if a.op == "ttm":  # stream (index + value + bf + sf) + U + semi-sparse output
                 ntl = h.info.ntiles
                 b = nnz * 8 + (nnz + 7) // 8 + 4 * ((ntl + 31) // 32) + 4 * w.dims[n] * R + 4 * h.info.nsegs * R
+            elif a.op == "ttmc":  # stream + the two factors + the I_n x R^2 output
+                b = compulsory_bytes(w.dims, nnz, n, R, h.info.tile_nnz) - 4 * w.dims[n] * R + 4 * w.dims[n] * width
             else:
                 b = compulsory_bytes(w.dims, nnz, n, R, h.info.tile_nnz)
+            flops = {"ttm": 2 * R, "ttmc": 2 * width + 1}.get(a.op, N * R) * nnz
             print(json.dumps({"engine": os.environ.get("FCOO_ENGINE", "default"), "workload": a.workload,
                               "op": a.op, "desc": a.desc, "mode": n, "R": R, "tile": h.info.tile_nnz, "ms": round(ms, 4),
-                              "gnnz_s": round(nnz / ms / 1e6, 2), "hbm_frac": round(b / (ms / 1e3) / 1e9 / peak, 4)}),
+                              "gnnz_s": round(nnz / ms / 1e6, 2), "gflops": round(flops / ms / 1e6, 1),
+                              "hbm_frac": round(b / (ms / 1e3) / 1e9 / peak, 4)}),
                   flush=True)
         h.destroy()
 
