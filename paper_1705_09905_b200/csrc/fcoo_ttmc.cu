@@ -66,42 +66,71 @@ __global__ void __launch_bounds__(256) k_ttmc(const TtmcParams P) {
       }
   };
 
-  uint32_t bfw = 0;
-  for (int64_t p = p0; p < p1; ++p) {
-    if ((p & 31) == 0 || p == p0) bfw = ld_stream4(P.bf + (p >> 5));
-    if ((bfw >> (p & 31)) & 1u) {
-      if (p != p0) flush(own);
+  auto open_segment = [&](int64_t p) {
+    if (p != p0) flush(own);
 #pragma unroll
-      for (int u = 0; u < NS; ++u) acc[u] = 0.f;
-      own = true;
-      ++s;
-      row = P.seg_coord ? P.seg_coord[s] : s;
-    }
-    const float v = __uint_as_float(ld_stream4(P.val + p));
-    const uint32_t ia = ld_stream4(P.pa + p), ib = ld_stream4(P.pb + p);
+    for (int u = 0; u < NS; ++u) acc[u] = 0.f;
+    own = true;
+    ++s;
+    row = P.seg_coord ? P.seg_coord[s] : s;
+  };
+  // one nonzero: gathers into registers, then NS FFMAs
+  auto gather = [&](uint32_t ia, uint32_t ib, float (&ga)[FAST ? 1 : NS], float (&gb)[NS]) {
     const float* ra = P.Ua + (size_t)ia * (uint32_t)P.Ra;
     const float* rb = P.Ub + (size_t)ib * (uint32_t)P.Rb;
     if constexpr (FAST) {  // shared outer index, contiguous inner run
-      const float va = ok[0] ? v * __ldg(ra + pcol[0]) : 0.f;
+      ga[0] = __ldg(ra + pcol[0]);
       if constexpr (NS % 4 == 0) {
 #pragma unroll
         for (int u = 0; u < NS; u += 4) {
           const float4 b = __ldg(reinterpret_cast<const float4*>(rb + qcol[0] + u));
-          acc[u] = fmaf(va, b.x, acc[u]);
-          acc[u + 1] = fmaf(va, b.y, acc[u + 1]);
-          acc[u + 2] = fmaf(va, b.z, acc[u + 2]);
-          acc[u + 3] = fmaf(va, b.w, acc[u + 3]);
+          gb[u] = b.x; gb[u + 1] = b.y; gb[u + 2] = b.z; gb[u + 3] = b.w;
         }
       } else {
 #pragma unroll
-        for (int u = 0; u < NS; ++u)
-          if (ok[u]) acc[u] = fmaf(va, __ldg(rb + qcol[u]), acc[u]);
+        for (int u = 0; u < NS; ++u) gb[u] = __ldg(rb + qcol[u]);
       }
     } else {
 #pragma unroll
-      for (int u = 0; u < NS; ++u)
-        if (ok[u]) acc[u] = fmaf(v * __ldg(ra + pcol[u]), __ldg(rb + qcol[u]), acc[u]);
+      for (int u = 0; u < NS; ++u) {
+        ga[u] = __ldg(ra + pcol[u]);
+        gb[u] = __ldg(rb + qcol[u]);
+      }
     }
+  };
+  auto accumulate = [&](float v, const float (&ga)[FAST ? 1 : NS], const float (&gb)[NS]) {
+#pragma unroll
+    for (int u = 0; u < NS; ++u) acc[u] = fmaf(v * ga[FAST ? 0 : u], gb[u], acc[u]);
+  };
+
+  // batches of B nonzeros: indices/values with 128-bit stream loads, every gather of the batch in
+  // flight before the FMAs, segment heads tested once per batch
+  constexpr int RP = FAST ? NS + 1 : 2 * NS;  // gathered registers per nonzero
+  constexpr int B = RP * 8 <= 96 ? 8 : RP * 4 <= 96 ? 4 : RP * 2 <= 96 ? 2 : 1;
+  const int64_t pfull = p0 + ((p1 - p0) / B) * B;
+  uint32_t bfw = 0;
+  for (int64_t pb = p0; pb < pfull; pb += B) {
+    if (((pb - p0) & 31) == 0) bfw = ld_stream4(P.bf + (pb >> 5));
+    uint32_t ia[B], ib[B], vb[B];
+    ld_batch<B>(P.pa + pb, ia);
+    ld_batch<B>(P.pb + pb, ib);
+    ld_batch<B>(P.val + pb, vb);
+    const uint32_t heads = (bfw >> ((pb - p0) & 31)) & ((1u << B) - 1u);
+    float ga[B][FAST ? 1 : NS], gb[B][NS];
+#pragma unroll
+    for (int e = 0; e < B; ++e) gather(ia[e], ib[e], ga[e], gb[e]);
+#pragma unroll
+    for (int e = 0; e < B; ++e) {
+      if (heads && ((heads >> e) & 1u)) open_segment(pb + e);
+      accumulate(__uint_as_float(vb[e]), ga[e], gb[e]);
+    }
+  }
+  for (int64_t p = pfull; p < p1; ++p) {  // ragged tail of the tensor's last tile
+    if ((p & 31) == 0 || p == pfull) bfw = ld_stream4(P.bf + (p >> 5));
+    if ((bfw >> (p & 31)) & 1u) open_segment(p);
+    float ga[FAST ? 1 : NS], gb[NS];
+    gather(ld_stream4(P.pa + p), ld_stream4(P.pb + p), ga, gb);
+    accumulate(__uint_as_float(ld_stream4(P.val + p)), ga, gb);
   }
   const bool right_open = (t + 1 < P.ntiles) && !((P.sf[(t + 1) >> 5] >> ((t + 1) & 31)) & 1u);
   flush(own && !right_open);
