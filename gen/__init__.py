@@ -108,6 +108,8 @@ WORKLOADS = {
     "netflix": Workload("netflix", (480189, 17770, 2182), 100480507, (0.5, 0.5, 0.2), 103),
     "brainq": Workload("brainq", (60, 70000, 9), 11000000, (0.0, 0.0, 0.0), 104),
     "order4": Workload("order4", (500000, 20000, 2000, 1000), 150000000, (0.5, 0.5, 0.5, 0.5), 105),
+    # SURVEY §8(d) "stress variant": heavy power law, one slice of ~7M nonzeros (reading Q16)
+    "netflix_stress": Workload("netflix_stress", (480189, 17770, 2182), 100480507, (1.0, 1.0, 0.5), 106),
 }
 
 

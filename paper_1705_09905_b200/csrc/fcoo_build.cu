@@ -4,7 +4,8 @@
 //   k_pack_keys   validate coordinates, pack one u64 sort key per nonzero:
 //                 index modes (ascending mode id) most significant, then the product modes in
 //                 ascending-extent order (reading Q5); ord = input ordinal
-//   CUB onesweep radix sort of (key, ord) over the key bits actually used (stable)
+//   CUB onesweep radix sort of (key, payload) over the key bits actually used (stable); the
+//                 payload is the value's bits, or the input ordinal when KEEP_PERM asks for perm
 //   k_flags       bf word per 32 nonzeros by warp ballot (head = index bits differ from the
 //                 previous key; reading Q1), duplicate detection (Q6), unpack product
 //                 indices from the key, gather values by ord, per-word head counts
@@ -37,8 +38,10 @@ struct IdxPtrs {
   const uint32_t* p[kMaxOrder];
 };
 
-__global__ void k_pack_keys(IdxPtrs idx, KeyLayout L, int64_t nnz, uint64_t* __restrict__ keys,
-                            uint32_t* __restrict__ ord, uint32_t* __restrict__ err) {
+// payload: the input ordinal (KEEP_PERM builds) or the value's bits (val_in != nullptr), so the
+// radix sort carries the values along and the flags kernel needs no random gather
+__global__ void k_pack_keys(IdxPtrs idx, KeyLayout L, int64_t nnz, const float* __restrict__ val_in,
+                            uint64_t* __restrict__ keys, uint32_t* __restrict__ ord, uint32_t* __restrict__ err) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nnz) return;
   uint64_t key = 0;
@@ -53,7 +56,7 @@ __global__ void k_pack_keys(IdxPtrs idx, KeyLayout L, int64_t nnz, uint64_t* __r
   }
   if (bad) atomicOr(err, ERRF_INDEX_RANGE);
   keys[q] = key;
-  ord[q] = (uint32_t)q;
+  ord[q] = val_in ? __float_as_uint(val_in[q]) : (uint32_t)q;
 }
 
 __device__ __forceinline__ uint64_t index_part(uint64_t key, int prod_bits) {
@@ -82,9 +85,13 @@ __global__ void k_flags(const uint64_t* __restrict__ keys, const uint32_t* __res
       int ka = L.n_idx + a;
       pidx[(int64_t)a * nnz_pad + p] = (uint32_t)((key >> L.shift[ka]) & L.mask[ka]);
     }
-    uint32_t o = ord[p];
-    val[p] = val_in[o];
-    if (perm) perm[p] = o;
+    uint32_t o = ord[p];  // input ordinal (perm != nullptr) or the sorted value's bits
+    if (perm) {
+      val[p] = val_in[o];
+      perm[p] = o;
+    } else {
+      val[p] = __uint_as_float(o);
+    }
   } else {
     for (int a = 0; a < n_prod; ++a) pidx[(int64_t)a * nnz_pad + p] = 0u;
     val[p] = 0.0f;
@@ -266,7 +273,9 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
       return bail(fail(FCOO_ERR_CUDA, "memset: %s", cudaGetErrorString(ce)));
 
     const int TB = 256;
-    k_pack_keys<<<(unsigned)((nnz + TB - 1) / TB), TB, 0, s>>>(ip, L, nnz, keys0.as<uint64_t>(), ord0.as<uint32_t>(),
+    const bool keep_perm = (flags & FCOO_BUILD_KEEP_PERM) != 0;
+    k_pack_keys<<<(unsigned)((nnz + TB - 1) / TB), TB, 0, s>>>(ip, L, nnz, keep_perm ? nullptr : coo->val,
+                                                               keys0.as<uint64_t>(), ord0.as<uint32_t>(),
                                                                errb.as<uint32_t>());
     count_launch();
     if ((ce = cudaGetLastError()) != cudaSuccess) return bail(fail(FCOO_ERR_CUDA, "k_pack_keys: %s", cudaGetErrorString(ce)));

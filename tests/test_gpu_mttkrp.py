@@ -130,3 +130,19 @@ def test_nell2_shaped_full_size(F):
         got = _run(F, w.dims, idx, val, mode, fs, 32, 2048)
         M, D = oracle.mttkrp(w.dims, idx, val, mode, fs, nthreads=os.cpu_count() or 8)
         assert_parity(got, M, D, what=f"nell2 mode {mode}")
+
+
+def test_netflix_stress_giant_slice(F):
+    """Reading Q16 at scale: heavy power law (alpha 1.0/1.0/0.5), 100M nonzeros, the largest slice
+    holds millions of nonzeros spread over thousands of tiles (boundary red.add on one row);
+    every mode, R=32, parity per element against the multi-threaded oracle."""
+    import os
+    w = gen.WORKLOADS["netflix_stress"]
+    idx, val = gen.coo(w.dims, w.nnz, w.alpha, w.seed)
+    biggest = int(np.bincount(idx[0]).max())
+    assert biggest > 1_000_000
+    for mode in range(3):
+        fs = gen.factors(w.dims, 32, 8)
+        got = _run(F, w.dims, idx, val, mode, fs, 32, 0)
+        M, D = oracle.mttkrp(w.dims, idx, val, mode, fs, nthreads=os.cpu_count() or 8)
+        assert_parity(got, M, D, what=f"netflix stress mode {mode}")
