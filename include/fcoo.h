@@ -73,10 +73,6 @@ typedef struct {
  * the default ascending order of reading Q5: the last (per-nonzero random) product mode is then
  * the smallest factor.  Same segments, same sum, another canonical permutation. */
 #define FCOO_BUILD_PRODUCT_DESC 2u
-/* Do not tag hot rows.  By default the build ranks the rows of every product mode by how often
- * they occur and tags the entries of the 4096 most frequent ones, so the kernels can keep those
- * rows in L1; the tags are internal — fcoo_export returns plain indices. */
-#define FCOO_BUILD_NO_HOT 4u
 
 /* Build options.  NULL -> {FCOO_OP_MTTKRP, 0 (automatic), 0}.
  * tile_nnz = T, the partition length ("threadlen", P:L272 / P:L426): a multiple of 32 in

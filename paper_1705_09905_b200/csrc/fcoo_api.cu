@@ -4,7 +4,6 @@
 #include <string.h>
 
 #include <algorithm>
-#include <vector>
 
 #include "fcoo_internal.cuh"
 
@@ -118,7 +117,7 @@ fcoo_status fcoo_info(fcoo_t f, fcoo_info_t* info) {
   info->storage_bytes = (4 * (int64_t)f->n_prod + 4) * f->nnz + (f->nnz + 7) / 8 + 4 * ((f->ntiles + 31) / 32);
   info->seg_table_bytes = 4 * (f->ntiles + 1) + 4 * f->nsegs * f->n_idx;
   info->device_bytes = (int64_t)(f->bytes_pidx + f->bytes_val + f->bytes_bf + f->bytes_sf + f->bytes_seg_base +
-                                 f->bytes_seg_coord + f->bytes_perm + f->bytes_hot_rows + f->bytes_uhot);
+                                 f->bytes_seg_coord + f->bytes_perm);
   info->shard = f->shard; info->nshards = f->nshards;
   info->tile_begin = f->tile_begin; info->tile_end = f->tile_end;
   return FCOO_OK;
@@ -141,16 +140,7 @@ fcoo_status fcoo_export(fcoo_t f, fcoo_host_view* v, void* stream) {
     for (int a = 0; a < f->n_prod; ++a)
       FCOO_CUDA_TRY(cudaMemcpyAsync(v->pidx + a * nnz, f->pidx + a * f->nnz_pad, 4 * nnz, cudaMemcpyDeviceToHost, s));
   if (v->val) FCOO_CUDA_TRY(cudaMemcpyAsync(v->val, f->val, 4 * nnz, cudaMemcpyDeviceToHost, s));
-  std::vector<uint32_t> hot((size_t)f->n_prod * fcoo::kHot);
-  if (v->pidx && f->hot_rows)
-    FCOO_CUDA_TRY(cudaMemcpyAsync(hot.data(), f->hot_rows, 4 * hot.size(), cudaMemcpyDeviceToHost, s));
   FCOO_CUDA_TRY(cudaStreamSynchronize(s));
-  if (v->pidx && f->hot_rows)  // hot-row tags are internal: return the plain product indices
-    for (int a = 0; a < f->n_prod; ++a)
-      for (int64_t p = 0; p < nnz; ++p) {
-        uint32_t& w = v->pidx[a * nnz + p];
-        if (w & fcoo::kHotTag) w = hot[(size_t)a * fcoo::kHot + (w & ~fcoo::kHotTag)];
-      }
   return FCOO_OK;
 }
 

@@ -132,27 +132,6 @@ __global__ void k_seg_coord(const uint64_t* __restrict__ keys, const uint32_t* _
   for (int a = 0; a < L.n_idx; ++a) seg_coord[(int64_t)s * L.n_idx + a] = (uint32_t)((key >> L.shift[a]) & L.mask[a]);
 }
 
-// ---- hot-row tagging ----
-__global__ void k_hist(const uint32_t* __restrict__ pidx, int64_t nnz, uint32_t* __restrict__ counts) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p < nnz) atomicAdd(&counts[pidx[p]], 1u);
-}
-__global__ void k_iota(uint32_t* __restrict__ v, int64_t n) {
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i < n) v[i] = (uint32_t)i;
-}
-// rank_of[row] = rank for the H hottest rows (rank_of pre-filled with 0xffffffff)
-__global__ void k_rank(const uint32_t* __restrict__ rows_sorted, int H, uint32_t* __restrict__ rank_of) {
-  int r = blockIdx.x * blockDim.x + threadIdx.x;
-  if (r < H) rank_of[rows_sorted[r]] = (uint32_t)r;
-}
-__global__ void k_tag(uint32_t* __restrict__ pidx, int64_t nnz, const uint32_t* __restrict__ rank_of) {
-  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= nnz) return;
-  const uint32_t r = rank_of[pidx[p]];
-  if (r != 0xffffffffu) pidx[p] = kHotTag | r;
-}
-
 int bits_for(int64_t n) {
   int b = 0;
   while (b < 63 && ((int64_t)1 << b) < n) ++b;
@@ -174,11 +153,8 @@ void free_handle_arrays(fcoo_s* f) {
   if (f->seg_base) f->alloc.put(f->seg_base, f->bytes_seg_base, s);
   if (f->seg_coord) f->alloc.put(f->seg_coord, f->bytes_seg_coord, s);
   if (f->perm) f->alloc.put(f->perm, f->bytes_perm, s);
-  if (f->hot_rows) f->alloc.put(f->hot_rows, f->bytes_hot_rows, s);
-  if (f->uhot) f->alloc.put(f->uhot, f->bytes_uhot, s);
   f->pidx = nullptr; f->val = nullptr; f->bf = nullptr; f->sf = nullptr;
   f->seg_base = nullptr; f->seg_coord = nullptr; f->perm = nullptr;
-  f->hot_rows = nullptr; f->uhot = nullptr;
 }
 
 }  // namespace
@@ -222,8 +198,6 @@ fcoo_status plan_modes(fcoo_s* f, int order, const int64_t* dims, int op, int mo
   f->n_idx = ni; f->n_prod = np;
   return FCOO_OK;
 }
-
-fcoo_status tag_hot_rows(fcoo_s* f, cudaStream_t s);
 
 fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opts, const fcoo_allocator* alloc,
                        cudaStream_t s, fcoo_t* out) {
@@ -360,55 +334,7 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
     count_launch();
     if ((ce = cudaGetLastError()) != cudaSuccess) return bail(fail(FCOO_ERR_CUDA, "k_seg_coord: %s", cudaGetErrorString(ce)));
   }  // scratch freed (stream-ordered)
-  if (!(flags & FCOO_BUILD_NO_HOT)) {
-    fcoo_status hs = tag_hot_rows(f, s);
-    if (hs) return bail(hs);
-  }
   *out = f;
-  return FCOO_OK;
-}
-
-// Tag the kHot most frequent rows of every product position: a stable
-// radix sort of the per-row counts (descending; ties keep ascending row id) ranks the rows, and
-// every pidx entry of a top-kHot row becomes kHotTag | rank.  The kernels read those rows from a
-// per-call contiguous copy with an L1-retaining load and every other row without L1 allocation.
-fcoo_status tag_hot_rows(fcoo_s* f, cudaStream_t s) {
-  const int TB = 256;
-  f->hot_rows = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)f->n_prod * kHot, s, &f->bytes_hot_rows);
-  if (!f->hot_rows) return fail(FCOO_ERR_OOM, "hot_rows");
-  for (int a = 0; a < f->n_prod; ++a) {
-    const int64_t I = f->dims[f->prod_modes[a]];
-    f->hot_n[a] = 0;
-    if (I >= (int64_t)kHotTag || I < 2) continue;  // tags need the top index bit free
-    const int H = (int)std::min<int64_t>(I, kHot);
-    uint32_t* pa = f->pidx + (int64_t)a * f->nnz_pad;
-    Buf cnt(&f->alloc, 4 * I, s), cnt2(&f->alloc, 4 * I, s), rows(&f->alloc, 4 * I, s), rows2(&f->alloc, 4 * I, s);
-    if (!cnt.ok() || !cnt2.ok() || !rows.ok() || !rows2.ok()) return fail(FCOO_ERR_OOM, "hot-row scratch");
-    FCOO_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, 4 * I, s));
-    k_hist<<<(unsigned)((f->nnz + TB - 1) / TB), TB, 0, s>>>(pa, f->nnz, cnt.as<uint32_t>());
-    FCOO_LAUNCH_CHECK();
-    k_iota<<<(unsigned)((I + TB - 1) / TB), TB, 0, s>>>(rows.as<uint32_t>(), I);
-    FCOO_LAUNCH_CHECK();
-    size_t tb = 0;
-    cub::DeviceRadixSort::SortPairsDescending(nullptr, tb, cnt.as<uint32_t>(), cnt2.as<uint32_t>(), rows.as<uint32_t>(),
-                                              rows2.as<uint32_t>(), (int64_t)I, 0, 32, s);
-    {
-      Buf tmp(&f->alloc, tb, s);
-      if (!tmp.ok()) return fail(FCOO_ERR_OOM, "hot-row sort scratch");
-      FCOO_CUDA_TRY(cub::DeviceRadixSort::SortPairsDescending(tmp.p, tb, cnt.as<uint32_t>(), cnt2.as<uint32_t>(),
-                                                              rows.as<uint32_t>(), rows2.as<uint32_t>(), (int64_t)I,
-                                                              0, 32, s));
-      count_launch(4);
-    }
-    FCOO_CUDA_TRY(cudaMemcpyAsync(f->hot_rows + (int64_t)a * kHot, rows2.p, 4 * (size_t)H, cudaMemcpyDeviceToDevice, s));
-    uint32_t* rank_of = cnt.as<uint32_t>();  // reuse: counts are no longer needed
-    FCOO_CUDA_TRY(cudaMemsetAsync(rank_of, 0xff, 4 * I, s));
-    k_rank<<<(unsigned)((H + TB - 1) / TB), TB, 0, s>>>(rows2.as<uint32_t>(), H, rank_of);
-    FCOO_LAUNCH_CHECK();
-    k_tag<<<(unsigned)((f->nnz + TB - 1) / TB), TB, 0, s>>>(pa, f->nnz, rank_of);
-    FCOO_LAUNCH_CHECK();
-    f->hot_n[a] = H;
-  }
   return FCOO_OK;
 }
 

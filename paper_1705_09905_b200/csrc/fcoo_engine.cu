@@ -20,36 +20,6 @@ __global__ void k_zero_boundary_rows(const uint32_t* __restrict__ sf, const uint
   for (int c = 0; c < R; ++c) o[c] = ACC(0);
 }
 
-__global__ void k_gather_hot(const float* __restrict__ U, int R, const uint32_t* __restrict__ rows, int H,
-                             float* __restrict__ dst) {
-  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= (int64_t)H * R) return;
-  const int64_t r = e / R, c = e % R;
-  dst[e] = U[(int64_t)rows[r] * R + c];
-}
-
-fcoo_status prepare_hot(fcoo_s* f, const float* const* U, const int* R, const float** Uh, cudaStream_t s) {
-  size_t need = 0;
-  for (int a = 0; a < f->n_prod; ++a) need += sizeof(float) * (size_t)f->hot_n[a] * R[a] + 16;
-  if (need > f->bytes_uhot) {
-    if (f->uhot) f->alloc.put(f->uhot, f->bytes_uhot, s);
-    f->uhot = reinterpret_cast<float*>(f->alloc.get(need, s));
-    f->bytes_uhot = f->uhot ? need : 0;
-    if (!f->uhot) return fail(FCOO_ERR_OOM, "hot-row buffer");
-  }
-  float* dst = f->uhot;
-  for (int a = 0; a < f->n_prod; ++a) {
-    Uh[a] = nullptr;
-    if (f->hot_n[a] == 0) continue;
-    const int64_t n = (int64_t)f->hot_n[a] * R[a];
-    k_gather_hot<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(U[a], R[a], f->hot_rows + (int64_t)a * kHot, f->hot_n[a], dst);
-    FCOO_LAUNCH_CHECK();
-    Uh[a] = dst;
-    dst += (n + 3) / 4 * 4;  // keep every copy 16-byte aligned for float4 rows
-  }
-  return FCOO_OK;
-}
-
 namespace {
 
 template <class ACC>
@@ -101,10 +71,6 @@ fcoo_status mttkrp_t(fcoo_s* f, const float* const* factors, int R, ACC* out, cu
   P.seg_coord = f->dense_rows ? nullptr : f->seg_coord;
   P.nnz = f->nnz; P.ntiles = f->ntiles; P.tile_begin = f->tile_begin; P.tile_end = f->tile_end;
   P.T = (int)f->T; P.R = R; P.out = out;
-  int Rs[kMaxProd];
-  for (int a = 0; a < f->n_prod; ++a) Rs[a] = R;
-  fcoo_status hs = prepare_hot(f, P.U, Rs, P.Uh, s);
-  if (hs) return hs;
   // all rows are segments (dense_rows): only tile-crossing rows need zeroing
   fcoo_status st = prepare_output<ACC>(f, R, out, f->dims[f->mode], f->dense_rows != 0, s);
   if (st) return st;
@@ -134,8 +100,6 @@ fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s
   P.seg_coord = nullptr;  // output row = fibre (segment) ordinal
   P.nnz = f->nnz; P.ntiles = f->ntiles; P.tile_begin = f->tile_begin; P.tile_end = f->tile_end;
   P.T = (int)f->T; P.R = R; P.out = out;
-  fcoo_status hs = prepare_hot(f, P.U, &R, P.Uh, s);
-  if (hs) return hs;
   fcoo_status st = prepare_output<float>(f, R, out, f->nsegs, true, s);
   if (st) return st;
   cudaError_t e = launch_engine<float>(P, 1, vec_ok, s);

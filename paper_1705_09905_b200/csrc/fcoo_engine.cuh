@@ -17,18 +17,7 @@ struct EngineParams {
   int64_t nnz, ntiles, tile_begin, tile_end;
   int T, R;
   void* out;  // float* (fp32 accumulation) or double* (fp64 accumulation)
-  // hot rows: a product index kHotTag | r reads row r of Uh[a] (the r-th most frequent row of
-  // U[a], gathered per call); nullptr when the position has no tags
-  const float* Uh[kMaxProd];
 };
-
-// Row address of product index w: tagged hot rows come from the contiguous hot copy.
-__device__ __forceinline__ const char* row_ptr(const char* cold, const char* hot, uint32_t w, uint32_t rowb) {
-  return (w & kHotTag) ? hot + (size_t)(w & ~kHotTag) * rowb : cold + (size_t)w * rowb;
-}
-
-// Per call: gather the hot rows of every tagged product position into f->uhot (fcoo_engine.cu).
-fcoo_status prepare_hot(fcoo_s* f, const float* const* U, const int* R, const float** Uh, cudaStream_t s);
 
 // Launch the segmented-reduction kernel for NP product modes, accumulator type ACC (instantiated
 // in fcoo_engine_np<NP>.cu so the template instances compile in parallel).

@@ -319,14 +319,10 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
   }
   // per-lane base pointers: factor a, column slot c
   const char* ub[NP][CPL];
-  const char* ubh[NP][CPL];  // hot-row copies (row_ptr)
 #pragma unroll
   for (int a = 0; a < NP; ++a)
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      ub[a][c] = reinterpret_cast<const char*>(P.U[a] + (cok[c] ? col[c] : 0));
-      ubh[a][c] = P.Uh[a] ? reinterpret_cast<const char*>(P.Uh[a] + (cok[c] ? col[c] : 0)) : ub[a][c];
-    }
+    for (int c = 0; c < CPL; ++c) ub[a][c] = reinterpret_cast<const char*>(P.U[a] + (cok[c] ? col[c] : 0));
 
   const int64_t p0 = t * (int64_t)P.T;
   const int64_t p1 = min(p0 + (int64_t)P.T, P.nnz);
@@ -375,7 +371,7 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
       for (int a = 0; a < NP; ++a)
 #pragma unroll
         for (int c = 0; c < CPL; ++c)
-          r[e][c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(row_ptr(ub[a][c], ubh[a][c], ix[a][e], rowb))) : V::zero();
+          r[e][c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(ub[a][c] + (size_t)ix[a][e] * rowb)) : V::zero();
     if (heads == 0) {
 #pragma unroll
       for (int e = 0; e < B; ++e)
@@ -403,7 +399,7 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
       uint32_t i = ld_stream4(P.pidx[a] + p);
 #pragma unroll
       for (int c = 0; c < CPL; ++c)
-        r1[c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(row_ptr(ub[a][c], ubh[a][c], i, rowb))) : V::zero();
+        r1[c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(ub[a][c] + (size_t)i * rowb)) : V::zero();
     }
 #pragma unroll
     for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], v, r1[c]);
@@ -442,14 +438,10 @@ __global__ void __launch_bounds__(256) k_segreduce_fact(const EngineParams P) {
     cok[c] = FULL || col[c] < R;
   }
   const char* ub[NP][CPL];
-  const char* ubh[NP][CPL];  // hot-row copies (row_ptr)
 #pragma unroll
   for (int a = 0; a < NP; ++a)
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      ub[a][c] = reinterpret_cast<const char*>(P.U[a] + (cok[c] ? col[c] : 0));
-      ubh[a][c] = P.Uh[a] ? reinterpret_cast<const char*>(P.Uh[a] + (cok[c] ? col[c] : 0)) : ub[a][c];
-    }
+    for (int c = 0; c < CPL; ++c) ub[a][c] = reinterpret_cast<const char*>(P.U[a] + (cok[c] ? col[c] : 0));
 
   const int64_t p0 = t * (int64_t)P.T;
   const int64_t p1 = min(p0 + (int64_t)P.T, P.nnz);
@@ -507,10 +499,10 @@ __global__ void __launch_bounds__(256) k_segreduce_fact(const EngineParams P) {
     for (int e = 0; e < B; ++e)
 #pragma unroll
       for (int c = 0; c < CPL; ++c) {
-        r[e][c][0] = V::load_if(nr[e] && cok[c], reinterpret_cast<const float*>(row_ptr(ub[0][c], ubh[0][c], ix[0][e], rowb)));
+        r[e][c][0] = V::load_if(nr[e] && cok[c], reinterpret_cast<const float*>(ub[0][c] + (size_t)ix[0][e] * rowb));
 #pragma unroll
         for (int a = 1; a < NP; ++a)
-          r[e][c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(row_ptr(ub[a][c], ubh[a][c], ix[a][e], rowb))) : V::zero();
+          r[e][c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(ub[a][c] + (size_t)ix[a][e] * rowb)) : V::zero();
       }
     if (heads == 0) {  // common case: no segment boundary in the batch, straight-line code
 #pragma unroll
@@ -556,7 +548,7 @@ __global__ void __launch_bounds__(256) k_segreduce_fact(const EngineParams P) {
       uint32_t i = a ? ld_stream4(P.pidx[a] + p) : i0;
 #pragma unroll
       for (int c = 0; c < CPL; ++c)
-        r1[c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(row_ptr(ub[a][c], ubh[a][c], i, rowb))) : V::zero();
+        r1[c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(ub[a][c] + (size_t)i * rowb)) : V::zero();
     }
     if (head || i0 != prev0) {
 #pragma unroll
@@ -626,14 +618,8 @@ struct Stage {
 template <int NP, int G, int VEC, int CPL, class ACC, bool FULL>
 // L1 policy of the factor-row gathers in the staged kernel (see Ld<4>::load_pol): the last
 // product position is the per-nonzero random gather, the others are sorted within a segment.
-// Hot (tagged) rows are loaded with L1::evict_last so the most frequent rows stay resident; cold
-// rows of the random innermost position bypass L1 (no_allocate) instead of evicting them; the
-// sorted outer positions keep the default policy (their runs hit L1 on the next nonzero).
-#ifndef FCOO_L1POL_HOT
-#define FCOO_L1POL_HOT 3
-#endif
 #ifndef FCOO_L1POL_INNER
-#define FCOO_L1POL_INNER 1
+#define FCOO_L1POL_INNER 0
 #endif
 #ifndef FCOO_L1POL_OUTER
 #define FCOO_L1POL_OUTER 0
@@ -664,14 +650,10 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
     cok[c] = FULL || col[c] < R;
   }
   const char* ub[NP][CPL];
-  const char* ubh[NP][CPL];  // hot-row copies (row_ptr)
 #pragma unroll
   for (int a = 0; a < NP; ++a)
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) {
-      ub[a][c] = reinterpret_cast<const char*>(P.U[a] + (cok[c] ? col[c] : 0));
-      ubh[a][c] = P.Uh[a] ? reinterpret_cast<const char*>(P.Uh[a] + (cok[c] ? col[c] : 0)) : ub[a][c];
-    }
+    for (int c = 0; c < CPL; ++c) ub[a][c] = reinterpret_cast<const char*>(P.U[a] + (cok[c] ? col[c] : 0));
 
   const int64_t p0 = t * (int64_t)P.T;
   const int64_t p1 = min(p0 + (int64_t)P.T, P.nnz);
@@ -745,11 +727,10 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
         for (int a = 0; a < NP; ++a)
 #pragma unroll
           for (int c = 0; c < CPL; ++c) {
-            const float* gp = reinterpret_cast<const float*>(row_ptr(ub[a][c], ubh[a][c], ix[a][e], rowb));
+            const float* gp = reinterpret_cast<const float*>(ub[a][c] + (size_t)ix[a][e] * rowb);
             r[e][c][a] = !cok[c] ? V::zero()
-                         : (ix[a][e] & kHotTag) ? V::template load_pol<FCOO_L1POL_HOT>(gp)
-                         : (a == NP - 1)        ? V::template load_pol<FCOO_L1POL_INNER>(gp)
-                                                : V::template load_pol<FCOO_L1POL_OUTER>(gp);
+                         : (a == NP - 1) ? V::template load_pol<FCOO_L1POL_INNER>(gp)
+                                         : V::template load_pol<FCOO_L1POL_OUTER>(gp);
           }
       if (heads == 0) {
 #pragma unroll
@@ -801,7 +782,7 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
       uint32_t i = ld_stream4(P.pidx[a] + p);
 #pragma unroll
       for (int c = 0; c < CPL; ++c)
-        r1[c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(row_ptr(ub[a][c], ubh[a][c], i, rowb))) : V::zero();
+        r1[c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(ub[a][c] + (size_t)i * rowb)) : V::zero();
     }
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {

@@ -12,8 +12,6 @@
 namespace fcoo {
 
 constexpr int kMaxOrder = 8;
-constexpr int kHot = 4096;                // hot rows tagged per product position
-constexpr uint32_t kHotTag = 0x80000000u; // product index = kHotTag | rank for a hot row
 
 // Thread-local detail message for fcoo_last_error().
 void set_error(const char* fmt, ...);
@@ -61,14 +59,8 @@ struct fcoo_s {
   uint32_t* seg_base = nullptr;  // ntiles + 1 (last = nsegs)
   uint32_t* seg_coord = nullptr; // nsegs x n_idx
   uint32_t* perm = nullptr;      // nnz (KEEP_PERM only)
-  // hot-row tags: pidx entries of the kHot most frequent rows of each
-  // product position carry kHotTag | rank; hot_rows[a*kHot + rank] is the original row
-  uint32_t* hot_rows = nullptr;  // n_prod x kHot
-  int hot_n[fcoo::kMaxOrder] = {0};
-  float* uhot = nullptr;         // per call: U_a rows of the hot ranks, n_prod x kHot x R
-  size_t bytes_uhot = 0;
   size_t bytes_pidx = 0, bytes_val = 0, bytes_bf = 0, bytes_sf = 0, bytes_seg_base = 0, bytes_seg_coord = 0,
-         bytes_perm = 0, bytes_hot_rows = 0;
+         bytes_perm = 0;
   // shard
   int shard = 0, nshards = 1;
   int64_t tile_begin = 0, tile_end = 0;

@@ -19,8 +19,6 @@ struct TtmcParams {
   const uint32_t* pb;  // indices of the inner Kronecker mode
   const float* Ua;     // I_a x Ra
   const float* Ub;     // I_b x Rb
-  const float* Uah;    // hot-row copies (row_ptr); equal to Ua / Ub when a position has no tags
-  const float* Ubh;
   int Ra, Rb, W;
   const float* val;
   const uint32_t* bf;
@@ -78,10 +76,8 @@ __global__ void __launch_bounds__(256) k_ttmc(const TtmcParams P) {
   };
   // one nonzero: gathers into registers, then NS FFMAs
   auto gather = [&](uint32_t ia, uint32_t ib, float (&ga)[FAST ? 1 : NS], float (&gb)[NS]) {
-    const float* ra = reinterpret_cast<const float*>(row_ptr(reinterpret_cast<const char*>(P.Ua),
-                                                             reinterpret_cast<const char*>(P.Uah), ia, 4u * P.Ra));
-    const float* rb = reinterpret_cast<const float*>(row_ptr(reinterpret_cast<const char*>(P.Ub),
-                                                             reinterpret_cast<const char*>(P.Ubh), ib, 4u * P.Rb));
+    const float* ra = P.Ua + (size_t)ia * (uint32_t)P.Ra;
+    const float* rb = P.Ub + (size_t)ib * (uint32_t)P.Rb;
     if constexpr (FAST) {  // shared outer index, contiguous inner run
       ga[0] = __ldg(ra + pcol[0]);
       if constexpr (NS % 4 == 0) {
@@ -177,13 +173,6 @@ fcoo_status run_ttmc(fcoo_s* f, const float* const* factors, const int* ranks, f
   P.seg_coord = f->dense_rows ? nullptr : f->seg_coord;
   P.nnz = f->nnz; P.ntiles = f->ntiles; P.tile_begin = f->tile_begin; P.tile_end = f->tile_end;
   P.T = (int)f->T; P.out = out;
-  const float* Us[2] = {a == 0 ? P.Ua : P.Ub, a == 0 ? P.Ub : P.Ua};  // stored product order
-  const int Rs[2] = {a == 0 ? Ra : Rb, a == 0 ? Rb : Ra};
-  const float* Uh[kMaxOrder] = {nullptr};
-  fcoo_status hs = prepare_hot(f, Us, Rs, Uh, s);
-  if (hs) return hs;
-  P.Uah = Uh[a] ? Uh[a] : P.Ua;
-  P.Ubh = Uh[b] ? Uh[b] : P.Ub;
   FCOO_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)f->dims[f->mode] * P.W, s));
   const int ns_needed = (P.W + 31) / 32;
   cudaError_t e;

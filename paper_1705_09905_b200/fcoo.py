@@ -22,7 +22,6 @@ ERR_ARG, ERR_ORDER, ERR_MODE, ERR_INDEX_RANGE, ERR_DUPLICATE, ERR_EMPTY, ERR_KEY
 OP_MTTKRP, OP_TTM = 0, 1
 BUILD_KEEP_PERM = 1
 BUILD_PRODUCT_DESC = 2
-BUILD_NO_HOT = 4
 
 
 class FcooError(RuntimeError):
@@ -243,11 +242,9 @@ class Fcoo:
 
 
 def fcoo_build(coo: Coo, mode: int, op: int = OP_MTTKRP, tile_nnz: int = 0, keep_perm: bool = False,
-               product_desc: bool = False, hot_rows: bool = True, stream=None) -> Fcoo:
+               product_desc: bool = False, stream=None) -> Fcoo:
     L = load_library()
-    flags = ((BUILD_KEEP_PERM if keep_perm else 0) | (BUILD_PRODUCT_DESC if product_desc else 0)
-             | (0 if hot_rows else BUILD_NO_HOT))
-    opts = _BuildOpts(op, tile_nnz, flags)
+    opts = _BuildOpts(op, tile_nnz, (BUILD_KEEP_PERM if keep_perm else 0) | (BUILD_PRODUCT_DESC if product_desc else 0))
     out = ctypes.c_void_p()
     _check(L.fcoo_build(ctypes.byref(coo.c), mode, ctypes.byref(opts), ctypes.byref(_ALLOCATOR),
                         ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out)), "fcoo_build")

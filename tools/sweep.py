@@ -20,7 +20,6 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--op", default="mttkrp")
     ap.add_argument("--desc", action="store_true", help="FCOO_BUILD_PRODUCT_DESC")
-    ap.add_argument("--no-hot", action="store_true", help="FCOO_BUILD_NO_HOT")
     a = ap.parse_args()
     import torch
 
@@ -33,8 +32,7 @@ def main():
     nnz = val.shape[0]
     peak, _ = hbm_peak()
     for n in range(N):
-        h = P.fcoo_build(coo, n, op=P.OP_TTM if a.op == "ttm" else P.OP_MTTKRP, tile_nnz=a.tile, product_desc=a.desc,
-                         hot_rows=not a.no_hot)
+        h = P.fcoo_build(coo, n, op=P.OP_TTM if a.op == "ttm" else P.OP_MTTKRP, tile_nnz=a.tile, product_desc=a.desc)
         for R in [int(x) for x in a.R.split(",")]:
             fs = [torch.from_numpy(f).cuda() for f in gen.factors(w.dims, R, 7)]
             rows = h.info.nsegs if a.op == "ttm" else w.dims[n]
@@ -68,7 +66,7 @@ def main():
                 b = compulsory_bytes(w.dims, nnz, n, R, h.info.tile_nnz)
             flops = {"ttm": 2 * R, "ttmc": 2 * width + 1}.get(a.op, N * R) * nnz
             print(json.dumps({"engine": os.environ.get("FCOO_ENGINE", "default"), "workload": a.workload,
-                              "op": a.op, "desc": a.desc, "hot": not a.no_hot, "mode": n, "R": R, "tile": h.info.tile_nnz, "ms": round(ms, 4),
+                              "op": a.op, "desc": a.desc, "mode": n, "R": R, "tile": h.info.tile_nnz, "ms": round(ms, 4),
                               "gnnz_s": round(nnz / ms / 1e6, 2), "gflops": round(flops / ms / 1e6, 1),
                               "hbm_frac": round(b / (ms / 1e3) / 1e9 / peak, 4)}),
                   flush=True)
