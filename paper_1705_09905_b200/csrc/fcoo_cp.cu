@@ -234,16 +234,21 @@ __global__ void k_solve(GramPtrs G, int order, int n, int R, double* __restrict_
 
 // U[i, b] = sum_a M[i, a] W[a, b]  (fp64 accumulation)
 template <class MT>
-__global__ void k_apply(const MT* __restrict__ M, const double* __restrict__ W, int64_t I, int R,
-                        float* __restrict__ U) {
+__device__ __forceinline__ double row_dot(const MT* m, const double* __restrict__ W, int R, int b) {
+  double s = 0.0;
+  for (int a = 0; a < R; ++a) s += (double)m[a] * W[a * R + b];
+  return s;
+}
+
+// U = M W with M read from the fp32 buffer, or from the fp64 one when *use64 (fit mode gate)
+__global__ void k_apply(const float* __restrict__ M, const double* __restrict__ M64, const int* __restrict__ use64,
+                        const double* __restrict__ W, int64_t I, int R, float* __restrict__ U) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= I * R) return;
   int64_t i = e / R;
   int b = (int)(e % R);
-  const MT* m = M + i * R;
-  double s = 0.0;
-  for (int a = 0; a < R; ++a) s += (double)m[a] * W[a * R + b];
-  U[e] = (float)s;
+  const bool f64 = use64 && *use64;
+  U[e] = (float)(f64 ? row_dot(M64 + i * R, W, R, b) : row_dot(M + i * R, W, R, b));
 }
 
 // part[c][a*R+b] = sum_{i in chunk c} U[i,a] U[i,b]
@@ -321,15 +326,21 @@ __global__ void k_scale(float* __restrict__ U, int64_t I, int R, const double* _
   if (l > 0) U[e] = (float)((double)U[e] / l);
 }
 
-// part[c] = sum_{i in chunk c} sum_r lambda_r M[i,r] U[i,r]   (M accumulated in fp64)
-__global__ void k_inner_partial(const double* __restrict__ M, const float* __restrict__ U,
-                                const double* __restrict__ lam, int64_t I, int R, int64_t rows_per,
-                                double* __restrict__ part) {
+__global__ void k_set_int(int* p, int v0, int v1) { p[0] = v0; p[1] = v1; }
+
+// part[c] = sum_{i in chunk c} sum_r lambda_r M[i,r] U[i,r]   (M from the fp64 buffer when *use64;
+// nothing at all when run_if is given and *run_if == 0)
+__global__ void k_inner_partial(const float* __restrict__ M32, const double* __restrict__ M64,
+                                const int* __restrict__ use64, const int* __restrict__ run_if,
+                                const float* __restrict__ U, const double* __restrict__ lam, int64_t I, int R,
+                                int64_t rows_per, double* __restrict__ part) {
   __shared__ double sh[kCT];
+  if (run_if && *run_if == 0) return;
   const int64_t i0 = (int64_t)blockIdx.x * rows_per, i1 = min(I, i0 + rows_per);
+  const bool f64 = *use64 != 0;
   double s = 0.0;
   for (int64_t e = i0 * R + threadIdx.x; e < i1 * R; e += blockDim.x)
-    s += lam[e % R] * (double)M[e] * (double)U[e];
+    s += lam[e % R] * (f64 ? M64[e] : (double)M32[e]) * (double)U[e];
   s = block_sum(s, sh);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
@@ -343,11 +354,18 @@ __global__ void k_sumsq_partial(const float* __restrict__ v, int64_t n, int64_t 
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// fit = 1 - sqrt(max(0, |X|^2 + |Xhat|^2 - 2 <X,Xhat>)) / |X|   (one CTA)
+// fit = 1 - sqrt(max(0, |X|^2 + |Xhat|^2 - 2 <X,Xhat>)) / |X|   (one CTA).
+// Fit-precision flags g: g[0] = the last mode's main MTTKRP accumulates exact
+// fp64 products (sticky); g[1] = recompute it exactly this iteration.  role 0 (main fit): if the
+// main pass was fp32 and fit >= kExactFit, request the recompute.  role 1 (after the exact
+// recompute; skipped unless g[1]): overwrite the fit and, if still >= kExactFit, make the next
+// iterations' main pass exact.
+constexpr double kExactFit = 0.9;
 __global__ void k_fit(const double* __restrict__ inner_part, int ninner, const double* __restrict__ xsq_part,
                       int nxsq, GramPtrs G, int order, const double* __restrict__ lam, int R,
-                      double* __restrict__ out) {
+                      double* __restrict__ out, int* __restrict__ g, int role) {
   __shared__ double sh[kCT];
+  if (role == 1 && g[1] == 0) return;
   double inner = 0.0, xsq = 0.0, xh = 0.0;
   // fixed-order sums (thread-strided then tree): deterministic
   for (int c = threadIdx.x; c < ninner; c += blockDim.x) inner += inner_part[c];
@@ -362,7 +380,10 @@ __global__ void k_fit(const double* __restrict__ inner_part, int ninner, const d
   xh = block_sum(xh, sh);
   if (threadIdx.x == 0) {
     double r2 = xsq + xh - 2.0 * inner;
-    out[0] = 1.0 - sqrt(r2 > 0 ? r2 : 0.0) / sqrt(xsq);
+    const double fit = 1.0 - sqrt(r2 > 0 ? r2 : 0.0) / sqrt(xsq);
+    out[0] = fit;
+    if (role == 0) g[1] = (g[0] == 0 && fit >= kExactFit) ? 1 : 0;
+    else if (fit >= kExactFit) g[0] = 1;
   }
 }
 
@@ -384,7 +405,8 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
 
   // F-COO for every mode, built once up front
   std::vector<fcoo_t> H(N, nullptr);
-  auto cleanup = [&]() { for (auto h : H) fcoo_destroy(h); };
+  auto cleanup = [&]() { for (auto& h : H) { fcoo_destroy(h); h = nullptr; } };
+  struct Guard { decltype(cleanup)& c; ~Guard() { c(); } } guard{cleanup};  // early returns too
   fcoo_build_opts bo{FCOO_OP_MTTKRP, o->tile_nnz > 0 ? o->tile_nnz : 0, 0u};
   for (int n = 0; n < N; ++n) {
     fcoo_status st = fcoo_build(X, n, &bo, alloc, (void*)s, &H[n]);
@@ -402,11 +424,16 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
   Buf lam(&al, sizeof(double) * R, s), part(&al, sizeof(double) * maxchunks * RR, s);
   Buf ipart(&al, sizeof(double) * maxchunks, s), xpart(&al, sizeof(double) * maxchunks, s);
   Buf fitd(&al, sizeof(double) * (o->iters + 1), s), status(&al, sizeof(int) * 2, s);
+  Buf flags(&al, sizeof(int) * 2, s);  // fit-precision flags g[0], g[1] (see k_fit)
   if (!M.ok() || !M64.ok() || !Gs.ok() || !Graw.ok() || !A.ok() || !Q.ok() || !W.ok() || !lam.ok() || !part.ok() || !ipart.ok() ||
-      !xpart.ok() || !fitd.ok() || !status.ok()) {
-    cleanup();
+      !xpart.ok() || !fitd.ok() || !status.ok() || !flags.ok()) {
     return fail(FCOO_ERR_OOM, "cp_als scratch");
   }
+  // sharded runs keep the last mode exact throughout (one fp64 all-reduce, no gated recompute)
+  const bool sharded = o->comm && o->nranks > 1;
+  int* g = flags.as<int>();
+  k_set_int<<<1, 1, 0, s>>>(g, sharded ? 1 : 0, 0);
+  FCOO_LAUNCH_CHECK();
   GramPtrs gp{};
   for (int m = 0; m < N; ++m) gp.g[m] = Gs.as<double>() + (int64_t)m * RR;
 
@@ -439,11 +466,15 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
     for (int n = 0; n < N && !st; ++n) {
       const int64_t In = X->dims[n];
       const bool last = (n == N - 1);
-      // M = MTTKRP_n; the last mode accumulates in fp64 because the fit's <X, Xhat> is taken
-      // from it; all-reduced across ranks on sharded handles.
-      if (last) {
+      // M = MTTKRP_n.  The fit's <X, Xhat> is taken from the last mode's M, so near fit 1 that
+      // one accumulates exact fp64 products: both launches are enqueued and
+      // the device flag g[0] lets exactly one of them work, with no host synchronisation.
+      if (last && sharded) {
         st = run_mttkrp_f64(H[n], factors, R, M64.as<double>(), s);
-        if (!st && o->comm && o->nranks > 1) st = comm_allreduce_f64(o->comm, M64.as<double>(), (size_t)In * R, s);
+        if (!st) st = comm_allreduce_f64(o->comm, M64.as<double>(), (size_t)In * R, s);
+      } else if (last) {
+        st = run_mttkrp(H[n], factors, R, M.as<float>(), s, g, 0);
+        if (!st) st = run_mttkrp_f64(H[n], factors, R, M64.as<double>(), s, g, 1);
       } else {
         st = fcoo_mttkrp(H[n], factors, R, M.as<float>(), (void*)s);
       }
@@ -455,8 +486,8 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
       k_solve<<<1, kCT, 0, s>>>(gp, N, n, R, A.as<double>(), Q.as<double>(), W.as<double>(), status.as<int>(),
                                 R <= kSmallR ? 1 : 0);
       FCOO_LAUNCH_CHECK();
-      if (last) k_apply<double><<<nblk(In * R), kCT, 0, s>>>(M64.as<double>(), W.as<double>(), In, R, factors[n]);
-      else k_apply<float><<<nblk(In * R), kCT, 0, s>>>(M.as<float>(), W.as<double>(), In, R, factors[n]);
+      k_apply<<<nblk(In * R), kCT, 0, s>>>(M.as<float>(), M64.as<double>(), last ? g : nullptr, W.as<double>(),
+                                           In, R, factors[n]);
       FCOO_LAUNCH_CHECK();
       st = gram(factors[n], In, Graw.as<double>());
       if (st) break;
@@ -473,11 +504,24 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
     const int64_t Il = X->dims[nl];
     int nc = chunks_for(Il);
     int64_t per = (Il + nc - 1) / nc;
-    k_inner_partial<<<nc, kCT, 0, s>>>(M64.as<double>(), factors[nl], lam.as<double>(), Il, R, per, ipart.as<double>());
+    k_inner_partial<<<nc, kCT, 0, s>>>(M.as<float>(), M64.as<double>(), g, nullptr, factors[nl],
+                                       lam.as<double>(), Il, R, per, ipart.as<double>());
     FCOO_LAUNCH_CHECK();
     k_fit<<<1, kCT, 0, s>>>(ipart.as<double>(), nc, xpart.as<double>(), nx, gp, N, lam.as<double>(), R,
-                            fitd.as<double>() + it);
+                            fitd.as<double>() + it, g, 0);
     FCOO_LAUNCH_CHECK();
+    if (!sharded) {
+      // the fp32 fit reached kExactFit: recompute the last mode's M exactly (it depends only on
+      // the other modes' factors, unchanged since) and take the fit again -- all gated on g[1]
+      st = run_mttkrp_f64(H[nl], factors, R, M64.as<double>(), s, g + 1, 1);
+      if (st) break;
+      k_inner_partial<<<nc, kCT, 0, s>>>(M.as<float>(), M64.as<double>(), g + 1, g + 1, factors[nl],
+                                         lam.as<double>(), Il, R, per, ipart.as<double>());
+      FCOO_LAUNCH_CHECK();
+      k_fit<<<1, kCT, 0, s>>>(ipart.as<double>(), nc, xpart.as<double>(), nx, gp, N, lam.as<double>(), R,
+                              fitd.as<double>() + it, g, 1);
+      FCOO_LAUNCH_CHECK();
+    }
     if (iters_done) *iters_done = it + 1;
     if (o->tol > 0) {  // the stopping rule needs the fit on the host every iteration
       double fit = 0.0;

@@ -57,8 +57,11 @@ fcoo_status prepare_output(fcoo_s* f, int R, ACC* out, int64_t rows, bool all_ro
 }  // namespace
 
 template <class ACC>
-fcoo_status mttkrp_t(fcoo_s* f, const float* const* factors, int R, ACC* out, cudaStream_t s) {
+fcoo_status mttkrp_t(fcoo_s* f, const float* const* factors, int R, ACC* out, cudaStream_t s,
+                     const int* gate = nullptr, int gate_on = 0) {
   EngineParams P{};
+  P.gate = gate;
+  P.gate_on = gate_on;
   bool vec_ok = (R % 4 == 0) && R <= 128 && aligned16(out);
   for (int a = 0; a < f->n_prod; ++a) {
     int m = f->prod_modes[a];
@@ -79,16 +82,18 @@ fcoo_status mttkrp_t(fcoo_s* f, const float* const* factors, int R, ACC* out, cu
   return FCOO_OK;
 }
 
-fcoo_status run_mttkrp(fcoo_s* f, const float* const* factors, int R, float* out, cudaStream_t s) {
-  fcoo_status st = mttkrp_t<float>(f, factors, R, out, s);
+fcoo_status run_mttkrp(fcoo_s* f, const float* const* factors, int R, float* out, cudaStream_t s, const int* gate,
+                       int gate_on) {
+  fcoo_status st = mttkrp_t<float>(f, factors, R, out, s, gate, gate_on);
   if (st) return st;
   if (f->comm) return comm_allreduce(f->comm, out, (size_t)f->dims[f->mode] * R, s);
   return FCOO_OK;
 }
 
 // fp64-accumulating MTTKRP (CP-ALS fit mode); sharded handles return the LOCAL partial.
-fcoo_status run_mttkrp_f64(fcoo_s* f, const float* const* factors, int R, double* out, cudaStream_t s) {
-  return mttkrp_t<double>(f, factors, R, out, s);
+fcoo_status run_mttkrp_f64(fcoo_s* f, const float* const* factors, int R, double* out, cudaStream_t s,
+                           const int* gate, int gate_on) {
+  return mttkrp_t<double>(f, factors, R, out, s, gate, gate_on);
 }
 
 fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s) {

@@ -17,7 +17,15 @@ struct EngineParams {
   int64_t nnz, ntiles, tile_begin, tile_end;
   int T, R;
   void* out;  // float* (fp32 accumulation) or double* (fp64 accumulation)
+  // device-side gate (CP-ALS fit mode): when non-null the launch does its work only if
+  // (*gate != 0) == gate_on, so the fp32/fp64 choice needs no host synchronisation
+  const int* gate;
+  int gate_on;
 };
+
+__device__ __forceinline__ bool gated_off(const EngineParams& P) {
+  return P.gate && ((__ldg(P.gate) != 0) != (P.gate_on != 0));
+}
 
 // Launch the segmented-reduction kernel for NP product modes, accumulator type ACC (instantiated
 // in fcoo_engine_np<NP>.cu so the template instances compile in parallel).

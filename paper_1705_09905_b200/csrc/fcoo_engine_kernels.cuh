@@ -306,7 +306,7 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
   constexpr int B = batch_size<NP, VEC, CPL>();  // nonzeros per batch (divides 32)
   const int gl = threadIdx.x % G;
   const int64_t t = P.tile_begin + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-  if (t >= P.tile_end) return;  // groups are lane-aligned: whole groups exit together
+  if (t >= P.tile_end || gated_off(P)) return;  // groups are lane-aligned: whole groups exit together
 
   const int R = P.R;
   const uint32_t rowb = (uint32_t)R * 4u;  // factor row stride in bytes
@@ -426,7 +426,7 @@ __global__ void __launch_bounds__(256) k_segreduce_fact(const EngineParams P) {
   constexpr int B = batch_size<NP, VEC, CPL>();
   const int gl = threadIdx.x % G;
   const int64_t t = P.tile_begin + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-  if (t >= P.tile_end) return;
+  if (t >= P.tile_end || gated_off(P)) return;
 
   const int R = P.R;
   const uint32_t rowb = (uint32_t)R * 4u;
@@ -636,7 +636,7 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
   const int lane = threadIdx.x & 31;
   const int gl = threadIdx.x % G;
   const int64_t t = P.tile_begin + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-  if (t >= P.tile_end) return;
+  if (t >= P.tile_end || gated_off(P)) return;
   const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << (lane & ~(G - 1)));
   uint32_t* my = reinterpret_cast<uint32_t*>(smem_raw) + (threadIdx.x / G) * S::STRIDE;
 

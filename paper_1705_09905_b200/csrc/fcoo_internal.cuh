@@ -72,8 +72,11 @@ struct fcoo_s {
 
 namespace fcoo {
 // engine entry points (fcoo_engine.cu)
-fcoo_status run_mttkrp(fcoo_s* f, const float* const* factors, int R, float* out, cudaStream_t s);
-fcoo_status run_mttkrp_f64(fcoo_s* f, const float* const* factors, int R, double* out, cudaStream_t s);
+// gate (device int, may be null): the launch works only if (*gate != 0) == gate_on
+fcoo_status run_mttkrp(fcoo_s* f, const float* const* factors, int R, float* out, cudaStream_t s,
+                       const int* gate = nullptr, int gate_on = 0);
+fcoo_status run_mttkrp_f64(fcoo_s* f, const float* const* factors, int R, double* out, cudaStream_t s,
+                           const int* gate = nullptr, int gate_on = 0);
 // comm (fcoo_comm.cu)
 fcoo_status comm_allreduce(fcoo_comm_t comm, float* buf, size_t count, cudaStream_t s);
 fcoo_status comm_allreduce_f64(fcoo_comm_t comm, double* buf, size_t count, cudaStream_t s);
