@@ -35,14 +35,15 @@ typedef enum {
   FCOO_ERR_INDEX_RANGE = 4, /* some idx[m][q] >= dims[m] (detected on device) */
   FCOO_ERR_DUPLICATE = 5,   /* two nonzeros share all coordinates (detected on device) */
   FCOO_ERR_EMPTY = 6,       /* nnz == 0 */
-  FCOO_ERR_KEY_BITS = 7,    /* sum_m ceil(log2 dims[m]) > 64: sort key does not fit */
+  FCOO_ERR_KEY_BITS = 7,    /* sum_m ceil(log2 dims[m]) > 128: sort key does not fit (<= 64: u64 keys, else u128) */
   FCOO_ERR_RANK = 8,        /* R outside [1, 256] */
   FCOO_ERR_SHAPE = 9,       /* op/handle mismatch (e.g. fcoo_ttm on an MTTKRP handle) */
   FCOO_ERR_ALIGN = 10,      /* reserved */
   FCOO_ERR_OOM = 11,        /* device allocation failed */
   FCOO_ERR_CUDA = 12,       /* CUDA launch / runtime error */
   FCOO_ERR_NCCL = 13,       /* NCCL error */
-  FCOO_ERR_NOT_FINITE = 14  /* reserved */
+  FCOO_ERR_NOT_FINITE = 14, /* reserved */
+  FCOO_ERR_IO = 15          /* .tns file: cannot open/read/write, or a malformed line */
 } fcoo_status;
 
 /* Operation a handle is built for: Table I.
@@ -228,6 +229,33 @@ typedef struct {
  */
 fcoo_status cp_als(const fcoo_coo* tensor, const fcoo_cp_opts* opts, float* const* factors, float* lambda,
                    double* fit_trace, int* iters_done, const fcoo_allocator* alloc, void* stream);
+
+/*
+ * FROSTT .tns text I/O (host only; no device work).  Table IV's datasets
+ * are distributed as FROSTT text: one nonzero per line, "i_1 ... i_N v", 1-based coordinates,
+ * whitespace-separated; lines whose first non-blank character is '#' and blank lines are
+ * skipped.  Every data line must have the arity of the first (N + 1 fields, 2 <= N <= 8);
+ * coordinates are integers in [1, 2^32 - 1]; v is a decimal float, rounded once to fp32.
+ *
+ * fcoo_tns_read — parse `path` with `nthreads` host threads (0 = all cores) into a
+ *   library-owned host tensor (0-based SoA).  dims_override: host [N] or NULL; NULL gives
+ *   dims[m] = max coordinate of mode m, otherwise every coordinate must be <= dims_override[m].
+ *   Errors: FCOO_ERR_IO (cannot open/read; malformed line: wrong arity, non-numeric, index < 1 or
+ *   > 2^32 - 1 -- fcoo_last_error() names the line), FCOO_ERR_ORDER, FCOO_ERR_EMPTY (no data
+ *   line), FCOO_ERR_INDEX_RANGE (coordinate above dims_override), FCOO_ERR_ARG.
+ * fcoo_tns_info — order, dims (host [8]; the first `order` entries written) and nnz.
+ * fcoo_tns_copy — copy into caller-owned HOST buffers: idx = host array of `order` host
+ *   pointers to nnz uint32 each, val = nnz floats.  File order is kept (not sorted).
+ * fcoo_tns_destroy — free the host tensor (NULL is a no-op).
+ * fcoo_tns_write — write a tensor held in HOST buffers as 1-based FROSTT text, file order =
+ *   row order, values as "%.9g" (exact fp32 round trip).  nnz == 0 writes an empty file.
+ */
+typedef struct fcoo_tns_s* fcoo_tns_t;
+fcoo_status fcoo_tns_read(const char* path, int nthreads, const int64_t* dims_override, fcoo_tns_t* out);
+fcoo_status fcoo_tns_info(fcoo_tns_t t, int* order, int64_t* dims, int64_t* nnz);
+fcoo_status fcoo_tns_copy(fcoo_tns_t t, uint32_t* const* idx, float* val);
+fcoo_status fcoo_tns_destroy(fcoo_tns_t t);
+fcoo_status fcoo_tns_write(const char* path, int order, int64_t nnz, const uint32_t* const* idx, const float* val);
 
 const char* fcoo_status_str(fcoo_status s);
 const char* fcoo_last_error(void);

@@ -69,6 +69,7 @@ const char* fcoo_status_str(fcoo_status s) {
     case FCOO_ERR_CUDA: return "FCOO_ERR_CUDA";
     case FCOO_ERR_NCCL: return "FCOO_ERR_NCCL";
     case FCOO_ERR_NOT_FINITE: return "FCOO_ERR_NOT_FINITE";
+    case FCOO_ERR_IO: return "FCOO_ERR_IO";
   }
   return "FCOO_ERR_UNKNOWN";
 }

@@ -40,18 +40,19 @@ struct IdxPtrs {
 
 // payload: the input ordinal (KEEP_PERM builds) or the value's bits (val_in != nullptr), so the
 // radix sort carries the values along and the flags kernel needs no random gather
+template <class K>
 __global__ void k_pack_keys(IdxPtrs idx, KeyLayout L, int64_t nnz, const float* __restrict__ val_in,
-                            uint64_t* __restrict__ keys, uint32_t* __restrict__ ord, uint32_t* __restrict__ err) {
+                            K* __restrict__ keys, uint32_t* __restrict__ ord, uint32_t* __restrict__ err) {
   int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nnz) return;
-  uint64_t key = 0;
+  K key = 0;
   bool bad = false;
 #pragma unroll
   for (int a = 0; a < kMaxOrder; ++a) {
     if (a < L.order) {
       uint32_t c = idx.p[a][q];
       bad |= (L.dims[a] != 0u && c >= L.dims[a]);
-      key |= ((uint64_t)c & L.mask[a]) << L.shift[a];
+      key |= (K)((uint64_t)c & L.mask[a]) << L.shift[a];
     }
   }
   if (bad) atomicOr(err, ERRF_INDEX_RANGE);
@@ -59,12 +60,14 @@ __global__ void k_pack_keys(IdxPtrs idx, KeyLayout L, int64_t nnz, const float* 
   ord[q] = val_in ? __float_as_uint(val_in[q]) : (uint32_t)q;
 }
 
-__device__ __forceinline__ uint64_t index_part(uint64_t key, int prod_bits) {
-  return prod_bits >= 64 ? 0ull : (key >> prod_bits);
+template <class K>
+__device__ __forceinline__ K index_part(K key, int prod_bits) {
+  return prod_bits >= (int)(8 * sizeof(K)) ? (K)0 : (key >> prod_bits);
 }
 
 // One thread per (padded) position p; nnz_pad is a multiple of 32 so warps are whole words.
-__global__ void k_flags(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ ord,
+template <class K>
+__global__ void k_flags(const K* __restrict__ keys, const uint32_t* __restrict__ ord,
                         const float* __restrict__ val_in, KeyLayout L, int n_prod, int64_t nnz, int64_t nnz_pad,
                         uint32_t* __restrict__ pidx, float* __restrict__ val, uint32_t* __restrict__ bf,
                         uint32_t* __restrict__ wcount, uint32_t* __restrict__ perm, uint32_t* __restrict__ err) {
@@ -73,11 +76,11 @@ __global__ void k_flags(const uint64_t* __restrict__ keys, const uint32_t* __res
   bool live = p < nnz;
   bool head = false;
   if (live) {
-    uint64_t key = keys[p];
+    K key = keys[p];
     if (p == 0) {
       head = true;
     } else {
-      uint64_t prev = keys[p - 1];
+      K prev = keys[p - 1];
       head = index_part(key, L.prod_bits) != index_part(prev, L.prod_bits);
       if (key == prev) atomicOr(err, ERRF_DUPLICATE);
     }
@@ -119,7 +122,8 @@ __global__ void k_tiles(const uint32_t* __restrict__ bf, const uint32_t* __restr
   if ((threadIdx.x & 31) == 0 && (t >> 5) <= (ntiles - 1) >> 5) sf[t >> 5] = word;
 }
 
-__global__ void k_seg_coord(const uint64_t* __restrict__ keys, const uint32_t* __restrict__ bf,
+template <class K>
+__global__ void k_seg_coord(const K* __restrict__ keys, const uint32_t* __restrict__ bf,
                             const uint32_t* __restrict__ wbase, KeyLayout L, int64_t nnz,
                             uint32_t* __restrict__ seg_coord) {
   int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -128,7 +132,7 @@ __global__ void k_seg_coord(const uint64_t* __restrict__ keys, const uint32_t* _
   int b = (int)(p & 31);
   if (!((word >> b) & 1u)) return;
   uint32_t s = wbase[p >> 5] + __popc(word & ((1u << b) - 1u));
-  uint64_t key = keys[p];
+  K key = keys[p];
   for (int a = 0; a < L.n_idx; ++a) seg_coord[(int64_t)s * L.n_idx + a] = (uint32_t)((key >> L.shift[a]) & L.mask[a]);
 }
 
@@ -199,6 +203,89 @@ fcoo_status plan_modes(fcoo_s* f, int order, const int64_t* dims, int op, int mo
   return FCOO_OK;
 }
 
+// Key packing, radix sort, flags, tiles, the one host sync and seg_coord, for sort keys of type K
+// (uint64_t up to 64 key bits; unsigned __int128 up to 128, e.g. nell1 = 69 bits, Table IV).
+// Returns a status; the caller frees the handle on failure.  Scratch is freed stream-ordered.
+template <class K>
+fcoo_status sort_and_flag(fcoo_s* f, const fcoo_coo* coo, const KeyLayout& L, const IdxPtrs& ip, int total,
+                          unsigned flags, cudaStream_t s) {
+  const int64_t nnz = f->nnz, nnz_pad = f->nnz_pad, nwords = nnz_pad / 32, ntiles = f->ntiles;
+  const int64_t T = f->T;
+  Buf keys0(&f->alloc, sizeof(K) * nnz, s), keys1(&f->alloc, sizeof(K) * nnz, s);
+  Buf ord0(&f->alloc, sizeof(uint32_t) * nnz, s), ord1(&f->alloc, sizeof(uint32_t) * nnz, s);
+  Buf wcount(&f->alloc, sizeof(uint32_t) * (nwords + 1), s), wbase(&f->alloc, sizeof(uint32_t) * (nwords + 1), s);
+  Buf errb(&f->alloc, sizeof(uint32_t) * 2, s);
+  if (!keys0.ok() || !keys1.ok() || !ord0.ok() || !ord1.ok() || !wcount.ok() || !wbase.ok() || !errb.ok())
+    return fail(FCOO_ERR_OOM, "build scratch allocation failed");
+  cudaError_t ce;
+  if ((ce = cudaMemsetAsync(errb.p, 0, sizeof(uint32_t) * 2, s)) != cudaSuccess ||
+      (ce = cudaMemsetAsync(wcount.p, 0, sizeof(uint32_t) * (nwords + 1), s)) != cudaSuccess)
+    return fail(FCOO_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
+
+  const int TB = 256;
+  const bool keep_perm = (flags & FCOO_BUILD_KEEP_PERM) != 0;
+  k_pack_keys<<<(unsigned)((nnz + TB - 1) / TB), TB, 0, s>>>(ip, L, nnz, keep_perm ? nullptr : coo->val,
+                                                             keys0.as<K>(), ord0.as<uint32_t>(),
+                                                             errb.as<uint32_t>());
+  count_launch();
+  if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_pack_keys: %s", cudaGetErrorString(ce));
+
+  cub::DoubleBuffer<K> dk(keys0.as<K>(), keys1.as<K>());
+  cub::DoubleBuffer<uint32_t> dv(ord0.as<uint32_t>(), ord1.as<uint32_t>());
+  int end_bit = total > 0 ? total : 1;
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, (int64_t)nnz, 0, end_bit, s);
+  {
+    Buf cubtmp(&f->alloc, tmp_bytes, s);
+    if (!cubtmp.ok()) return fail(FCOO_ERR_OOM, "radix sort scratch");
+    if ((ce = cub::DeviceRadixSort::SortPairs(cubtmp.p, tmp_bytes, dk, dv, (int64_t)nnz, 0, end_bit, s)) != cudaSuccess)
+      return fail(FCOO_ERR_CUDA, "radix sort: %s", cudaGetErrorString(ce));
+    count_launch(2 + (end_bit + 7) / 8);
+  }
+  const K* keys = dk.Current();
+  const uint32_t* ord = dv.Current();
+
+  k_flags<<<(unsigned)((nnz_pad + TB - 1) / TB), TB, 0, s>>>(keys, ord, coo->val, L, f->n_prod, nnz, nnz_pad, f->pidx,
+                                                            f->val, f->bf, wcount.as<uint32_t>(), f->perm,
+                                                            errb.as<uint32_t>());
+  count_launch();
+  if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_flags: %s", cudaGetErrorString(ce));
+
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, wcount.as<uint32_t>(), wbase.as<uint32_t>(), (int64_t)(nwords + 1), s);
+  {
+    Buf scantmp(&f->alloc, scan_bytes, s);
+    if (!scantmp.ok()) return fail(FCOO_ERR_OOM, "scan scratch");
+    if ((ce = cub::DeviceScan::ExclusiveSum(scantmp.p, scan_bytes, wcount.as<uint32_t>(), wbase.as<uint32_t>(),
+                                            (int64_t)(nwords + 1), s)) != cudaSuccess)
+      return fail(FCOO_ERR_CUDA, "scan: %s", cudaGetErrorString(ce));
+    count_launch(2);
+  }
+  int64_t tthreads = ((ntiles + 1 + 31) / 32) * 32;
+  k_tiles<<<(unsigned)((tthreads + TB - 1) / TB), TB, 0, s>>>(f->bf, wbase.as<uint32_t>(), ntiles, T / 32, nwords,
+                                                             f->sf, f->seg_base);
+  count_launch();
+  if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_tiles: %s", cudaGetErrorString(ce));
+
+  uint32_t host[2] = {0, 0};
+  if ((ce = cudaMemcpyAsync(&host[0], errb.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+      (ce = cudaMemcpyAsync(&host[1], wbase.as<uint32_t>() + nwords, sizeof(uint32_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+      (ce = cudaStreamSynchronize(s)) != cudaSuccess)
+    return fail(FCOO_ERR_CUDA, "build sync: %s", cudaGetErrorString(ce));
+  if (host[0] & ERRF_INDEX_RANGE) return fail(FCOO_ERR_INDEX_RANGE, "a coordinate is >= its mode extent");
+  if (host[0] & ERRF_DUPLICATE) return fail(FCOO_ERR_DUPLICATE, "duplicate coordinates");
+  f->nsegs = host[1];
+  f->dense_rows = (f->op == FCOO_OP_MTTKRP && f->nsegs == f->dims[f->mode]) ? 1 : 0;
+
+  f->seg_coord = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)std::max<int64_t>(1, f->nsegs * f->n_idx), s,
+                                &f->bytes_seg_coord);
+  if (!f->seg_coord) return fail(FCOO_ERR_OOM, "seg_coord allocation");
+  k_seg_coord<<<(unsigned)((nnz + TB - 1) / TB), TB, 0, s>>>(keys, f->bf, wbase.as<uint32_t>(), L, nnz, f->seg_coord);
+  count_launch();
+  if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_seg_coord: %s", cudaGetErrorString(ce));
+  return FCOO_OK;
+}
+
 fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opts, const fcoo_allocator* alloc,
                        cudaStream_t s, fcoo_t* out) {
   if (!coo || !out) return fail(FCOO_ERR_ARG, "NULL coo/out");
@@ -224,7 +311,7 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
   for (int a = 0; a < tmp.n_prod; ++a) L.key_modes[tmp.n_idx + a] = tmp.prod_modes[a];
   int total = 0, bits[kMaxOrder];
   for (int a = 0; a < L.order; ++a) { bits[a] = bits_for(coo->dims[L.key_modes[a]]); total += bits[a]; }
-  if (total > 64) return fail(FCOO_ERR_KEY_BITS, "sort key needs %d bits > 64", total);
+  if (total > 128) return fail(FCOO_ERR_KEY_BITS, "sort key needs %d bits > 128", total);
   int sh = 0;
   for (int a = L.order - 1; a >= 0; --a) {
     L.shift[a] = sh;
@@ -260,80 +347,9 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
   if (!f->pidx || !f->val || !f->bf || !f->sf || !f->seg_base || ((flags & FCOO_BUILD_KEEP_PERM) && !f->perm))
     return bail(fail(FCOO_ERR_OOM, "handle allocation failed"));
 
-  {
-    Buf keys0(&f->alloc, sizeof(uint64_t) * nnz, s), keys1(&f->alloc, sizeof(uint64_t) * nnz, s);
-    Buf ord0(&f->alloc, sizeof(uint32_t) * nnz, s), ord1(&f->alloc, sizeof(uint32_t) * nnz, s);
-    Buf wcount(&f->alloc, sizeof(uint32_t) * (nwords + 1), s), wbase(&f->alloc, sizeof(uint32_t) * (nwords + 1), s);
-    Buf errb(&f->alloc, sizeof(uint32_t) * 2, s);
-    if (!keys0.ok() || !keys1.ok() || !ord0.ok() || !ord1.ok() || !wcount.ok() || !wbase.ok() || !errb.ok())
-      return bail(fail(FCOO_ERR_OOM, "build scratch allocation failed"));
-    cudaError_t ce;
-    if ((ce = cudaMemsetAsync(errb.p, 0, sizeof(uint32_t) * 2, s)) != cudaSuccess ||
-        (ce = cudaMemsetAsync(wcount.p, 0, sizeof(uint32_t) * (nwords + 1), s)) != cudaSuccess)
-      return bail(fail(FCOO_ERR_CUDA, "memset: %s", cudaGetErrorString(ce)));
-
-    const int TB = 256;
-    const bool keep_perm = (flags & FCOO_BUILD_KEEP_PERM) != 0;
-    k_pack_keys<<<(unsigned)((nnz + TB - 1) / TB), TB, 0, s>>>(ip, L, nnz, keep_perm ? nullptr : coo->val,
-                                                               keys0.as<uint64_t>(), ord0.as<uint32_t>(),
-                                                               errb.as<uint32_t>());
-    count_launch();
-    if ((ce = cudaGetLastError()) != cudaSuccess) return bail(fail(FCOO_ERR_CUDA, "k_pack_keys: %s", cudaGetErrorString(ce)));
-
-    cub::DoubleBuffer<uint64_t> dk(keys0.as<uint64_t>(), keys1.as<uint64_t>());
-    cub::DoubleBuffer<uint32_t> dv(ord0.as<uint32_t>(), ord1.as<uint32_t>());
-    int end_bit = total > 0 ? total : 1;
-    size_t tmp_bytes = 0;
-    cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, (int64_t)nnz, 0, end_bit, s);
-    {
-      Buf cubtmp(&f->alloc, tmp_bytes, s);
-      if (!cubtmp.ok()) return bail(fail(FCOO_ERR_OOM, "radix sort scratch"));
-      if ((ce = cub::DeviceRadixSort::SortPairs(cubtmp.p, tmp_bytes, dk, dv, (int64_t)nnz, 0, end_bit, s)) != cudaSuccess)
-        return bail(fail(FCOO_ERR_CUDA, "radix sort: %s", cudaGetErrorString(ce)));
-      count_launch(2 + (end_bit + 7) / 8);
-    }
-    const uint64_t* keys = dk.Current();
-    const uint32_t* ord = dv.Current();
-
-    k_flags<<<(unsigned)((nnz_pad + TB - 1) / TB), TB, 0, s>>>(keys, ord, coo->val, L, f->n_prod, nnz, nnz_pad, f->pidx,
-                                                              f->val, f->bf, wcount.as<uint32_t>(), f->perm,
-                                                              errb.as<uint32_t>());
-    count_launch();
-    if ((ce = cudaGetLastError()) != cudaSuccess) return bail(fail(FCOO_ERR_CUDA, "k_flags: %s", cudaGetErrorString(ce)));
-
-    size_t scan_bytes = 0;
-    cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, wcount.as<uint32_t>(), wbase.as<uint32_t>(), (int64_t)(nwords + 1), s);
-    {
-      Buf scantmp(&f->alloc, scan_bytes, s);
-      if (!scantmp.ok()) return bail(fail(FCOO_ERR_OOM, "scan scratch"));
-      if ((ce = cub::DeviceScan::ExclusiveSum(scantmp.p, scan_bytes, wcount.as<uint32_t>(), wbase.as<uint32_t>(),
-                                              (int64_t)(nwords + 1), s)) != cudaSuccess)
-        return bail(fail(FCOO_ERR_CUDA, "scan: %s", cudaGetErrorString(ce)));
-      count_launch(2);
-    }
-    int64_t tthreads = ((ntiles + 1 + 31) / 32) * 32;
-    k_tiles<<<(unsigned)((tthreads + TB - 1) / TB), TB, 0, s>>>(f->bf, wbase.as<uint32_t>(), ntiles, T / 32, nwords,
-                                                               f->sf, f->seg_base);
-    count_launch();
-    if ((ce = cudaGetLastError()) != cudaSuccess) return bail(fail(FCOO_ERR_CUDA, "k_tiles: %s", cudaGetErrorString(ce)));
-
-    uint32_t host[2] = {0, 0};
-    if ((ce = cudaMemcpyAsync(&host[0], errb.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
-        (ce = cudaMemcpyAsync(&host[1], wbase.as<uint32_t>() + nwords, sizeof(uint32_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
-        (ce = cudaStreamSynchronize(s)) != cudaSuccess)
-      return bail(fail(FCOO_ERR_CUDA, "build sync: %s", cudaGetErrorString(ce)));
-    if (host[0] & ERRF_INDEX_RANGE) return bail(fail(FCOO_ERR_INDEX_RANGE, "a coordinate is >= its mode extent"));
-    if (host[0] & ERRF_DUPLICATE) return bail(fail(FCOO_ERR_DUPLICATE, "duplicate coordinates"));
-    f->nsegs = host[1];
-    f->dense_rows = (f->op == FCOO_OP_MTTKRP && f->nsegs == f->dims[f->mode]) ? 1 : 0;
-
-    f->seg_coord = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)std::max<int64_t>(1, f->nsegs * f->n_idx), s,
-                                  &f->bytes_seg_coord);
-    if (!f->seg_coord) return bail(fail(FCOO_ERR_OOM, "seg_coord allocation"));
-    k_seg_coord<<<(unsigned)((nnz + TB - 1) / TB), TB, 0, s>>>(keys, f->bf, wbase.as<uint32_t>(), L, nnz, f->seg_coord);
-    count_launch();
-    if ((ce = cudaGetLastError()) != cudaSuccess) return bail(fail(FCOO_ERR_CUDA, "k_seg_coord: %s", cudaGetErrorString(ce)));
-  }  // scratch freed (stream-ordered)
+  if (total <= 64) st = sort_and_flag<uint64_t>(f, coo, L, ip, total, flags, s);
+  else st = sort_and_flag<unsigned __int128>(f, coo, L, ip, total, flags, s);
+  if (st) return bail(st);
   *out = f;
   return FCOO_OK;
 }

@@ -18,7 +18,7 @@ LIB_PATH = os.environ.get("FCOO_LIB") or os.path.join(_PKG, "libfcoo.so")  # FCO
 
 OK = 0
 ERR_ARG, ERR_ORDER, ERR_MODE, ERR_INDEX_RANGE, ERR_DUPLICATE, ERR_EMPTY, ERR_KEY_BITS, ERR_RANK, ERR_SHAPE, \
-    ERR_ALIGN, ERR_OOM, ERR_CUDA, ERR_NCCL, ERR_NOT_FINITE = range(1, 15)
+    ERR_ALIGN, ERR_OOM, ERR_CUDA, ERR_NCCL, ERR_NOT_FINITE, ERR_IO = range(1, 16)
 OP_MTTKRP, OP_TTM = 0, 1
 BUILD_KEEP_PERM = 1
 BUILD_PRODUCT_DESC = 2
@@ -71,7 +71,8 @@ class _CpOpts(ctypes.Structure):
 # The exported symbols (every one declared in include/fcoo.h).
 SYMBOLS = ["fcoo_build", "fcoo_mttkrp", "fcoo_ttm", "fcoo_ttmc", "fcoo_info", "fcoo_export", "fcoo_destroy",
            "fcoo_comm_unique_id", "fcoo_comm_init", "fcoo_comm_destroy", "fcoo_allreduce_sum", "fcoo_set_shard",
-           "fcoo_shard_range", "cp_als", "fcoo_status_str", "fcoo_last_error", "fcoo_launch_count"]
+           "fcoo_shard_range", "cp_als", "fcoo_tns_read", "fcoo_tns_info", "fcoo_tns_copy", "fcoo_tns_destroy",
+           "fcoo_tns_write", "fcoo_status_str", "fcoo_last_error", "fcoo_launch_count"]
 
 _lib = None
 
@@ -101,6 +102,11 @@ def load_library():
     L.fcoo_shard_range.argtypes = [i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.cp_als.argtypes = [ctypes.POINTER(_Coo), ctypes.POINTER(_CpOpts), ctypes.POINTER(vp), vp,
                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ci), ctypes.POINTER(_Allocator), vp]
+    L.fcoo_tns_read.argtypes = [ctypes.c_char_p, ci, ctypes.POINTER(i64), ctypes.POINTER(vp)]
+    L.fcoo_tns_info.argtypes = [vp, ctypes.POINTER(ci), ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.fcoo_tns_copy.argtypes = [vp, ctypes.POINTER(vp), vp]
+    L.fcoo_tns_destroy.argtypes = [vp]
+    L.fcoo_tns_write.argtypes = [ctypes.c_char_p, ci, i64, ctypes.POINTER(vp), vp]
     L.fcoo_status_str.restype = ctypes.c_char_p
     L.fcoo_status_str.argtypes = [ci]
     L.fcoo_last_error.restype = ctypes.c_char_p
@@ -158,6 +164,38 @@ def _require_cuda(t: torch.Tensor, dtype, name: str):
         raise ValueError(f"{name} must be {dtype}")
     if not t.is_contiguous():
         raise ValueError(f"{name} must be contiguous")
+
+
+def read_tns(path: str, nthreads: int = 0, dims=None):
+    """FROSTT .tns text -> (dims, idx (order, nnz) uint32 0-based, val (nnz,) float32) host arrays,
+    parsed by the library's native reader (fcoo_tns_read).  Coo.from_numpy uploads them."""
+    import numpy as np
+    L = load_library()
+    t = ctypes.c_void_p()
+    ov = None if dims is None else (ctypes.c_int64 * len(dims))(*[int(d) for d in dims])
+    _check(L.fcoo_tns_read(os.fsencode(path), int(nthreads), ov, ctypes.byref(t)), "fcoo_tns_read")
+    try:
+        order, nnz = ctypes.c_int(), ctypes.c_int64()
+        d = (ctypes.c_int64 * 8)()
+        _check(L.fcoo_tns_info(t, ctypes.byref(order), d, ctypes.byref(nnz)), "fcoo_tns_info")
+        idx = np.empty((order.value, nnz.value), np.uint32)
+        val = np.empty(nnz.value, np.float32)
+        ptrs = (ctypes.c_void_p * order.value)(*[idx[m].ctypes.data for m in range(order.value)])
+        _check(L.fcoo_tns_copy(t, ptrs, val.ctypes.data), "fcoo_tns_copy")
+        return tuple(int(d[m]) for m in range(order.value)), idx, val
+    finally:
+        L.fcoo_tns_destroy(t)
+
+
+def write_tns(path: str, idx, val):
+    """Write host arrays (idx (order, nnz) 0-based, val (nnz,)) as 1-based FROSTT text (fcoo_tns_write)."""
+    import numpy as np
+    L = load_library()
+    idx = np.ascontiguousarray(idx, dtype=np.uint32)
+    val = np.ascontiguousarray(val, dtype=np.float32)
+    order, nnz = idx.shape
+    ptrs = (ctypes.c_void_p * order)(*[idx[m].ctypes.data for m in range(order)])
+    _check(L.fcoo_tns_write(os.fsencode(path), order, nnz, ptrs, val.ctypes.data), "fcoo_tns_write")
 
 
 class Coo:

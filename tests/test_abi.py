@@ -50,8 +50,9 @@ def test_host_checked_errors_without_gpu():
     assert L.fcoo_build(ctypes.byref(coo1), 0, ctypes.byref(opts), None, None, ctypes.byref(out)) == fcoo.ERR_ORDER
     coo0 = fcoo._Coo(3, dims3, 0, ptrs3, 8)
     assert L.fcoo_build(ctypes.byref(coo0), 0, ctypes.byref(opts), None, None, ctypes.byref(out)) == fcoo.ERR_EMPTY
-    big = (ctypes.c_int64 * 3)(1 << 30, 1 << 30, 1 << 30)
-    cooK = fcoo._Coo(3, big, 10, ptrs3, 8)
+    big = (ctypes.c_int64 * 5)(*([1 << 30] * 5))  # 150 key bits > 128
+    ptrs5 = (ctypes.c_void_p * 5)(8, 8, 8, 8, 8)
+    cooK = fcoo._Coo(5, big, 10, ptrs5, 8)
     assert L.fcoo_build(ctypes.byref(cooK), 0, ctypes.byref(opts), None, None, ctypes.byref(out)) == fcoo.ERR_KEY_BITS
     assert L.fcoo_mttkrp(None, None, 8, None, None) == fcoo.ERR_ARG
     assert L.fcoo_ttm(None, None, 8, None, None) == fcoo.ERR_ARG

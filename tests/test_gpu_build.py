@@ -81,6 +81,32 @@ def test_build_edge_cases(F):
     _compare(F, (n, 13, 1), single, v, F.OP_TTM, 2, 32)
 
 
+# FROSTT nell-1 extents (Table IV P:L414 "2.9M x 2.1M x 25.5M"): 22 + 22 + 25 = 69 key bits, so the
+# build takes the 128-bit key path
+NELL1_DIMS = (2902330, 2143368, 25495389)
+
+
+def test_build_wide_keys_nell1_shape(F):
+    idx, val = gen.coo(NELL1_DIMS, 300_000, (0.5, 0.5, 0.5), 23)
+    for mode in range(3):
+        for op in (F.OP_MTTKRP, F.OP_TTM):
+            _compare(F, NELL1_DIMS, idx, val, op, mode, 256)
+
+
+def test_build_wide_keys_boundaries(F):
+    # 64 bits exactly (last 64-bit case), 65 bits (first 128-bit case), 128 bits exactly
+    for dims in (((1 << 32) - 1, (1 << 32) - 1), ((1 << 32) - 1, (1 << 32) - 1, 2),
+                 ((1 << 32) - 1,) * 4):
+        n = 3000
+        # row 0 is q * prime mod (2^32 - 1): distinct, so no duplicate coordinates
+        idx = np.stack([(np.arange(n, dtype=np.uint64) * np.uint64(2654435761 + 2 * m) % np.uint64(dims[m]))
+                        .astype(np.uint32) for m in range(len(dims))])
+        val = (gen.uniform((n,), 41, 0) + 0.5).astype(np.float32)
+        for mode in range(len(dims)):
+            _compare(F, dims, idx, val, F.OP_MTTKRP, mode, 64)
+            _compare(F, dims, idx, val, F.OP_TTM, mode, 32)
+
+
 def test_build_errors(F):
     dims = (10, 10, 10)
     idx = np.array([[1, 2, 1], [1, 2, 1], [1, 2, 1]], np.uint32)  # duplicate (1,1,1)
@@ -92,7 +118,20 @@ def test_build_errors(F):
     with pytest.raises(F.FcooError) as e:
         F.fcoo_build(F.Coo.from_numpy(dims, bad, val[:2]), 0)
     assert e.value.code == 4  # FCOO_ERR_INDEX_RANGE
-    big = (1 << 30, 1 << 30, 1 << 30)
+    big = (1 << 30,) * 5  # 150 key bits > 128
+    idx5 = np.array([[1, 2]] * 5, np.uint32)
     with pytest.raises(F.FcooError) as e:
-        F.fcoo_build(F.Coo.from_numpy(big, idx[:, :2].copy(), val[:2]), 0)
+        F.fcoo_build(F.Coo.from_numpy(big, idx5, val[:2]), 0)
     assert e.value.code == 7  # FCOO_ERR_KEY_BITS
+
+
+def test_tns_file_to_device_build(F, tmp_path):
+    """Real-dataset path: FROSTT text -> native reader -> device build, with
+    nell-1 extents given as the dims override (69-bit keys)."""
+    idx, val = gen.coo(NELL1_DIMS, 50_000, (0.5, 0.5, 0.5), 29)
+    path = str(tmp_path / "nell1_sample.tns")
+    F.write_tns(path, idx, val)
+    dims, idx2, val2 = F.read_tns(path, dims=NELL1_DIMS)
+    assert dims == NELL1_DIMS and np.array_equal(idx2, idx) and np.array_equal(val2, val)
+    for mode in range(3):
+        _compare(F, dims, idx2, val2, F.OP_MTTKRP, mode, 128)

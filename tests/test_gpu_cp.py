@@ -51,6 +51,22 @@ def test_recovery_matches_oracle(F, dims, R):
     assert tr_g[-1] >= 0.999
 
 
+def test_fit_precision_switch_long_segments(F):
+    """Dense 120x100x80 rank-6 tensor: last-mode slices of 12000 nonzeros, so an fp32 <X,Xhat> near
+    fit 1 would be off by >1e-4.  The trace crosses the 0.9 switch (fp32 -> exact fp64 recompute of
+    the last mode) and must match the oracle at every iteration."""
+    dims, R = (120, 100, 80), 6
+    A = [gen.uniform((d, R), 310 + m, 1, signed=True) for m, d in enumerate(dims)]
+    cells = np.array(list(np.ndindex(*dims)), np.uint32).T.copy()
+    val = gen.kruskal_coo(A, np.linspace(1.0, 2.0, R), cells)
+    # truth + heavy perturbation: fit 0.53 -> 0.79 -> 0.96 -> ... -> 0.9999995
+    init = [(a + 3.0 * gen.uniform(a.shape, 330 + m, 1, signed=True)).astype(np.float32) for m, a in enumerate(A)]
+    _, _, tr_o = oracle.cp_als(dims, cells, val, R, 20, init)
+    _, _, tr_g = _cp(F, dims, cells, val, R, 20, init, T=256)
+    assert tr_o[0] < 0.9 and tr_o[-1] > 0.99999
+    assert np.max(np.abs(tr_g - tr_o)) <= 1e-4, (tr_g, tr_o)
+
+
 def test_rank_deficient_fallback(F):
     """R above a mode extent: V is singular, the Jacobi pinv fallback must match the oracle."""
     dims = (10, 9, 3)
