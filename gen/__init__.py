@@ -21,8 +21,10 @@ _lib = None
 
 
 def build(force: bool = False) -> str:
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
-        subprocess.check_call(["gcc", "-O2", "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
+    deps = [_SRC, os.path.join(os.path.dirname(_SRC), "tensorgen_dedup.h")]
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(os.path.getmtime(d) for d in deps):
+        # -mcx16: lock-free 16-byte compare-and-swap for the 128-bit tuple table
+        subprocess.check_call(["gcc", "-O2", "-mcx16", "-fopenmp", "-fPIC", "-shared", "-o", _LIB, _SRC, "-lm"])
     return _LIB
 
 

@@ -113,11 +113,43 @@ static int bits_for(int64_t n) {
   return b;
 }
 
+/* the dedup loop, for 64-bit and 128-bit packed tuples (tensorgen_dedup.h) */
+#define TG_KEY uint64_t
+#define TG_FN tg_dedup64
+#define TG_HASH(k) splitmix64(k)
+#define TG_LOAD(p) __atomic_load_n((p), __ATOMIC_RELAXED)
+#define TG_CAS(p, e, d) __atomic_compare_exchange_n((p), (e), (d), 0, __ATOMIC_RELAXED, __ATOMIC_RELAXED)
+#include "tensorgen_dedup.h"
+#undef TG_KEY
+#undef TG_FN
+#undef TG_HASH
+#undef TG_LOAD
+#undef TG_CAS
+typedef unsigned __int128 tg_u128;
+static inline tg_u128 tg_load128(tg_u128* p) { return __sync_val_compare_and_swap(p, (tg_u128)0, (tg_u128)0); }
+static inline int tg_cas128(tg_u128* p, tg_u128* expect, tg_u128 desired) {
+  tg_u128 old = __sync_val_compare_and_swap(p, *expect, desired);
+  if (old == *expect) return 1;
+  *expect = old;
+  return 0;
+}
+#define TG_KEY tg_u128
+#define TG_FN tg_dedup128
+#define TG_HASH(k) splitmix64((uint64_t)(k) ^ splitmix64((uint64_t)((k) >> 64)))
+#define TG_LOAD(p) tg_load128(p)
+#define TG_CAS(p, e, d) tg_cas128((p), (e), (d))
+#include "tensorgen_dedup.h"
+#undef TG_KEY
+#undef TG_FN
+#undef TG_HASH
+#undef TG_LOAD
+#undef TG_CAS
+
 /*
  * Generate a duplicate-free COO tensor.
  *   idx: order*nnz uint32, SoA (idx[m*nnz + p]); val: nnz float.
  *   draws_out (may be NULL): number of draws consumed.
- * Returns 0, or -1 (alloc), -2 (bad args / nnz > prod dims), -3 (tuple > 63 bits),
+ * Returns 0, or -1 (alloc), -2 (bad args / nnz > prod dims), -3 (tuple > 127 bits),
  * -4 (too many duplicate draws).
  */
 int tg_coo(int order, const int64_t* dims, int64_t nnz, const double* alpha, uint64_t seed,
@@ -132,7 +164,7 @@ int tg_coo(int order, const int64_t* dims, int64_t nnz, const double* alpha, uin
     tot += bits_for(dims[m]);
     cells *= (double)dims[m];
   }
-  if (tot > 63) return -3; /* key+1 and the ~0 drop marker must stay free */
+  if (tot > 127) return -3; /* key+1 and the ~0 drop marker must stay free */
   if ((double)nnz > cells) return -2;
   if (nnz == 0) { if (draws_out) *draws_out = 0; return 0; }
 
@@ -140,123 +172,9 @@ int tg_coo(int order, const int64_t* dims, int64_t nnz, const double* alpha, uin
   for (int m = 0; m < order; ++m)
     if (tg_mode_init(&md[m], dims[m], alpha ? alpha[m] : 0.0, seed, m)) return -1;
 
-  uint64_t cap = 1024;
-  while (cap < (uint64_t)nnz * 2) cap <<= 1;
-  uint64_t* tkey = (uint64_t*)malloc(sizeof(uint64_t) * cap);   /* key+1, 0 = empty */
-  uint32_t* tmin = (uint32_t*)malloc(sizeof(uint32_t) * cap);   /* min draw index */
-  int64_t kcap = nnz + nnz / 4 + 1024;
-  uint64_t* keys = (uint64_t*)malloc(sizeof(uint64_t) * (size_t)kcap);
-  int rc = 0;
-  if (!tkey || !tmin || !keys) { rc = -1; goto done; }
-  memset(tkey, 0, sizeof(uint64_t) * cap);
-  memset(tmin, 0xff, sizeof(uint32_t) * cap);
-
-  int64_t q_lo = 0, q_hi = nnz, distinct = 0;
-  for (;;) {
-    if (q_hi > kcap) {
-      int64_t nk = q_hi + q_hi / 4;
-      uint64_t* k2 = (uint64_t*)realloc(keys, sizeof(uint64_t) * (size_t)nk);
-      if (!k2) { rc = -1; goto done; }
-      keys = k2; kcap = nk;
-    }
-    if (q_hi > 4294967294LL || (double)q_hi > 64.0 * (double)nnz + 1e6) { rc = -4; goto done; }
-    int rehash = 0;
-    while ((uint64_t)q_hi > (cap / 10) * 7) { cap <<= 1; rehash = 1; }
-    if (rehash) { /* grow the table and re-insert the draws so far (same min-q result) */
-      free(tkey); free(tmin);
-      tkey = (uint64_t*)malloc(sizeof(uint64_t) * cap);
-      tmin = (uint32_t*)malloc(sizeof(uint32_t) * cap);
-      if (!tkey || !tmin) { rc = -1; goto done; }
-      memset(tkey, 0, sizeof(uint64_t) * cap);
-      memset(tmin, 0xff, sizeof(uint32_t) * cap);
-    }
-    int64_t added = 0;
-    int64_t q_from = rehash ? 0 : q_lo;
-#pragma omp parallel for schedule(static) reduction(+ : added)
-    for (int64_t q = q_from; q < q_hi; ++q) {
-      uint64_t key = 0;
-      if (q >= q_lo) {
-        for (int m = 0; m < order; ++m) {
-          uint32_t c = tg_mode_draw(&md[m], tg_h(seed, (uint64_t)m, (uint64_t)q));
-          key |= (uint64_t)c << shift[m];
-        }
-        keys[q] = key;
-      } else {
-        key = keys[q];
-      }
-      uint64_t slot = splitmix64(key) & (cap - 1);
-      for (;;) {
-        uint64_t cur = __atomic_load_n(&tkey[slot], __ATOMIC_RELAXED);
-        if (cur == 0) {
-          uint64_t expect = 0;
-          if (__atomic_compare_exchange_n(&tkey[slot], &expect, key + 1, 0, __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
-            added++;
-            break;
-          }
-          cur = expect;
-        }
-        if (cur == key + 1) break;
-        slot = (slot + 1) & (cap - 1);
-      }
-      uint32_t qq = (uint32_t)q, old = __atomic_load_n(&tmin[slot], __ATOMIC_RELAXED);
-      while (qq < old && !__atomic_compare_exchange_n(&tmin[slot], &old, qq, 1, __ATOMIC_RELAXED, __ATOMIC_RELAXED)) {
-      }
-    }
-    distinct = rehash ? added : distinct + added;
-    if (distinct >= nnz) break;
-    q_lo = q_hi;
-    q_hi += (nnz - distinct) + (nnz - distinct) / 4 + 16;
-  }
-
-  {
-    /* survivors in draw order: draw q survives iff it is the first draw of its tuple */
-    int nth = 1;
-#ifdef _OPENMP
-    nth = omp_get_max_threads();
-#endif
-    int64_t* cnt = (int64_t*)calloc((size_t)nth + 1, sizeof(int64_t));
-    if (!cnt) { rc = -1; goto done; }
-    int64_t total = q_hi;
-#pragma omp parallel num_threads(nth)
-    {
-      int t = 0;
-#ifdef _OPENMP
-      t = omp_get_thread_num();
-#endif
-      int64_t lo = total * t / nth, hi = total * (t + 1) / nth, c = 0;
-      for (int64_t q = lo; q < hi; ++q) {
-        uint64_t key = keys[q], slot = splitmix64(key) & (cap - 1);
-        while (tkey[slot] != key + 1) slot = (slot + 1) & (cap - 1);
-        if (tmin[slot] == (uint32_t)q) c++; else keys[q] = ~0ULL; /* mark dropped */
-      }
-      cnt[t + 1] = c;
-#pragma omp barrier
-#pragma omp single
-      for (int i = 1; i <= nth; ++i) cnt[i] += cnt[i - 1];
-      int64_t pos = cnt[t];
-      for (int64_t q = lo; q < hi && pos < nnz; ++q) {
-        if (keys[q] == ~0ULL) continue; /* dropped duplicate */
-        uint64_t key = keys[q];
-        for (int m = 0; m < order; ++m) {
-          int b = (m + 1 < order ? shift[m + 1] : tot) - shift[m];
-          uint64_t mask = b >= 64 ? ~0ULL : (((uint64_t)1 << b) - 1);
-          idx[(int64_t)m * nnz + pos] = (uint32_t)((key >> shift[m]) & mask);
-        }
-        val[pos] = (float)((double)(1 + (tg_h(seed, TG_VALUE_STREAM, (uint64_t)q) >> 40)) * (1.0 / 16777216.0));
-        pos++;
-      }
-    }
-    /* the last draw kept defines how many draws were consumed */
-    if (draws_out) {
-      int64_t seen = 0, q = 0;
-      for (; q < total; ++q) if (keys[q] != ~0ULL && ++seen == nnz) break;
-      *draws_out = q + 1;
-    }
-    free(cnt);
-  }
-
-done:
+  int rc;
+  if (tot <= 63) rc = tg_dedup64(order, nnz, shift, tot, seed, md, idx, val, draws_out);
+  else rc = tg_dedup128(order, nnz, shift, tot, seed, md, idx, val, draws_out);
   for (int m = 0; m < order; ++m) { free(md[m].cdf); free(md[m].perm); }
-  free(tkey); free(tmin); free(keys);
   return rc;
 }
