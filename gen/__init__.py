@@ -112,6 +112,10 @@ WORKLOADS = {
     "order4": Workload("order4", (500000, 20000, 2000, 1000), 150000000, (0.5, 0.5, 0.5, 0.5), 105),
     # SURVEY §8(d) "stress variant": heavy power law, one slice of ~7M nonzeros (reading Q16)
     "netflix_stress": Workload("netflix_stress", (480189, 17770, 2182), 100480507, (1.0, 1.0, 0.5), 106),
+    # Table IV's two large tensors (FROSTT extents): 67- and 69-bit sort keys, so the
+    # device build takes the 128-bit key path
+    "delicious": Workload("delicious", (532924, 17262471, 2480308), 140126181, (0.5, 0.5, 0.5), 107),
+    "nell1": Workload("nell1", (2902330, 2143368, 25495389), 143599552, (0.5, 0.5, 0.5), 108),
 }
 
 

@@ -136,12 +136,248 @@ __global__ void __launch_bounds__(256) k_ttmc(const TtmcParams P) {
   flush(own && !right_open);
 }
 
+// Staged, register-tiled variant (Ra + Rb <= kStagedMaxRow).  Per segment the output block
+// Y(i_n) is the Ra x Rb matrix sum_q v_q U_a(i_a(q),:)^T U_b(i_b(q),:): a sum of rank-1 updates, so
+// the warp tiles it like a GEMM accumulator.  The 32 lanes form an LP x LQ grid (LP = Ra/TP,
+// LQ = Rb/TQ) and each lane owns a TP x TQ block in registers; per nonzero a lane reads TP elements
+// of the staged A row and TQ elements of the staged B row (vector LDS, at most 8 distinct 16-byte
+// chunks per instruction: one wavefront) and issues TP*TQ FMAs (packed FFMA2 where TQ is even).
+// The warp copies each batch of kNB nonzeros' rows and values into shared memory with cp.async one
+// batch ahead, and the batch's indices two batches ahead, so the L2 gather latency overlaps the
+// previous batch's FMAs.  Batches never cross the tile's end: pidx and val are padded to whole
+// tiles with index 0 / value 0, so a tail batch's padding adds exactly 0.
+constexpr int kNB = 16;             // nonzeros per batch
+constexpr int kStagedMaxRow = 128;  // Ra + Rb bound (shared memory: 2 x 16 x 129 floats per warp)
+constexpr int kStagedWarps = 8;
+
+__host__ __device__ constexpr int ttmc_rows_words(int Ra, int Rb) { return kNB * (Ra + Rb) + kNB; }
+__host__ __device__ constexpr int ttmc_idx_words() { return 2 * kNB + 4; }
+__host__ __device__ constexpr int ttmc_warp_words(int Ra, int Rb) {
+  return 2 * ttmc_rows_words(Ra, Rb) + 2 * ttmc_idx_words();
+}
+
+// N consecutive floats from shared memory (aligned to min(16, 4N) bytes by the launch conditions)
+template <int N>
+__device__ __forceinline__ void lds_vec(const float* p, float (&x)[N]) {
+  if constexpr (N % 4 == 0) {
+#pragma unroll
+    for (int i = 0; i < N; i += 4) {
+      const float4 q = *reinterpret_cast<const float4*>(p + i);
+      x[i] = q.x; x[i + 1] = q.y; x[i + 2] = q.z; x[i + 3] = q.w;
+    }
+  } else if constexpr (N == 2) {
+    const float2 q = *reinterpret_cast<const float2*>(p);
+    x[0] = q.x; x[1] = q.y;
+  } else {
+#pragma unroll
+    for (int i = 0; i < N; ++i) x[i] = p[i];
+  }
+}
+
+// RA, RB: compile-time ranks for the common square cases (0 = runtime P.Ra / P.Rb)
+template <int TP, int TQ, bool V16, int RA, int RB>
+__global__ void __launch_bounds__(kStagedWarps * 32) k_ttmc_staged(const TtmcParams P) {
+  extern __shared__ uint4 smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int64_t t = P.tile_begin + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (t >= P.tile_end) return;
+  const int Ra = RA ? RA : P.Ra, Rb = RB ? RB : P.Rb;
+  const int RW = ttmc_rows_words(Ra, Rb);
+  float* rows = reinterpret_cast<float*>(smem_raw) + (threadIdx.x / 32) * ttmc_warp_words(Ra, Rb);
+  uint32_t* idxb = reinterpret_cast<uint32_t*>(rows + 2 * RW);  // 2 x {ia[NB], ib[NB], bf, pad}
+
+  const int LQ = Rb / TQ;
+  const int pa0 = (lane / LQ) * TP, qb0 = (lane % LQ) * TQ;  // the lane's block of Y(i_n)
+  const int64_t p0 = t * (int64_t)P.T;
+  const int64_t p1 = min(p0 + (int64_t)P.T, P.nnz);
+  const int nb = (int)((p1 - p0 + kNB - 1) / kNB);
+  const bool left_open = !((P.sf[t >> 5] >> (t & 31)) & 1u);
+  uint32_t s = P.seg_base[t] - 1u;
+  uint32_t row = 0;
+  if (left_open) row = P.seg_coord ? P.seg_coord[s] : s;
+  bool own = false;
+  float acc[TP][TQ];
+#pragma unroll
+  for (int i = 0; i < TP; ++i)
+#pragma unroll
+    for (int j = 0; j < TQ; ++j) acc[i][j] = 0.f;
+  auto flush = [&](bool store) {
+    float* o = P.out + (size_t)row * (uint32_t)P.W + (uint32_t)(pa0 * Rb + qb0);
+#pragma unroll
+    for (int i = 0; i < TP; ++i) {
+      float* oi = o + i * Rb;
+      if (store) {
+        if constexpr (TQ % 4 == 0) {
+#pragma unroll
+          for (int j = 0; j < TQ; j += 4)
+            *reinterpret_cast<float4*>(oi + j) = make_float4(acc[i][j], acc[i][j + 1], acc[i][j + 2], acc[i][j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < TQ; ++j) oi[j] = acc[i][j];
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < TQ; ++j) atomicAdd(oi + j, acc[i][j]);
+      }
+    }
+  };
+  auto open_segment = [&](int64_t p) {
+    if (p != p0) flush(own);
+#pragma unroll
+    for (int i = 0; i < TP; ++i)
+#pragma unroll
+      for (int j = 0; j < TQ; ++j) acc[i][j] = 0.f;
+    own = true;
+    ++s;
+    row = P.seg_coord ? P.seg_coord[s] : s;
+  };
+  // indices (and the bf word) of batch b into idx buffer b % 2
+  auto issue_idx = [&](int b) {
+    const int64_t pb = p0 + (int64_t)b * kNB;
+    uint32_t* d = idxb + (b & 1) * ttmc_idx_words();
+    if (lane < 4) cp_async16(d + lane * 4, P.pa + pb + lane * 4);
+    else if (lane < 8) cp_async16(d + kNB + (lane - 4) * 4, P.pb + pb + (lane - 4) * 4);
+    else if (lane == 8) cp_async4(d + 2 * kNB, P.bf + (pb >> 5));
+  };
+  // factor rows and values of batch b into row buffer b % 2 (indices already in shared memory)
+  auto issue_rows = [&](int b) {
+    const int64_t pb = p0 + (int64_t)b * kNB;
+    const uint32_t* ix = idxb + (b & 1) * ttmc_idx_words();
+    float* sA = rows + (b & 1) * RW;
+    float* sB = sA + kNB * Ra;
+    float* sV = sB + kNB * Rb;
+    // chunk c = lane + 32 j of the batch's kNB * cpn chunks (cpn per nonzero: A row then B row);
+    // when cpn divides 32 a lane keeps one column offset and steps 32 / cpn nonzeros per chunk
+    constexpr int CW = V16 ? 4 : 1;  // words per chunk
+    const int ca = Ra / CW, cpn = (Ra + Rb) / CW;
+    auto copy = [&](int e, int w) {
+      if (w < ca) {
+        if constexpr (V16) cp_async16(sA + e * Ra + CW * w, P.Ua + (size_t)ix[e] * (uint32_t)Ra + CW * w);
+        else cp_async4(sA + e * Ra + w, P.Ua + (size_t)ix[e] * (uint32_t)Ra + w);
+      } else {
+        const int wb = CW * (w - ca);
+        if constexpr (V16) cp_async16(sB + e * Rb + wb, P.Ub + (size_t)ix[kNB + e] * (uint32_t)Rb + wb);
+        else cp_async4(sB + e * Rb + wb, P.Ub + (size_t)ix[kNB + e] * (uint32_t)Rb + wb);
+      }
+    };
+    if (32 % cpn == 0) {
+      const int step = 32 / cpn, w = lane % cpn;
+      for (int e = lane / cpn; e < kNB; e += step) copy(e, w);
+    } else {
+      for (int c = lane; c < kNB * cpn; c += 32) {
+        const int e = c / cpn;
+        copy(e, c - e * cpn);
+      }
+    }
+    if constexpr (V16) {
+      if (lane < kNB / 4) cp_async16(sV + lane * 4, P.val + pb + lane * 4);
+    } else {
+      if (lane < kNB) cp_async4(sV + lane, P.val + pb + lane);
+    }
+  };
+
+  issue_idx(0);
+  cp_async_commit();
+  cp_async_wait<0>();
+  __syncwarp();
+  issue_rows(0);
+  if (nb > 1) issue_idx(1);
+  cp_async_commit();
+  for (int b = 0; b < nb; ++b) {
+    cp_async_wait<0>();  // rows of b and indices of b+1 have landed
+    __syncwarp();
+    const uint32_t bfw = idxb[(b & 1) * ttmc_idx_words() + 2 * kNB];
+    const uint32_t heads = (bfw >> ((b * kNB) & 31)) & ((1u << kNB) - 1u);
+    if (b + 1 < nb) {
+      issue_rows(b + 1);
+      if (b + 2 < nb) issue_idx(b + 2);
+    }
+    cp_async_commit();
+    const float* sA = rows + (b & 1) * RW + pa0;
+    const float* sB = rows + (b & 1) * RW + kNB * Ra + qb0;
+    const float* sV = rows + (b & 1) * RW + kNB * (Ra + Rb);
+    // operands of nonzero e+1 are loaded before the FMAs of e (two register sets)
+    float x[2][TP], y[2][TQ];
+    lds_vec<TP>(sA, x[0]);
+    lds_vec<TQ>(sB, y[0]);
+#pragma unroll
+    for (int e = 0; e < kNB; ++e) {
+      const int c = e & 1;
+      if (e + 1 < kNB) {
+        lds_vec<TP>(sA + (e + 1) * Ra, x[c ^ 1]);
+        lds_vec<TQ>(sB + (e + 1) * Rb, y[c ^ 1]);
+      }
+      if (heads && ((heads >> e) & 1u)) open_segment(p0 + (int64_t)b * kNB + e);
+      const float v = sV[e];
+#pragma unroll
+      for (int i = 0; i < TP; ++i) {
+        const float a = v * x[c][i];
+        if constexpr (TQ % 2 == 0) {  // packed FFMA2 (same per-element rounding as fmaf)
+          const float2 a2 = make_float2(a, a);
+#pragma unroll
+          for (int j = 0; j < TQ; j += 2) {
+            const float2 r = __ffma2_rn(a2, make_float2(y[c][j], y[c][j + 1]), make_float2(acc[i][j], acc[i][j + 1]));
+            acc[i][j] = r.x; acc[i][j + 1] = r.y;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < TQ; ++j) acc[i][j] = fmaf(a, y[c][j], acc[i][j]);
+        }
+      }
+    }
+    __syncwarp();  // row buffer b % 2 is refilled by issue_rows(b + 2)
+  }
+  const bool right_open = (t + 1 < P.ntiles) && !((P.sf[(t + 1) >> 5] >> ((t + 1) & 31)) & 1u);
+  flush(own && !right_open);
+}
+
+template <int TP, int TQ, int RA = 0, int RB = 0>
+bool try_staged(const TtmcParams& P, bool v16, cudaStream_t s, cudaError_t* err) {
+  if ((RA && P.Ra != RA) || (RB && P.Rb != RB)) return false;
+  // the lane grid must tile Ra x Rb exactly, and the vector LDS/STG need aligned runs
+  if (P.Ra % TP || P.Rb % TQ || (P.Ra / TP) * (P.Rb / TQ) != 32) return false;
+  if ((TP % 4 == 0 && P.Ra % 4) || (TP == 2 && P.Ra % 2)) return false;
+  if ((TQ % 4 == 0 && P.Rb % 4) || (TQ == 2 && P.Rb % 2)) return false;
+  if (TQ % 4 == 0 && (reinterpret_cast<uintptr_t>(P.out) & 15u)) return false;  // float4 stores
+  const size_t smem = sizeof(float) * (size_t)kStagedWarps * ttmc_warp_words(P.Ra, P.Rb);
+  const unsigned blocks = (unsigned)((P.tile_end - P.tile_begin + kStagedWarps - 1) / kStagedWarps);
+  auto kern = v16 ? k_ttmc_staged<TP, TQ, true, RA, RB> : k_ttmc_staged<TP, TQ, false, RA, RB>;
+  *err = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (*err == cudaSuccess && blocks) {
+    kern<<<blocks, kStagedWarps * 32, smem, s>>>(P);
+    count_launch();
+    *err = cudaGetLastError();
+  }
+  return true;
+}
+
+// Register tiles per lane, tried in order (balanced tiles first: fewest shared-memory loads).
+cudaError_t launch_staged(const TtmcParams& P, bool* done, cudaStream_t s) {
+  cudaError_t e = cudaSuccess;
+  const bool v16 = P.Ra % 4 == 0 && P.Rb % 4 == 0 && (reinterpret_cast<uintptr_t>(P.Ua) & 15u) == 0 &&
+                   (reinterpret_cast<uintptr_t>(P.Ub) & 15u) == 0 && (reinterpret_cast<uintptr_t>(P.val) & 15u) == 0;
+  *done = P.Ra + P.Rb <= kStagedMaxRow && P.W % 32 == 0 &&
+          (try_staged<4, 8, 32, 32>(P, v16, s, &e) || try_staged<2, 4, 16, 16>(P, v16, s, &e) ||
+           try_staged<1, 2, 8, 8>(P, v16, s, &e) || try_staged<4, 8>(P, v16, s, &e) || try_staged<8, 4>(P, v16, s, &e) || try_staged<4, 4>(P, v16, s, &e) ||
+           try_staged<2, 4>(P, v16, s, &e) || try_staged<4, 2>(P, v16, s, &e) || try_staged<2, 2>(P, v16, s, &e) ||
+           try_staged<1, 4>(P, v16, s, &e) || try_staged<4, 1>(P, v16, s, &e) || try_staged<1, 2>(P, v16, s, &e) ||
+           try_staged<2, 1>(P, v16, s, &e) || try_staged<1, 1>(P, v16, s, &e) || try_staged<2, 8>(P, v16, s, &e) ||
+           try_staged<8, 2>(P, v16, s, &e) || try_staged<1, 8>(P, v16, s, &e) || try_staged<8, 1>(P, v16, s, &e));
+  return e;
+}
+
 template <int NS>
 cudaError_t launch_ttmc_ns(const TtmcParams& P, cudaStream_t s) {
   const int TB = 256;
   int64_t threads = (P.tile_end - P.tile_begin) * 32;
   unsigned blocks = (unsigned)((threads + TB - 1) / TB);
   if (blocks == 0) return cudaSuccess;
+  static const bool staged_env = !getenv("FCOO_TTMC_UNSTAGED");
+  if (staged_env) {
+    bool done = false;
+    cudaError_t e = launch_staged(P, &done, s);
+    if (done || e != cudaSuccess) return e;
+  }
   // fast path: every lane's NS columns share p and run over contiguous q (NS divides Rb); the
   // float4 form also needs 16-byte aligned runs (Rb and NS multiples of 4, aligned Ub)
   const bool fast = (P.Rb % NS == 0) && P.W % 32 == 0 &&

@@ -34,6 +34,11 @@ def main():
             out = torch.empty((h.info.nsegs, a.R), device="cuda")
             for _ in range(a.reps):
                 P.fcoo_ttm(h, fs[n], a.R, out)
+        elif a.op == "ttmc":
+            h = P.fcoo_build(coo, n, tile_nnz=a.tile)
+            out = torch.empty((w.dims[n], a.R * a.R), device="cuda")
+            for _ in range(a.reps):
+                P.fcoo_ttmc(h, fs, out)
         else:
             h = P.fcoo_build(coo, n, tile_nnz=a.tile)
             out = torch.empty((w.dims[n], a.R), device="cuda")
