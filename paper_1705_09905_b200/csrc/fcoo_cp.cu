@@ -326,7 +326,7 @@ __global__ void k_scale(float* __restrict__ U, int64_t I, int R, const double* _
   if (l > 0) U[e] = (float)((double)U[e] / l);
 }
 
-__global__ void k_set_int(int* p, int v0, int v1) { p[0] = v0; p[1] = v1; }
+__global__ void k_set_int(int* p, int v0, int v1, int v2) { p[0] = v0; p[1] = v1; p[2] = v2; }
 
 // part[c] = sum_{i in chunk c} sum_r lambda_r M[i,r] U[i,r]   (M from the fp64 buffer when *use64;
 // nothing at all when run_if is given and *run_if == 0)
@@ -361,11 +361,16 @@ __global__ void k_sumsq_partial(const float* __restrict__ v, int64_t n, int64_t 
 // recompute; skipped unless g[1]): overwrite the fit and, if still >= kExactFit, make the next
 // iterations' main pass exact.
 constexpr double kExactFit = 0.9;
+// The fit of iteration *itc goes to fitd[*itc] (a device counter, so one captured iteration
+// replays unchanged); role 1 always advances the counter, role 0 only when inc (no role 1 launch).
 __global__ void k_fit(const double* __restrict__ inner_part, int ninner, const double* __restrict__ xsq_part,
                       int nxsq, GramPtrs G, int order, const double* __restrict__ lam, int R,
-                      double* __restrict__ out, int* __restrict__ g, int role) {
+                      double* __restrict__ fitd, int* __restrict__ itc, int* __restrict__ g, int role, int inc) {
   __shared__ double sh[kCT];
-  if (role == 1 && g[1] == 0) return;
+  if (role == 1 && g[1] == 0) {
+    if (threadIdx.x == 0) ++*itc;
+    return;
+  }
   double inner = 0.0, xsq = 0.0, xh = 0.0;
   // fixed-order sums (thread-strided then tree): deterministic
   for (int c = threadIdx.x; c < ninner; c += blockDim.x) inner += inner_part[c];
@@ -381,9 +386,10 @@ __global__ void k_fit(const double* __restrict__ inner_part, int ninner, const d
   if (threadIdx.x == 0) {
     double r2 = xsq + xh - 2.0 * inner;
     const double fit = 1.0 - sqrt(r2 > 0 ? r2 : 0.0) / sqrt(xsq);
-    out[0] = fit;
+    fitd[*itc] = fit;
     if (role == 0) g[1] = (g[0] == 0 && fit >= kExactFit) ? 1 : 0;
     else if (fit >= kExactFit) g[0] = 1;
+    if (role == 1 || inc) ++*itc;
   }
 }
 
@@ -424,15 +430,40 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
   Buf lam(&al, sizeof(double) * R, s), part(&al, sizeof(double) * maxchunks * RR, s);
   Buf ipart(&al, sizeof(double) * maxchunks, s), xpart(&al, sizeof(double) * maxchunks, s);
   Buf fitd(&al, sizeof(double) * (o->iters + 1), s), status(&al, sizeof(int) * 2, s);
-  Buf flags(&al, sizeof(int) * 2, s);  // fit-precision flags g[0], g[1] (see k_fit)
+  Buf flags(&al, sizeof(int) * 3, s);  // fit-precision flags g[0], g[1] (see k_fit); g[2] = iteration
   if (!M.ok() || !M64.ok() || !Gs.ok() || !Graw.ok() || !A.ok() || !Q.ok() || !W.ok() || !lam.ok() || !part.ok() || !ipart.ok() ||
       !xpart.ok() || !fitd.ok() || !status.ok() || !flags.ok()) {
     return fail(FCOO_ERR_OOM, "cp_als scratch");
   }
+  // The iterations run on a private non-blocking stream joined to the caller's at both ends, so
+  // they can be captured into a CUDA graph even when the caller passes the legacy default stream
+  // (which cannot be captured).  The join runs before the scratch buffers are freed on `s`.
+  cudaStream_t const user = s;
+  struct Join {
+    cudaStream_t user, ws = nullptr;
+    cudaEvent_t in = nullptr, out = nullptr;
+    ~Join() {
+      if (!ws) return;
+      cudaEventRecord(out, ws);
+      cudaStreamWaitEvent(user, out, 0);
+      cudaEventDestroy(in);
+      cudaEventDestroy(out);
+      cudaStreamDestroy(ws);  // released once its work completes
+    }
+  } join{user};
+  if (cudaStreamCreateWithFlags(&join.ws, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&join.in, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&join.out, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventRecord(join.in, user) != cudaSuccess || cudaStreamWaitEvent(join.ws, join.in, 0) != cudaSuccess) {
+    if (join.ws && !join.out) { cudaStreamDestroy(join.ws); join.ws = nullptr; }
+    return fail(FCOO_ERR_CUDA, "cp_als stream setup: %s", cudaGetErrorString(cudaGetLastError()));
+  }
+  s = join.ws;
   // sharded runs keep the last mode exact throughout (one fp64 all-reduce, no gated recompute)
   const bool sharded = o->comm && o->nranks > 1;
   int* g = flags.as<int>();
-  k_set_int<<<1, 1, 0, s>>>(g, sharded ? 1 : 0, 0);
+  int* itc = g + 2;
+  k_set_int<<<1, 1, 0, s>>>(g, sharded ? 1 : 0, 0, 0);
   FCOO_LAUNCH_CHECK();
   GramPtrs gp{};
   for (int m = 0; m < N; ++m) gp.g[m] = Gs.as<double>() + (int64_t)m * RR;
@@ -460,10 +491,10 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
     fcoo::count_launch();
     if (cudaGetLastError() != cudaSuccess) st = fail(FCOO_ERR_CUDA, "k_sumsq_partial");
   }
-  double fit_prev = 0.0;
-  int it = 0;
-  for (; it < o->iters && !st; ++it) {
-    for (int n = 0; n < N && !st; ++n) {
+  // One CP-ALS iteration (Alg. 1 body), enqueued on s with no host synchronisation.
+  auto iteration = [&]() -> fcoo_status {
+    fcoo_status st = FCOO_OK;
+    for (int n = 0; n < N; ++n) {
       const int64_t In = X->dims[n];
       const bool last = (n == N - 1);
       // M = MTTKRP_n.  The fit's <X, Xhat> is taken from the last mode's M, so near fit 1 that
@@ -478,7 +509,7 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
       } else {
         st = fcoo_mttkrp(H[n], factors, R, M.as<float>(), (void*)s);
       }
-      if (st) break;
+      if (st) return st;
       if (R <= kSmallR) {
         k_solve_small<<<1, kCT, 0, s>>>(gp, N, n, R, W.as<double>(), status.as<int>());
         FCOO_LAUNCH_CHECK();
@@ -490,7 +521,7 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
                                            In, R, factors[n]);
       FCOO_LAUNCH_CHECK();
       st = gram(factors[n], In, Graw.as<double>());
-      if (st) break;
+      if (st) return st;
       k_norm_stats<<<1, kCT, 0, s>>>(Graw.as<double>(), R, lam.as<double>(), lambda);
       FCOO_LAUNCH_CHECK();
       k_scale<<<nblk(In * R), kCT, 0, s>>>(factors[n], In, R, lam.as<double>());
@@ -498,8 +529,8 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
       // Gram of the STORED (normalised, fp32) factor, so |Xhat|^2 and V describe exactly the
       // model held in memory
       st = gram(factors[n], In, Gs.as<double>() + (int64_t)n * RR);
+      if (st) return st;
     }
-    if (st) break;
     const int nl = N - 1;
     const int64_t Il = X->dims[nl];
     int nc = chunks_for(Il);
@@ -508,19 +539,69 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
                                        lam.as<double>(), Il, R, per, ipart.as<double>());
     FCOO_LAUNCH_CHECK();
     k_fit<<<1, kCT, 0, s>>>(ipart.as<double>(), nc, xpart.as<double>(), nx, gp, N, lam.as<double>(), R,
-                            fitd.as<double>() + it, g, 0);
+                            fitd.as<double>(), itc, g, 0, sharded ? 1 : 0);
     FCOO_LAUNCH_CHECK();
     if (!sharded) {
       // the fp32 fit reached kExactFit: recompute the last mode's M exactly (it depends only on
       // the other modes' factors, unchanged since) and take the fit again -- all gated on g[1]
       st = run_mttkrp_f64(H[nl], factors, R, M64.as<double>(), s, g + 1, 1);
-      if (st) break;
+      if (st) return st;
       k_inner_partial<<<nc, kCT, 0, s>>>(M.as<float>(), M64.as<double>(), g + 1, g + 1, factors[nl],
                                          lam.as<double>(), Il, R, per, ipart.as<double>());
       FCOO_LAUNCH_CHECK();
       k_fit<<<1, kCT, 0, s>>>(ipart.as<double>(), nc, xpart.as<double>(), nx, gp, N, lam.as<double>(), R,
-                              fitd.as<double>() + it, g, 1);
+                              fitd.as<double>(), itc, g, 1, 0);
       FCOO_LAUNCH_CHECK();
+    }
+    return FCOO_OK;
+  };
+
+  // Iteration 0 runs eagerly; iteration 1 is captured into a CUDA graph and every later iteration
+  // replays it (the ~45 small launches of an iteration become one graph launch).  Any capture or
+  // instantiation failure falls back to eager launches.  FCOO_CP_NO_GRAPH=1 disables the graph.
+  static const bool no_graph = getenv("FCOO_CP_NO_GRAPH") != nullptr;
+  cudaGraphExec_t exec = nullptr;
+  uint64_t graph_kernels = 0;
+  struct ExecGuard { cudaGraphExec_t& e; ~ExecGuard() { if (e) cudaGraphExecDestroy(e); } } exec_guard{exec};
+  double fit_prev = 0.0;
+  int it = 0;
+  for (; it < o->iters && !st; ++it) {
+    if (it == 1 && !no_graph && o->iters > 2 &&
+        cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
+      const uint64_t before = fcoo::g_launches.load();
+      fcoo_status cst = iteration();
+      const uint64_t captured = fcoo::g_launches.load() - before;
+      fcoo::g_launches.fetch_sub(captured);  // recorded, not executed
+      cudaGraph_t graph = nullptr;
+      cudaError_t ce = cudaStreamEndCapture(s, &graph);
+      if (cst) {
+        if (graph) cudaGraphDestroy(graph);
+        st = cst;
+        break;
+      }
+      if (ce == cudaSuccess && graph) {
+        size_t nn = 0;
+        cudaGraphGetNodes(graph, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        if (nn) cudaGraphGetNodes(graph, nodes.data(), &nn);
+        for (auto nd : nodes) {
+          cudaGraphNodeType ty;
+          if (cudaGraphNodeGetType(nd, &ty) == cudaSuccess && ty == cudaGraphNodeTypeKernel) ++graph_kernels;
+        }
+        if (cudaGraphInstantiate(&exec, graph, 0) != cudaSuccess) exec = nullptr;
+        cudaGraphDestroy(graph);
+      }
+      if (!exec) (void)cudaGetLastError();  // eager fallback below
+    } else if (it == 1) {
+      (void)cudaGetLastError();  // a refused capture must not leave a sticky error behind
+    }
+    if (exec) {
+      cudaError_t ce = cudaGraphLaunch(exec, s);
+      if (ce != cudaSuccess) { st = fail(FCOO_ERR_CUDA, "graph launch: %s", cudaGetErrorString(ce)); break; }
+      fcoo::count_launch(graph_kernels);
+    } else {
+      st = iteration();
+      if (st) break;
     }
     if (iters_done) *iters_done = it + 1;
     if (o->tol > 0) {  // the stopping rule needs the fit on the host every iteration
