@@ -288,6 +288,7 @@ __global__ void __launch_bounds__(kStagedWarps * 32) k_ttmc_staged(const TtmcPar
     __syncwarp();
     const uint32_t bfw = idxb[(b & 1) * ttmc_idx_words() + 2 * kNB];
     const uint32_t heads = (bfw >> ((b * kNB) & 31)) & ((1u << kNB) - 1u);
+    __syncwarp();  // every lane has read idx buffer b % 2 before issue_idx(b + 2) refills it
     if (b + 1 < nb) {
       issue_rows(b + 1);
       if (b + 2 < nb) issue_idx(b + 2);

@@ -146,3 +146,29 @@ def test_netflix_stress_giant_slice(F):
         got = _run(F, w.dims, idx, val, mode, fs, 32, 0)
         M, D = oracle.mttkrp(w.dims, idx, val, mode, fs, nthreads=os.cpu_count() or 8)
         assert_parity(got, M, D, what=f"netflix stress mode {mode}")
+
+
+def test_order4_full_size(F):
+    """BASELINE configs[4] shape at full size (500K x 20K x 2K x 1K, 150M nnz), R=32, every mode,
+    automatic tile, element by element against the multi-threaded oracle."""
+    import os
+    w = gen.WORKLOADS["order4"]
+    idx, val = gen.coo(w.dims, w.nnz, w.alpha, w.seed)
+    for mode in range(4):
+        fs = gen.factors(w.dims, 32, 9)
+        got = _run(F, w.dims, idx, val, mode, fs, 32, 0)
+        M, D = oracle.mttkrp(w.dims, idx, val, mode, fs, nthreads=os.cpu_count() or 8)
+        assert_parity(got, M, D, what=f"order4 mode {mode}")
+
+
+def test_nell1_full_size_wide_keys(F):
+    """Table IV nell-1 extents at full size (143.6M nnz, 69-bit build keys -> the 128-bit sort
+    path), every mode, R=8 (keeps the fp64 oracle output for the 25.5M-row mode in host memory)."""
+    import os
+    w = gen.WORKLOADS["nell1"]
+    idx, val = gen.coo(w.dims, w.nnz, w.alpha, w.seed)
+    for mode in range(3):
+        fs = gen.factors(w.dims, 8, 10)
+        got = _run(F, w.dims, idx, val, mode, fs, 8, 0)
+        M, D = oracle.mttkrp(w.dims, idx, val, mode, fs, nthreads=os.cpu_count() or 8)
+        assert_parity(got, M, D, what=f"nell1 mode {mode}")

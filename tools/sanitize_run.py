@@ -12,6 +12,7 @@ sys.path.insert(0, ROOT)
 
 
 def main():
+    import numpy as np
     import torch
 
     import gen
@@ -32,8 +33,27 @@ def main():
             yo = torch.empty((t.info.nsegs, R), device="cuda")
             P.fcoo_ttm(t, fs[n], R, yo)
             t.destroy()
+    # SpTTMc: staged register-tiled kernels (4x8, 2x4, 1x2, scalar-copy variant) and the unstaged one
+    for ranks in ((32, 32), (16, 16), (8, 8), (2, 16), (3, 5)):
+        for n in range(3):
+            rk = [1, 1, 1]
+            others = [m for m in range(3) if m != n]
+            rk[others[0]], rk[others[1]] = ranks
+            fs = [torch.from_numpy(gen.uniform((d, r), 6, m)).cuda() for m, (d, r) in enumerate(zip(dims, rk))]
+            h = P.fcoo_build(coo, n, tile_nnz=64)
+            out = torch.empty((dims[n], ranks[0] * ranks[1]), device="cuda")
+            P.fcoo_ttmc(h, fs, out)
+            h.destroy()
+    # 128-bit build keys (65 key bits)
+    wd = ((1 << 32) - 1, (1 << 32) - 1, 2)
+    widx = np.stack([(np.arange(2000, dtype=np.uint64) * np.uint64(2654435761 + 2 * m) % np.uint64(wd[m]))
+                     .astype(np.uint32) for m in range(3)])
+    wc = P.Coo.from_numpy(wd, widx, np.ones(2000, np.float32))
+    for n in range(3):
+        P.fcoo_build(wc, n, tile_nnz=64, keep_perm=True).destroy()
+    # CP-ALS: eager first iteration, the captured graph for the rest, the exact-fit recompute
     fs = [torch.from_numpy(f).cuda() for f in gen.factors(dims, 8, 5)]
-    P.cp_als(coo, 8, 3, fs, tile_nnz=64)
+    P.cp_als(coo, 8, 4, fs, tile_nnz=64)
     torch.cuda.synchronize()
     print("sanitize_run OK")
 
