@@ -352,8 +352,260 @@ bool try_staged(const TtmcParams& P, bool v16, cudaStream_t s, cudaError_t* err)
   return true;
 }
 
+// Tensor-core variant for RA, RB multiples of 16 and 8: per segment Y(i_n) = A^T B with
+// A(k, p) = v_k U_a(i_a(k), p) and B(k, q) = U_b(i_b(k), q), K = the segment's nonzeros, is a dense
+// contraction, so each K-chunk of 8 staged nonzeros feeds mma.sync m16n8k8 TF32 tiles.  fp32
+// accuracy comes from the 3xTF32 split (x = hi + lo, both TF32; A·B ≈ hi·hi + hi·lo + lo·hi,
+// relative error ~2^-19 per product), and each chunk's tile product is started from zero and added
+// to the fp32 register accumulator with an RN FADD, so no long accumulation chain runs inside the
+// tensor core.  Staging (rows, values, indices via cp.async) is as in k_ttmc_staged, with row
+// strides padded by 8 words so the fragment loads are bank-conflict free.  A segment head inside a
+// chunk splits it: the sub-ranges run with the other nonzeros' values masked to 0.
+template <int RA, int RB>
+struct MmaGeom {
+  static constexpr int MT = RA / 16, NT = RB / 8;
+  static constexpr int SA = RA + 8, SB = RB + 8;  // padded row strides (words)
+  static constexpr int ROWS = kNB * (SA + SB) + kNB;  // one row buffer: A rows, B rows, values
+  static constexpr int WARP = 2 * ROWS;
+};
+
+// x = hi + lo with hi = x truncated to TF32 (sign, exponent, 10 mantissa bits: one LOP3) and
+// lo = x - hi exact in fp32; the tensor core reads lo's top 19 bits, so |x - hi - lo_tf32| <=
+// 2^-20 |x|.  (cvt.rna.tf32.f32 lowers to a ~5-instruction sequence on sm_100a; the mask is 2.)
+__device__ __forceinline__ void split_tf32(float x, uint32_t& hi, uint32_t& lo) {
+  hi = __float_as_uint(x) & 0xffffe000u;
+  lo = __float_as_uint(x - __uint_as_float(hi));
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+
+template <int RA, int RB>
+__global__ void __launch_bounds__(kStagedWarps * 32) k_ttmc_mma(const TtmcParams P) {
+  using Gm = MmaGeom<RA, RB>;
+  constexpr int MT = Gm::MT, NT = Gm::NT, SA = Gm::SA, SB = Gm::SB;
+  extern __shared__ uint4 smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int g = lane >> 2, tq = lane & 3;  // mma fragment coordinates
+  const int64_t t = P.tile_begin + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  if (t >= P.tile_end) return;
+  float* rows = reinterpret_cast<float*>(smem_raw) + (threadIdx.x / 32) * Gm::WARP;
+
+  const int64_t p0 = t * (int64_t)P.T;
+  const int64_t p1 = min(p0 + (int64_t)P.T, P.nnz);
+  const int nb = (int)((p1 - p0 + kNB - 1) / kNB);
+  const bool left_open = !((P.sf[t >> 5] >> (t & 31)) & 1u);
+  uint32_t s = P.seg_base[t] - 1u;
+  uint32_t row = 0;
+  if (left_open) row = P.seg_coord ? P.seg_coord[s] : s;
+  bool own = false;
+  float acc[MT][NT][4];
+#pragma unroll
+  for (int i = 0; i < MT; ++i)
+#pragma unroll
+    for (int j = 0; j < NT; ++j)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[i][j][c] = 0.f;
+  // C fragment (i, j): rows p = 16i + g (+8), columns q = 8j + 2tq (+1) of Y(i_n) (p outer, Eq.(4))
+  auto flush = [&](bool store) {
+    float* o = P.out + (size_t)row * (uint32_t)(RA * RB);
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j) {
+        float* o0 = o + (16 * i + g) * RB + 8 * j + 2 * tq;
+        float* o1 = o0 + 8 * RB;
+        if (store) {
+          *reinterpret_cast<float2*>(o0) = make_float2(acc[i][j][0], acc[i][j][1]);
+          *reinterpret_cast<float2*>(o1) = make_float2(acc[i][j][2], acc[i][j][3]);
+        } else {
+          atomicAdd(o0, acc[i][j][0]); atomicAdd(o0 + 1, acc[i][j][1]);
+          atomicAdd(o1, acc[i][j][2]); atomicAdd(o1 + 1, acc[i][j][3]);
+        }
+      }
+  };
+  auto open_segment = [&](int64_t p) {
+    if (p != p0) flush(own);
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) acc[i][j][c] = 0.f;
+    own = true;
+    ++s;
+    row = P.seg_coord ? P.seg_coord[s] : s;
+  };
+  // a batch's 16 + 16 indices in one register per lane (lane e < 16: i_a of nonzero e; lane
+  // 16 + e: i_b of nonzero e), loaded with one coalesced 128-byte load
+  auto ld_idx = [&](int b) -> uint32_t {
+    const int64_t pb = p0 + (int64_t)b * kNB;
+    return ld_stream4((lane < kNB ? P.pa : P.pb) + pb + (lane & (kNB - 1)));
+  };
+  // factor rows and values of batch b into row buffer b % 2; indices arrive by shuffle
+  auto issue_rows = [&](int b, uint32_t ixr) {
+    const int64_t pb = p0 + (int64_t)b * kNB;
+    float* sA = rows + (b & 1) * Gm::ROWS;
+    float* sB = sA + kNB * SA;
+    float* sV = sB + kNB * SB;
+    constexpr int CA = RA / 4, CPN = (RA + RB) / 4;  // 16-byte chunks per A row / per nonzero
+    if constexpr (32 % CPN == 0) {  // a lane keeps one chunk column and steps 32/CPN nonzeros
+      constexpr int STEP = 32 / CPN;
+      const int w = lane % CPN;
+      const bool isA = w < CA;
+      const float* base = isA ? P.Ua + 4 * w : P.Ub + 4 * (w - CA);
+      float* dst = isA ? sA + 4 * w : sB + 4 * (w - CA);
+      const int rs = isA ? RA : RB, ds = isA ? SA : SB, src0 = isA ? 0 : kNB;
+#pragma unroll
+      for (int e0 = 0; e0 < kNB; e0 += STEP) {
+        const int e = e0 + lane / CPN;
+        const uint32_t ix = __shfl_sync(0xffffffffu, ixr, src0 + e);
+        cp_async16(dst + e * ds, base + (size_t)ix * rs);
+      }
+    } else {
+#pragma unroll
+      for (int c0 = 0; c0 < kNB * CPN; c0 += 32) {
+        const int c = c0 + lane;
+        const int e = c / CPN, w = c - e * CPN;
+        const bool isA = w < CA;
+        const uint32_t ix = __shfl_sync(0xffffffffu, ixr, (isA ? 0 : kNB) + (e & (kNB - 1)));
+        if (c < kNB * CPN) {
+          if (isA) cp_async16(sA + e * SA + 4 * w, P.Ua + (size_t)ix * RA + 4 * w);
+          else cp_async16(sB + e * SB + 4 * (w - CA), P.Ub + (size_t)ix * RB + 4 * (w - CA));
+        }
+      }
+    }
+    if (lane < kNB / 4) cp_async16(sV + lane * 4, P.val + pb + lane * 4);
+  };
+  // one K-chunk of 8 staged nonzeros [k0, k0+8) into d, values outside [ks, ke) masked to 0
+  auto chunk = [&](float (&d)[MT][NT][4], const float* sA, const float* sB, const float* sV, int k0, int ks,
+                   int ke) {
+    const int ka = k0 + tq, kb = k0 + tq + 4;
+    const float va = (tq >= ks && tq < ke) ? sV[ka] : 0.f;
+    const float vb = (tq + 4 >= ks && tq + 4 < ke) ? sV[kb] : 0.f;
+    uint32_t ah[MT][4], al[MT][4];
+#pragma unroll
+    for (int i = 0; i < MT; ++i) {
+      const int m = 16 * i + g;
+      split_tf32(va * sA[ka * SA + m], ah[i][0], al[i][0]);
+      split_tf32(va * sA[ka * SA + m + 8], ah[i][1], al[i][1]);
+      split_tf32(vb * sA[kb * SA + m], ah[i][2], al[i][2]);
+      split_tf32(vb * sA[kb * SA + m + 8], ah[i][3], al[i][3]);
+    }
+#pragma unroll
+    for (int j = 0; j < NT; ++j) {
+      const int n = 8 * j + g;
+      uint32_t bh[2], bl[2];
+      split_tf32(sB[ka * SB + n], bh[0], bl[0]);
+      split_tf32(sB[kb * SB + n], bh[1], bl[1]);
+#pragma unroll
+      for (int i = 0; i < MT; ++i) {
+        mma_tf32(d[i][j], al[i], bh);
+        mma_tf32(d[i][j], ah[i], bl);
+        mma_tf32(d[i][j], ah[i], bh);
+      }
+    }
+  };
+  auto add_into_acc = [&](float (&d)[MT][NT][4]) {  // fp32 RN accumulation outside the tensor core
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          acc[i][j][c] += d[i][j][c];
+          d[i][j][c] = 0.f;
+        }
+  };
+
+  uint32_t ix_next = ld_idx(0);
+  uint32_t bf_cur = ld_stream4(P.bf + (p0 >> 5));
+  issue_rows(0, ix_next);
+  cp_async_commit();
+  ix_next = nb > 1 ? ld_idx(1) : 0u;
+  uint32_t ix_after = nb > 2 ? ld_idx(2) : 0u;  // indices run three batches ahead of the FMAs
+  for (int b = 0; b < nb; ++b) {
+    const uint32_t ix_far = b + 3 < nb ? ld_idx(b + 3) : 0u;
+    const uint32_t bf_next = b + 1 < nb ? ld_stream4(P.bf + ((p0 + (int64_t)(b + 1) * kNB) >> 5)) : 0u;
+    if (b + 1 < nb) issue_rows(b + 1, ix_next);
+    cp_async_commit();
+    cp_async_wait<1>();  // rows of batch b have landed (batch b+1 stays in flight)
+    __syncwarp();
+    const uint32_t heads = (bf_cur >> ((b * kNB) & 31)) & ((1u << kNB) - 1u);
+    const float* sA = rows + (b & 1) * Gm::ROWS;
+    const float* sB = sA + kNB * SA;
+    const float* sV = sB + kNB * SB;
+    float d[MT][NT][4];
+#pragma unroll
+    for (int i = 0; i < MT; ++i)
+#pragma unroll
+      for (int j = 0; j < NT; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) d[i][j][c] = 0.f;
+    if (heads == 0) {  // the common case: the whole batch continues the running segment
+      chunk(d, sA, sB, sV, 0, 0, 8);
+      chunk(d, sA, sB, sV, 8, 0, 8);
+      add_into_acc(d);
+    } else {  // sub-ranges between segment heads
+#pragma unroll
+      for (int k0 = 0; k0 < kNB; k0 += 8) {
+        uint32_t hm = (heads >> k0) & 0xffu;
+        int ks = 0;
+        while (true) {
+          const int e = hm ? __ffs(hm) - 1 : 8;
+          if (e > ks) {
+            chunk(d, sA, sB, sV, k0, ks, e);
+            add_into_acc(d);
+          }
+          if (e == 8) break;
+          open_segment(p0 + (int64_t)b * kNB + k0 + e);
+          hm &= hm - 1;
+          ks = e;
+        }
+      }
+    }
+    __syncwarp();  // row buffer b % 2 is refilled by issue_rows(b + 2)
+    ix_next = ix_after;
+    ix_after = ix_far;
+    bf_cur = bf_next;
+  }
+  const bool right_open = (t + 1 < P.ntiles) && !((P.sf[(t + 1) >> 5] >> ((t + 1) & 31)) & 1u);
+  flush(own && !right_open);
+}
+
+template <int RA, int RB>
+bool try_mma(const TtmcParams& P, cudaStream_t s, cudaError_t* err) {
+  if (P.Ra != RA || P.Rb != RB) return false;
+  if ((reinterpret_cast<uintptr_t>(P.Ua) | reinterpret_cast<uintptr_t>(P.Ub) | reinterpret_cast<uintptr_t>(P.val) |
+       reinterpret_cast<uintptr_t>(P.out)) & 15u)
+    return false;
+  const size_t smem = sizeof(float) * (size_t)kStagedWarps * MmaGeom<RA, RB>::WARP;
+  const unsigned blocks = (unsigned)((P.tile_end - P.tile_begin + kStagedWarps - 1) / kStagedWarps);
+  *err = cudaFuncSetAttribute(k_ttmc_mma<RA, RB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (*err == cudaSuccess && blocks) {
+    k_ttmc_mma<RA, RB><<<blocks, kStagedWarps * 32, smem, s>>>(P);
+    count_launch();
+    *err = cudaGetLastError();
+  }
+  return true;
+}
+
 // Register tiles per lane, tried in order (balanced tiles first: fewest shared-memory loads).
 cudaError_t launch_staged(const TtmcParams& P, bool* done, cudaStream_t s) {
+  static const bool use_mma = !getenv("FCOO_TTMC_NO_MMA");
+  if (use_mma) {
+    cudaError_t e = cudaSuccess;
+    if (try_mma<32, 32>(P, s, &e) || try_mma<16, 16>(P, s, &e) || try_mma<16, 32>(P, s, &e) ||
+        try_mma<32, 16>(P, s, &e) || try_mma<16, 64>(P, s, &e) || try_mma<64, 16>(P, s, &e) ||
+        try_mma<16, 8>(P, s, &e) || try_mma<32, 8>(P, s, &e) || try_mma<64, 8>(P, s, &e)) {
+      *done = true;
+      return e;
+    }
+  }
   cudaError_t e = cudaSuccess;
   const bool v16 = P.Ra % 4 == 0 && P.Rb % 4 == 0 && (reinterpret_cast<uintptr_t>(P.Ua) & 15u) == 0 &&
                    (reinterpret_cast<uintptr_t>(P.Ub) & 15u) == 0 && (reinterpret_cast<uintptr_t>(P.val) & 15u) == 0;

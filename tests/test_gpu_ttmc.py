@@ -101,3 +101,22 @@ def test_errors(F):
     with pytest.raises(F.FcooError) as e:
         F.fcoo_ttmc(hm, big, torch.empty((10, 2048), device="cuda"))
     assert e.value.code == 8  # FCOO_ERR_RANK
+
+
+def test_long_segment_accumulation(F):
+    """One slice holding 200K nonzeros (a single segment across ~100 tiles): the tensor-core path's
+    3xTF32 products and per-chunk fp32 accumulation must stay within 1e-4 over a long chain; signed
+    factors exercise cancellation."""
+    n = 200_000
+    dims = (2, 1000, 1000)
+    q = np.arange(n, dtype=np.int64)
+    idx = np.stack([np.zeros(n, np.int64), q // 1000 * 5 % 1000, q % 1000]).astype(np.uint32)
+    idx = np.unique(idx, axis=1)
+    val = (gen.uniform((idx.shape[1],), 131, 0) + 0.5).astype(np.float32)
+    for ranks in ((32, 32), (16, 16)):
+        fs = [gen.uniform((dims[0], 1), 132, 0, signed=True),
+              gen.uniform((dims[1], ranks[0]), 132, 1, signed=True),
+              gen.uniform((dims[2], ranks[1]), 132, 2, signed=True)]
+        got = _run(F, dims, idx, val, 0, fs, T=2048)
+        Y, D = oracle.ttmc(dims, idx, val, 0, [None, fs[1], fs[2]])
+        assert_parity(got, Y, D, what=f"long segment ranks={ranks}")
