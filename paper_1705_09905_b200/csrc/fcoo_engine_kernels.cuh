@@ -805,6 +805,23 @@ inline int engine_variant() {
   return v;
 }
 
+// CTAs per SM the staged kernel's shared-memory carveout is sized for: the register-limited count
+// (64K registers / (regs x 256 threads), at most 4), so shared memory never lowers occupancy and
+// the rest of the unified 228 KB stays L1 for the factor rows.  Measured: SpTTM (NP=1, 70 regs)
+// 2 -> 3 CTAs is 10-15% faster on brainq; MTTKRP (>= 94 regs) stays at 2.  Env FCOO_STAGED_CTAS
+// overrides (A/B).
+inline int staged_ctas_per_sm(const void* kern) {
+  const char* e = getenv("FCOO_STAGED_CTAS");
+  int v = e ? atoi(e) : 0;
+  if (v <= 0) {
+    cudaFuncAttributes fa;
+    v = 2;
+    if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && fa.numRegs > 0) v = 65536 / (fa.numRegs * 256);
+    if (v > 4) v = 4;
+  }
+  return v < 1 ? 1 : v > 8 ? 8 : v;
+}
+
 template <int NP, int G, int VEC, int CPL, class ACC>
 cudaError_t launch_one(const EngineParams& P, cudaStream_t s) {
   const bool full = (P.R == G * VEC * CPL);
@@ -828,7 +845,8 @@ cudaError_t launch_one(const EngineParams& P, cudaStream_t s) {
   if (!configured[full][ci]) {
     if (staged) {  // small staging buffers: ask for just enough carveout, keep the rest as L1
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      int pct = (int)((2 * smem * 100 + 228 * 1024 - 1) / (228 * 1024)) + 1;
+      const int ctas = staged_ctas_per_sm(reinterpret_cast<const void*>(kern));
+      int pct = (int)((ctas * smem * 100 + 228 * 1024 - 1) / (228 * 1024)) + 1;
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
     } else {  // no shared memory: give the whole unified carveout to L1 (factor rows)
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
