@@ -231,13 +231,12 @@ def main():
     P.fcoo_build(coo, 0, tile_nnz=T).destroy()  # warm-up: module load, allocator, CUB tuning
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    H = [P.fcoo_build(coo, n, tile_nnz=T) for n in range(N)]
+    # N > 1: fcoo_build_sharded = the redundant build + this rank's tile-aligned slice
+    H = [P.fcoo_build_sharded(coo, n, comm, tile_nnz=T) if world > 1 else P.fcoo_build(coo, n, tile_nnz=T)
+         for n in range(N)]
     T = H[0].info.tile_nnz  # the tile actually used (0 = automatic)
     torch.cuda.synchronize()
     build_ms = (time.perf_counter() - t0) * 1e3
-    if world > 1:
-        for h in H:
-            P.fcoo_set_shard(h, rank, world, comm)
 
     def factors(R_):
         return [torch.from_numpy(f).to(dev) for f in gen.factors(dims, R_, 7)]
@@ -447,10 +446,9 @@ def main():
             val_d = val_h.to(dev, non_blocking=True)
             fd = [f.to(dev, non_blocking=True) for f in f_h]
             c = P.Coo(dims, idx_d, val_d)
-            hs = [P.fcoo_build(c, n, tile_nnz=T, stream=stream) for n in range(N)]
+            hs = [P.fcoo_build_sharded(c, n, comm, tile_nnz=T, stream=stream) if world > 1
+                  else P.fcoo_build(c, n, tile_nnz=T, stream=stream) for n in range(N)]
             for n in range(N):
-                if world > 1:
-                    P.fcoo_set_shard(hs[n], rank, world, comm)
                 P.fcoo_mttkrp(hs[n], fd, R, outs[n], stream)
                 o_h[n].copy_(outs[n], non_blocking=True)
             torch.cuda.synchronize()

@@ -197,6 +197,16 @@ fcoo_status fcoo_allreduce_sum(fcoo_comm_t comm, float* buf, size_t count, void*
  * nshards == 1 restores the whole handle. */
 fcoo_status fcoo_set_shard(fcoo_t f, int shard, int nshards, fcoo_comm_t comm);
 
+/* fcoo_build_sharded — fcoo_build followed by fcoo_set_shard(rank, nranks, comm) with the rank
+ * and size of `comm` (every rank sorts the whole tensor redundantly —
+ * no distributed sort — and then works only on its tile-aligned, nnz-balanced slice; the
+ * handle keeps the full stream, the kernels read only the slice).  fcoo_mttkrp / fcoo_ttm on the
+ * result all-reduce the partial outputs over `comm`, so every rank receives the full output.
+ * Same inputs, ownership, host synchronisation and errors as fcoo_build, plus ARG for a NULL
+ * comm.  `comm` must outlive the handle. */
+fcoo_status fcoo_build_sharded(const fcoo_coo* coo, int mode, const fcoo_build_opts* opts, fcoo_comm_t comm,
+                               const fcoo_allocator* alloc, void* stream, fcoo_t* out);
+
 /* fcoo_shard_range — the tile range fcoo_set_shard uses (pure host arithmetic, no device):
  * [*begin, *end) = [floor(shard*ntiles/nshards), floor((shard+1)*ntiles/nshards)). */
 fcoo_status fcoo_shard_range(int64_t ntiles, int shard, int nshards, int64_t* begin, int64_t* end);

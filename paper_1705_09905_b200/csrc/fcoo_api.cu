@@ -83,6 +83,24 @@ fcoo_status fcoo_build(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
   return fcoo::build_impl(coo, mode, opts, alloc, (cudaStream_t)stream, out);
 }
 
+fcoo_status fcoo_build_sharded(const fcoo_coo* coo, int mode, const fcoo_build_opts* opts, fcoo_comm_t comm,
+                               const fcoo_allocator* alloc, void* stream, fcoo_t* out) {
+  if (!comm) return fcoo::fail(FCOO_ERR_ARG, "NULL comm");
+  if (!out) return fcoo::fail(FCOO_ERR_ARG, "NULL out");
+  int rank = 0, nranks = 1;
+  fcoo::comm_rank_size(comm, &rank, &nranks);
+  fcoo_t f = nullptr;
+  fcoo_status st = fcoo::build_impl(coo, mode, opts, alloc, (cudaStream_t)stream, &f);
+  if (st) return st;
+  st = fcoo_set_shard(f, rank, nranks, comm);
+  if (st) {
+    fcoo_destroy(f);
+    return st;
+  }
+  *out = f;
+  return FCOO_OK;
+}
+
 fcoo_status fcoo_mttkrp(fcoo_t f, const float* const* factors, int R, float* out, void* stream) {
   if (!f || !factors || !out) return fcoo::fail(FCOO_ERR_ARG, "NULL handle/factors/out");
   if (f->op != FCOO_OP_MTTKRP) return fcoo::fail(FCOO_ERR_SHAPE, "handle was built for SpTTM");

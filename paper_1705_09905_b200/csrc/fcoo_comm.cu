@@ -30,6 +30,11 @@ fcoo_status comm_allreduce_f64(fcoo_comm_t c, double* buf, size_t count, cudaStr
   return FCOO_OK;
 }
 
+void comm_rank_size(fcoo_comm_t c, int* rank, int* nranks) {
+  *rank = c ? c->rank : 0;
+  *nranks = c ? c->nranks : 1;
+}
+
 }  // namespace fcoo
 
 extern "C" {

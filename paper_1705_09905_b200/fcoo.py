@@ -69,7 +69,7 @@ class _CpOpts(ctypes.Structure):
 
 
 # The exported symbols (every one declared in include/fcoo.h).
-SYMBOLS = ["fcoo_build", "fcoo_mttkrp", "fcoo_ttm", "fcoo_ttmc", "fcoo_info", "fcoo_export", "fcoo_destroy",
+SYMBOLS = ["fcoo_build", "fcoo_build_sharded", "fcoo_mttkrp", "fcoo_ttm", "fcoo_ttmc", "fcoo_info", "fcoo_export", "fcoo_destroy",
            "fcoo_comm_unique_id", "fcoo_comm_init", "fcoo_comm_destroy", "fcoo_allreduce_sum", "fcoo_set_shard",
            "fcoo_shard_range", "cp_als", "fcoo_tns_read", "fcoo_tns_info", "fcoo_tns_copy", "fcoo_tns_destroy",
            "fcoo_tns_write", "fcoo_status_str", "fcoo_last_error", "fcoo_launch_count"]
@@ -88,6 +88,8 @@ def load_library():
     vp, ci, i64 = ctypes.c_void_p, ctypes.c_int, ctypes.c_int64
     L.fcoo_build.argtypes = [ctypes.POINTER(_Coo), ci, ctypes.POINTER(_BuildOpts), ctypes.POINTER(_Allocator), vp,
                              ctypes.POINTER(vp)]
+    L.fcoo_build_sharded.argtypes = [ctypes.POINTER(_Coo), ci, ctypes.POINTER(_BuildOpts), vp,
+                                     ctypes.POINTER(_Allocator), vp, ctypes.POINTER(vp)]
     L.fcoo_mttkrp.argtypes = [vp, ctypes.POINTER(vp), ci, vp, vp]
     L.fcoo_ttm.argtypes = [vp, vp, ci, vp, vp]
     L.fcoo_ttmc.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(ci), vp, vp]
@@ -286,6 +288,17 @@ def fcoo_build(coo: Coo, mode: int, op: int = OP_MTTKRP, tile_nnz: int = 0, keep
     out = ctypes.c_void_p()
     _check(L.fcoo_build(ctypes.byref(coo.c), mode, ctypes.byref(opts), ctypes.byref(_ALLOCATOR),
                         ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out)), "fcoo_build")
+    return Fcoo(out.value, coo)
+
+
+def fcoo_build_sharded(coo: Coo, mode: int, comm: "Comm", op: int = OP_MTTKRP, tile_nnz: int = 0,
+                       keep_perm: bool = False, stream=None) -> Fcoo:
+    """fcoo_build + fcoo_set_shard(comm.rank, comm.nranks, comm) in one C call."""
+    L = load_library()
+    opts = _BuildOpts(op, tile_nnz, BUILD_KEEP_PERM if keep_perm else 0)
+    out = ctypes.c_void_p()
+    _check(L.fcoo_build_sharded(ctypes.byref(coo.c), mode, ctypes.byref(opts), comm.h, ctypes.byref(_ALLOCATOR),
+                                ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out)), "fcoo_build_sharded")
     return Fcoo(out.value, coo)
 
 

@@ -54,6 +54,8 @@ def test_host_checked_errors_without_gpu():
     ptrs5 = (ctypes.c_void_p * 5)(8, 8, 8, 8, 8)
     cooK = fcoo._Coo(5, big, 10, ptrs5, 8)
     assert L.fcoo_build(ctypes.byref(cooK), 0, ctypes.byref(opts), None, None, ctypes.byref(out)) == fcoo.ERR_KEY_BITS
+    assert L.fcoo_build_sharded(ctypes.byref(coo3), 0, ctypes.byref(opts), None, None, None,
+                                ctypes.byref(out)) == fcoo.ERR_ARG  # NULL comm
     assert L.fcoo_mttkrp(None, None, 8, None, None) == fcoo.ERR_ARG
     assert L.fcoo_ttm(None, None, 8, None, None) == fcoo.ERR_ARG
     assert L.fcoo_status_str(fcoo.ERR_DUPLICATE) == b"FCOO_ERR_DUPLICATE"

@@ -106,6 +106,29 @@ def test_fake_multirank_shards(F, shards):
         _check(F, dims, idx, val, mode, 32, T=64, shards=shards)
 
 
+def test_build_sharded_single_rank_comm(F):
+    """fcoo_build_sharded with a 1-rank communicator: shard 0 of 1 is the whole
+    tensor, no collective runs, and the result equals the oracle; the handle reports the shard."""
+    import torch
+    dims = (300, 200, 100)
+    idx, val = gen.coo(dims, 20000, (0.5, 0.5, 0.5), 41)
+    R = 16
+    fs = gen.factors(dims, R, 3, signed=True)
+    comm = F.fcoo_comm_init(0, 1, F.fcoo_comm_unique_id())
+    coo = F.Coo.from_numpy(dims, idx, val)
+    ft = [torch.from_numpy(f).cuda() for f in fs]
+    for mode in range(3):
+        h = F.fcoo_build_sharded(coo, mode, comm, tile_nnz=64)
+        assert (h.info.shard, h.info.nshards, h.info.tile_begin, h.info.tile_end) == (0, 1, 0, h.info.ntiles)
+        out = torch.full((dims[mode], R), float("nan"), device="cuda")
+        F.fcoo_mttkrp(h, ft, R, out)
+        torch.cuda.synchronize()
+        M, D = oracle.mttkrp(dims, idx, val, mode, fs, nthreads=8)
+        assert_parity(out.cpu().numpy(), M, D, what=f"build_sharded mode={mode}")
+        h.destroy()
+    comm.destroy()
+
+
 def test_deterministic_repeat(F):
     """Stores + boundary-only atomics: repeated calls agree to the last bit except where
     red.add ordering differs; rows fully owned by one tile are bitwise stable."""
