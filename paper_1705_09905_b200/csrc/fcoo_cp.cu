@@ -5,14 +5,20 @@
 // a Jacobi pseudo-inverse when V is not positive definite (reading Q14); k_apply: U_n = M W
 // (fp64 accumulation, fp32 store); k_gram_partial + k_gram_reduce: G_raw = U_n^T U_n (fp64,
 // deterministic two-stage sum); k_norm_stats: lambda = sqrt(diag G_raw); k_scale: U_n /= lambda
-// (reading Q13); then G_n = Gram of the stored normalised U_n.  After the last mode,
+// (reading Q13); then G_n = Gram of the stored normalised U_n.  Fast path (R | 256, R <= 64, the
+// paper's ranks): k_apply_colsq (U_n = M W fused with the column norms -> lambda; only the Gram's
+// diagonal was ever used) and k_gram_chunks (normalise in place + Gram partials in one pass) +
+// k_gram_reduce_t (+ k_colsq_reduce): 4 launches after the MTTKRP instead of 7.  The R x R solve of mode n needs
+// only the other modes' Grams, which are final before MTTKRP_n starts, so it runs on a second
+// stream concurrently with the MTTKRP (the paper's "second stream") and is joined before
+// k_apply.  After the last mode,
 // k_inner_partial + k_fit compute the fit from <X,Xhat> = sum_r lambda_r sum_i M(i,r) U_N(i,r)
 // and |Xhat|^2 = lambda^T (Hadamard G_m) lambda with no extra pass over X; the last mode's M is
 // accumulated in fp64 so the cancellation in |X|^2 + |Xhat|^2 - 2<X,Xhat> near fit = 1 does
 // not swamp the result.  Every reduction has a fixed order, so
 // replicated ranks compute bit-identical factors from identical M.
 // The paper runs the small matrix ops with CUBLAS on a second stream; here they are
-// microsecond-scale single-purpose kernels on the same stream.
+// microsecond-scale single-purpose kernels, the solve on a second stream.
 #include <math.h>
 #include <string.h>
 
@@ -265,11 +271,66 @@ __global__ void k_gram_partial(const float* __restrict__ U, int64_t I, int R, in
   }
 }
 
-// Tiled Gram partial for R <= 64: 32-row tiles of U staged in shared memory (coalesced loads);
-// thread tid owns entries e = tid + k*256 (k < EPT) of the R x R block in fp64 registers.
+// Fast path for R | 256, R <= 64 (the paper's ranks): U = M W over a fixed grid of row chunks,
+// fused with the column sums of squares of the STORED fp32 U (the diagonal of its Gram: all that
+// lambda needs, so the full pre-normalisation Gram is not formed); per-chunk partials go
+// column-major to cpart for k_colsq_reduce.
+__global__ void __launch_bounds__(kCT) k_apply_colsq(const float* __restrict__ M, const double* __restrict__ M64,
+                                                     const int* __restrict__ use64, const double* __restrict__ W,
+                                                     int64_t I, int R, float* __restrict__ U, int64_t rows_per,
+                                                     double* __restrict__ cpart) {
+  __shared__ double sh[kCT];
+  const int tid = threadIdx.x;
+  const int b = tid % R, rstep = kCT / R;
+  const int64_t i0 = (int64_t)blockIdx.x * rows_per, i1 = min(I, i0 + rows_per);
+  const bool f64 = use64 && *use64;
+  double cs = 0.0;
+  for (int64_t i = i0 + tid / R; i < i1; i += rstep) {
+    const float u = (float)(f64 ? row_dot(M64 + i * R, W, R, b) : row_dot(M + i * R, W, R, b));
+    U[i * R + b] = u;
+    cs += (double)u * (double)u;
+  }
+  sh[tid] = cs;
+  __syncthreads();
+  if (tid < R) {
+    double t = 0.0;
+    for (int q = 0; q < rstep; ++q) t += sh[tid + q * R];
+    cpart[(int64_t)tid * gridDim.x + blockIdx.x] = t;  // column-major: contiguous per column
+  }
+}
+
+// lambda[col] = sqrt(sum_c cpart[col * nchunks + c]): one warp per column, 8 independent
+// lane accumulators (memory-level parallelism), combined in a fixed order: deterministic.
+__global__ void k_colsq_reduce(const double* __restrict__ cpart, int nchunks, int R, double* __restrict__ lam,
+                               float* __restrict__ lam_f) {
+  const int col = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (col >= R) return;
+  const double* p = cpart + (int64_t)col * nchunks;
+  double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+  int c = lane;
+  for (; c + 7 * 32 < nchunks; c += 8 * 32) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] += p[c + k * 32];
+  }
+  for (int k = 0; c < nchunks; c += 32, ++k) a[k] += p[c];
+  double t = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) {
+    const double l = sqrt(t);
+    lam[col] = l;
+    if (lam_f) lam_f[col] = (float)l;
+  }
+}
+
+// Gram partials for R <= 64 over a fixed grid of row chunks, written entry-major
+// (part[e * nchunks + c]) for the warp-per-entry reduce.  With lam != nullptr the tile is first
+// normalised exactly as k_scale does (fp32 (double)U / lambda) and written back, so the Gram is
+// that of the stored normalised factor in the same pass.
 template <int EPT>
-__global__ void __launch_bounds__(kCT) k_gram_tiled(const float* __restrict__ U, int64_t I, int R, int64_t rows_per,
-                                                    double* __restrict__ part) {
+__global__ void __launch_bounds__(kCT) k_gram_chunks(float* __restrict__ U, int64_t I, int R, int64_t rows_per,
+                                                     const double* __restrict__ lam, double* __restrict__ part) {
   constexpr int TR = 32;
   __shared__ float tile[TR * 64];
   const int c = blockIdx.x;
@@ -287,7 +348,17 @@ __global__ void __launch_bounds__(kCT) k_gram_tiled(const float* __restrict__ U,
   for (int64_t r0 = i0; r0 < i1; r0 += TR) {
     const int nr = (int)min((int64_t)TR, i1 - r0);
     __syncthreads();
-    for (int q = threadIdx.x; q < nr * R; q += kCT) tile[q] = U[r0 * R + q];
+    for (int q = threadIdx.x; q < nr * R; q += kCT) {
+      float x = U[r0 * R + q];
+      if (lam) {
+        const double l = lam[q % R];
+        if (l > 0) {
+          x = (float)((double)x / l);
+          U[r0 * R + q] = x;
+        }
+      }
+      tile[q] = x;
+    }
     __syncthreads();
     for (int r = 0; r < nr; ++r) {
 #pragma unroll
@@ -297,8 +368,22 @@ __global__ void __launch_bounds__(kCT) k_gram_tiled(const float* __restrict__ U,
 #pragma unroll
   for (int k = 0; k < EPT; ++k) {
     const int e = threadIdx.x + k * kCT;
-    if (e < RR) part[(int64_t)c * RR + e] = acc[k];
+    if (e < RR) part[(int64_t)e * gridDim.x + c] = acc[k];
   }
+}
+
+// G[e] = sum_c part[e * nchunks + c]: one warp per entry, lane-strided then a fixed xor tree
+// (deterministic; contiguous loads).
+__global__ void k_gram_reduce_t(const double* __restrict__ part, int nchunks, int RR, double* __restrict__ G) {
+  const int e = (int)(((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int lane = threadIdx.x & 31;
+  if (e >= RR) return;
+  const double* p = part + (int64_t)e * nchunks;
+  double t = 0.0;
+  for (int c = lane; c < nchunks; c += 32) t += p[c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (lane == 0) G[e] = t;
 }
 
 __global__ void k_gram_reduce(const double* __restrict__ part, int nchunks, int RR, double* __restrict__ G) {
@@ -431,6 +516,11 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
   Buf ipart(&al, sizeof(double) * maxchunks, s), xpart(&al, sizeof(double) * maxchunks, s);
   Buf fitd(&al, sizeof(double) * (o->iters + 1), s), status(&al, sizeof(int) * 2, s);
   Buf flags(&al, sizeof(int) * 3, s);  // fit-precision flags g[0], g[1] (see k_fit); g[2] = iteration
+  // fast per-mode path (R | 256, R <= 64): fused apply + column norms, fused normalise + Gram
+  const bool fast = (kCT % R) == 0 && R <= 64;
+  constexpr int kApplyChunks = 16 * 148;  // >= one element per thread up to I*R = 9.7M
+  Buf cpart(&al, sizeof(double) * kApplyChunks * R, s);
+  if (!cpart.ok()) return fail(FCOO_ERR_OOM, "cp_als scratch");
   if (!M.ok() || !M64.ok() || !Gs.ok() || !Graw.ok() || !A.ok() || !Q.ok() || !W.ok() || !lam.ok() || !part.ok() || !ipart.ok() ||
       !xpart.ok() || !fitd.ok() || !status.ok() || !flags.ok()) {
     return fail(FCOO_ERR_OOM, "cp_als scratch");
@@ -459,6 +549,26 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
     return fail(FCOO_ERR_CUDA, "cp_als stream setup: %s", cudaGetErrorString(cudaGetLastError()));
   }
   s = join.ws;
+  // second stream for the R x R solve, forked from and joined into s each mode (captured into the
+  // graph as a parallel branch); high priority so its single CTA is scheduled as soon as an SM
+  // slot frees up during the MTTKRP
+  struct Side {
+    cudaStream_t st = nullptr;
+    cudaEvent_t fork = nullptr, done = nullptr;
+    ~Side() {
+      if (fork) cudaEventDestroy(fork);
+      if (done) cudaEventDestroy(done);
+      if (st) cudaStreamDestroy(st);
+    }
+  } side;
+  {
+    int lo = 0, hi = 0;
+    cudaDeviceGetStreamPriorityRange(&lo, &hi);
+    if (cudaStreamCreateWithPriority(&side.st, cudaStreamNonBlocking, hi) != cudaSuccess ||
+        cudaEventCreateWithFlags(&side.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&side.done, cudaEventDisableTiming) != cudaSuccess)
+      return fail(FCOO_ERR_CUDA, "cp_als side stream: %s", cudaGetErrorString(cudaGetLastError()));
+  }
   // sharded runs keep the last mode exact throughout (one fp64 all-reduce, no gated recompute)
   const bool sharded = o->comm && o->nranks > 1;
   int* g = flags.as<int>();
@@ -469,13 +579,24 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
   for (int m = 0; m < N; ++m) gp.g[m] = Gs.as<double>() + (int64_t)m * RR;
 
   auto chunks_for = [&](int64_t I) { return (int)std::min<int64_t>(maxchunks, std::max<int64_t>(1, (I + 127) / 128)); };
+  // Gram of U (R <= 64: chunked partials entry-major + warp-per-entry reduce; with lam the chunks
+  // also normalise U in place first, see k_gram_chunks)
+  auto gram_fast = [&](float* U, int64_t I, const double* lamp, double* out) -> fcoo_status {
+    const int nc = (int)std::min<int64_t>(maxchunks, std::max<int64_t>(1, (I + 63) / 64));
+    const int64_t per = (I + nc - 1) / nc;
+    if (RR <= kCT) k_gram_chunks<1><<<nc, kCT, 0, s>>>(U, I, R, per, lamp, part.as<double>());
+    else if (RR <= 4 * kCT) k_gram_chunks<4><<<nc, kCT, 0, s>>>(U, I, R, per, lamp, part.as<double>());
+    else k_gram_chunks<16><<<nc, kCT, 0, s>>>(U, I, R, per, lamp, part.as<double>());
+    FCOO_LAUNCH_CHECK();
+    k_gram_reduce_t<<<nblk((int64_t)RR * 32), kCT, 0, s>>>(part.as<double>(), nc, RR, out);
+    FCOO_LAUNCH_CHECK();
+    return FCOO_OK;
+  };
   auto gram = [&](const float* U, int64_t I, double* out) -> fcoo_status {
+    if (R <= 64) return gram_fast(const_cast<float*>(U), I, nullptr, out);
     int nc = chunks_for(I);
     int64_t per = (I + nc - 1) / nc;
-    if (RR <= kCT) k_gram_tiled<1><<<nc, kCT, 0, s>>>(U, I, R, per, part.as<double>());
-    else if (RR <= 4 * kCT) k_gram_tiled<4><<<nc, kCT, 0, s>>>(U, I, R, per, part.as<double>());
-    else if (RR <= 16 * kCT) k_gram_tiled<16><<<nc, kCT, 0, s>>>(U, I, R, per, part.as<double>());
-    else k_gram_partial<<<nc, kCT, 0, s>>>(U, I, R, per, part.as<double>());
+    k_gram_partial<<<nc, kCT, 0, s>>>(U, I, R, per, part.as<double>());
     FCOO_LAUNCH_CHECK();
     k_gram_reduce<<<nblk(RR), kCT, 0, s>>>(part.as<double>(), nc, RR, out);
     FCOO_LAUNCH_CHECK();
@@ -500,6 +621,17 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
       // M = MTTKRP_n.  The fit's <X, Xhat> is taken from the last mode's M, so near fit 1 that
       // one accumulates exact fp64 products: both launches are enqueued and
       // the device flag g[0] lets exactly one of them work, with no host synchronisation.
+      // fork: the solve for mode n reads only G_m (m != n), final at this point
+      FCOO_CUDA_TRY(cudaEventRecord(side.fork, s));
+      FCOO_CUDA_TRY(cudaStreamWaitEvent(side.st, side.fork, 0));
+      if (R <= kSmallR) {
+        k_solve_small<<<1, kCT, 0, side.st>>>(gp, N, n, R, W.as<double>(), status.as<int>());
+        FCOO_LAUNCH_CHECK();
+      }
+      k_solve<<<1, kCT, 0, side.st>>>(gp, N, n, R, A.as<double>(), Q.as<double>(), W.as<double>(),
+                                      status.as<int>(), R <= kSmallR ? 1 : 0);
+      FCOO_LAUNCH_CHECK();
+      FCOO_CUDA_TRY(cudaEventRecord(side.done, side.st));
       if (last && sharded) {
         st = run_mttkrp_f64(H[n], factors, R, M64.as<double>(), s);
         if (!st) st = comm_allreduce_f64(o->comm, M64.as<double>(), (size_t)In * R, s);
@@ -510,13 +642,21 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
         st = fcoo_mttkrp(H[n], factors, R, M.as<float>(), (void*)s);
       }
       if (st) return st;
-      if (R <= kSmallR) {
-        k_solve_small<<<1, kCT, 0, s>>>(gp, N, n, R, W.as<double>(), status.as<int>());
+      FCOO_CUDA_TRY(cudaStreamWaitEvent(s, side.done, 0));  // join: W ready
+      if (fast) {
+        const int nb = (int)std::min<int64_t>(kApplyChunks, std::max<int64_t>(1, (In * R + kCT - 1) / kCT));
+        const int64_t per = (In + nb - 1) / nb;
+        k_apply_colsq<<<nb, kCT, 0, s>>>(M.as<float>(), M64.as<double>(), last ? g : nullptr, W.as<double>(), In, R,
+                                         factors[n], per, cpart.as<double>());
         FCOO_LAUNCH_CHECK();
+        k_colsq_reduce<<<nblk((int64_t)R * 32), kCT, 0, s>>>(cpart.as<double>(), nb, R, lam.as<double>(), lambda);
+        FCOO_LAUNCH_CHECK();
+        // normalise in place and take the Gram of the STORED (normalised, fp32) factor in the same
+        // pass, so |Xhat|^2 and V describe exactly the model held in memory
+        st = gram_fast(factors[n], In, lam.as<double>(), Gs.as<double>() + (int64_t)n * RR);
+        if (st) return st;
+        continue;
       }
-      k_solve<<<1, kCT, 0, s>>>(gp, N, n, R, A.as<double>(), Q.as<double>(), W.as<double>(), status.as<int>(),
-                                R <= kSmallR ? 1 : 0);
-      FCOO_LAUNCH_CHECK();
       k_apply<<<nblk(In * R), kCT, 0, s>>>(M.as<float>(), M64.as<double>(), last ? g : nullptr, W.as<double>(),
                                            In, R, factors[n]);
       FCOO_LAUNCH_CHECK();
