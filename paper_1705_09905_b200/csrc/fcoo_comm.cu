@@ -15,7 +15,7 @@ struct fcoo_comm_s {
 namespace fcoo {
 
 fcoo_status comm_allreduce(fcoo_comm_t c, float* buf, size_t count, cudaStream_t s) {
-  if (!c || c->nranks == 1) return FCOO_OK;
+  if (!c || !c->comm) return FCOO_OK;
   ncclResult_t r = ncclAllReduce(buf, buf, count, ncclFloat, ncclSum, c->comm, s);
   if (r != ncclSuccess) return fail(FCOO_ERR_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
   count_launch();
@@ -23,7 +23,7 @@ fcoo_status comm_allreduce(fcoo_comm_t c, float* buf, size_t count, cudaStream_t
 }
 
 fcoo_status comm_allreduce_f64(fcoo_comm_t c, double* buf, size_t count, cudaStream_t s) {
-  if (!c || c->nranks == 1) return FCOO_OK;
+  if (!c || !c->comm) return FCOO_OK;
   ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, s);
   if (r != ncclSuccess) return fail(FCOO_ERR_NCCL, "ncclAllReduce(f64): %s", ncclGetErrorString(r));
   count_launch();
@@ -54,7 +54,9 @@ fcoo_status fcoo_comm_init(int rank, int nranks, const void* uid128, fcoo_comm_t
   fcoo_comm_s* c = new fcoo_comm_s();
   c->rank = rank;
   c->nranks = nranks;
-  if (nranks > 1) {
+  // a 1-rank communicator is a real NCCL communicator too (the handles never attach it: sharding
+  // into one shard drops the comm), so the NCCL path can be exercised on a single GPU
+  {
     ncclUniqueId id;
     memcpy(&id, uid128, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);

@@ -1,0 +1,91 @@
+"""The NCCL path of the multi-GPU combine on one GPU: a 1-rank
+torch.distributed NCCL group broadcasts the library's unique id (comm_from_process_group), the
+library's own NCCL communicator all-reduces through fcoo_allreduce_sum, and a sharded build over
+that communicator runs SpMTTKRP.  With one rank the all-reduce is the identity; the multi-rank
+arithmetic of the same code is covered by the fake-shard GPU tests and the gloo CPU tests."""
+import os
+import socket
+
+import numpy as np
+import pytest
+
+import gen
+import oracle
+from parity import assert_parity
+
+pytestmark = pytest.mark.gpu
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+@pytest.fixture(scope="module")
+def pg():
+    import torch
+    import torch.distributed as dist
+    assert torch.cuda.is_available()
+    torch.cuda.set_device(0)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(_free_port())
+    dist.init_process_group("nccl", rank=0, world_size=1, device_id=torch.device("cuda", 0))
+    yield dist
+    dist.destroy_process_group()
+
+
+def test_allreduce_through_library_communicator(pg):
+    import torch
+    import paper_1705_09905_b200 as P
+    comm = P.comm_from_process_group()
+    assert (comm.rank, comm.nranks) == (0, 1)
+    x = torch.arange(1000, dtype=torch.float32, device="cuda") * 0.5 - 7.0
+    ref = x.clone()
+    P.fcoo_allreduce_sum(comm, x)
+    torch.cuda.synchronize()
+    assert torch.equal(x, ref)  # sum over one rank
+    comm.destroy()
+
+
+def test_sharded_build_over_nccl_comm(pg):
+    import torch
+    import paper_1705_09905_b200 as P
+    comm = P.comm_from_process_group()
+    dims = (500, 300, 200)
+    idx, val = gen.coo(dims, 40000, (0.5, 0.5, 0.5), 43)
+    R = 32
+    fs = gen.factors(dims, R, 4, signed=True)
+    coo = P.Coo.from_numpy(dims, idx, val)
+    ft = [torch.from_numpy(f).cuda() for f in fs]
+    for mode in range(3):
+        h = P.fcoo_build_sharded(coo, mode, comm)
+        out = torch.full((dims[mode], R), float("nan"), device="cuda")
+        P.fcoo_mttkrp(h, ft, R, out)
+        torch.cuda.synchronize()
+        M, D = oracle.mttkrp(dims, idx, val, mode, fs, nthreads=8)
+        assert_parity(out.cpu().numpy(), M, D, what=f"nccl comm mode={mode}")
+        h.destroy()
+    comm.destroy()
+
+
+def test_cp_als_with_comm_matches_without(pg):
+    """cp_als given the 1-rank communicator runs the same iteration as the comm-less call (the
+    boundary red.add order of the MTTKRP is not fixed, so runs agree to rounding, not bitwise)."""
+    import torch
+    import paper_1705_09905_b200 as P
+    comm = P.comm_from_process_group()
+    dims = (60, 50, 40)
+    idx, val = gen.coo(dims, 8000, (0.3, 0.3, 0.3), 44)
+    R = 8
+    init = gen.factors(dims, R, 12)
+    coo = P.Coo.from_numpy(dims, idx, val)
+    a = [torch.from_numpy(f).cuda() for f in init]
+    b = [torch.from_numpy(f).cuda() for f in init]
+    _, ta = P.cp_als(coo, R, 5, a)
+    _, tb = P.cp_als(coo, R, 5, b, comm=comm)
+    torch.cuda.synchronize()
+    assert np.allclose(np.asarray(ta), np.asarray(tb), rtol=0, atol=1e-7)
+    for x, y in zip(a, b):
+        assert torch.allclose(x, y, rtol=0, atol=1e-4)
+    comm.destroy()
