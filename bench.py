@@ -40,6 +40,9 @@ def parse():
     ap.add_argument("--R", type=int, default=32)
     ap.add_argument("--tile", type=int, default=0, help="tile_nnz; 0 = the library's automatic choice")
     ap.add_argument("--nnz", type=int, default=None, help="override nnz (debug only; not a bench number)")
+    ap.add_argument("--fused-combine", action="store_true",
+                    help="N > 1: combine the ranks' partial outputs in the MTTKRP epilogue through an NVLS "
+                         "multicast buffer (fcoo_mttkrp_mc) instead of a separate NCCL all-reduce")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -246,11 +249,18 @@ def main():
     flops_step = N * R * nnz * N  # every mode
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(N)]
 
+    mc = None
+    if a.fused_combine and world > 1:  # one multicast-bound output buffer, reused by every mode
+        mc = P.McBuffer(comm, max(dims) * R)
+
     def step(record=None):
         for n in range(N):
             if record is not None:
                 record[n][0].record(stream)
-            P.fcoo_mttkrp(H[n], fs, R, outs[n], stream)
+            if mc is not None:
+                P.fcoo_mttkrp_mc(H[n], fs, R, mc, stream)
+            else:
+                P.fcoo_mttkrp(H[n], fs, R, outs[n], stream)
             if record is not None:
                 record[n][1].record(stream)
 
@@ -340,7 +350,9 @@ def main():
         "config": {"workload": f"{w.name}-shaped {'x'.join(map(str, dims))}, {nnz} nnz, Zipf alpha {list(w.alpha)}, "
                                f"seed {w.seed}",
                    "R": R, "modes": list(range(N)), "tile_nnz": T,
-                   "parallelism": f"nnz-sharded x{world}, factors replicated, NCCL all-reduce per mode" if world > 1
+                   "parallelism": (f"nnz-sharded x{world}, factors replicated, "
+                                   + ("combine fused into the MTTKRP epilogue (NVLS multicast)" if mc is not None
+                                      else "NCCL all-reduce per mode")) if world > 1
                    else "1 GPU",
                    "l2": "inputs larger than L2: F-COO stream %.2f GB per mode vs 126 MB L2; no explicit flush"
                          % (bytes_modes[0] / 1e9)},

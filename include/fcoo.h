@@ -88,6 +88,7 @@ typedef struct {
 
 typedef struct fcoo_s* fcoo_t;
 typedef struct fcoo_comm_s* fcoo_comm_t;
+typedef struct fcoo_mc_s* fcoo_mc_t;
 
 /*
  * fcoo_build — F-COO format for (op, mode) (§IV-B, Fig. 2; Table II).
@@ -190,6 +191,30 @@ fcoo_status fcoo_comm_init(int rank, int nranks, const void* uid128, fcoo_comm_t
 fcoo_status fcoo_comm_destroy(fcoo_comm_t comm);
 /* In-place sum all-reduce of `count` fp32 values on `stream` (NCCL over NVLink/NVSwitch). */
 fcoo_status fcoo_allreduce_sum(fcoo_comm_t comm, float* buf, size_t count, void* stream);
+
+/* ---- collective fused into the SpMTTKRP epilogue (P:L369 multi-GPU) ----
+ * fcoo_mc_alloc — COLLECTIVE over `comm` (every rank calls it with the same `bytes`): each rank
+ * allocates `bytes` (rounded up to the multicast granularity) of its own device memory and binds
+ * it to one NVLink-SHARP multicast object shared by all ranks (created on rank 0, exported as a
+ * fabric handle and broadcast over the comm's NCCL communicator).  A 1-rank comm gives a
+ * one-device multicast object.  Errors: ARG (NULL/zero, comm without NCCL, device without
+ * multicast support), OOM, CUDA, NCCL.  Synchronises the host (setup, not the timed path).
+ * fcoo_mc_ptr — this rank's local (unicast) device view of the buffer and its requested size.
+ * fcoo_mc_free — unmap and release (synchronises the device; collective only in the sense that
+ *   no rank may still be writing through the multicast range). */
+fcoo_status fcoo_mc_alloc(fcoo_comm_t comm, size_t bytes, fcoo_mc_t* out);
+fcoo_status fcoo_mc_ptr(fcoo_mc_t mc, void** local, size_t* bytes);
+fcoo_status fcoo_mc_free(fcoo_mc_t mc);
+/* fcoo_mttkrp_mc — SpMTTKRP (as fcoo_mttkrp) on a sharded handle whose combine across ranks is
+ * fused into the kernel's epilogue: segments owned by one tile are written with multimem.st
+ * (every rank's copy), segments shared with neighbouring tiles — the only rows partial on more
+ * than one rank — with multimem.red.add, reduced in the NVSwitch.  No separate all-reduce: each
+ * rank's copy holds the full I_n x R output (row-major fp32, via fcoo_mc_ptr) when the call's
+ * work completes on `stream`.  Sequence on `stream`: zero the local copy, comm barrier (no rank
+ * writes into a copy before it is zeroed), kernel, comm barrier (every rank's writes landed).
+ * Requires the staged float4 engine: order >= 3, R % 4 == 0, 16 <= R <= 128, 16-byte aligned factors;
+ * buffer >= I_n*R*4 bytes; every rank calls it (collective).  Errors: ARG, RANK, SHAPE, CUDA, NCCL. */
+fcoo_status fcoo_mttkrp_mc(fcoo_t f, const float* const* factors, int R, fcoo_mc_t out, void* stream);
 
 /* fcoo_set_shard — restrict the handle to the tiles of shard `shard` of `nshards`: the
  * tile-aligned nnz range [floor(shard*ntiles/nshards), floor((shard+1)*ntiles/nshards)).

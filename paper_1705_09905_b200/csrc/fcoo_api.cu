@@ -108,6 +108,13 @@ fcoo_status fcoo_mttkrp(fcoo_t f, const float* const* factors, int R, float* out
   return fcoo::run_mttkrp(f, factors, R, out, (cudaStream_t)stream);
 }
 
+fcoo_status fcoo_mttkrp_mc(fcoo_t f, const float* const* factors, int R, fcoo_mc_t out, void* stream) {
+  if (!f || !factors || !out) return fcoo::fail(FCOO_ERR_ARG, "NULL handle/factors/out");
+  if (f->op != FCOO_OP_MTTKRP) return fcoo::fail(FCOO_ERR_SHAPE, "handle was built for SpTTM");
+  if (R < 1 || R > 256) return fcoo::fail(FCOO_ERR_RANK, "R=%d outside [1,256]", R);
+  return fcoo::run_mttkrp_mc(f, factors, R, out, (cudaStream_t)stream);
+}
+
 fcoo_status fcoo_ttm(fcoo_t f, const float* U, int R, float* out, void* stream) {
   if (!f || !U || !out) return fcoo::fail(FCOO_ERR_ARG, "NULL handle/U/out");
   if (f->op != FCOO_OP_TTM) return fcoo::fail(FCOO_ERR_SHAPE, "handle was built for SpMTTKRP");

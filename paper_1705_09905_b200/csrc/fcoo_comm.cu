@@ -2,6 +2,7 @@
 // path is a per-mode sum all-reduce of the partial MTTKRP output over NVLink/NVSwitch (NCCL picks
 // NVLS in-switch reduction where available).  One process per GPU; the 128-byte NCCL unique id
 // is broadcast by the caller (torch.distributed in the Python binding).
+#include <cuda.h>  // driver API types only; entry points come from cudaGetDriverEntryPoint
 #include <nccl.h>
 #include <string.h>
 
@@ -10,6 +11,20 @@
 struct fcoo_comm_s {
   ncclComm_t comm = nullptr;
   int rank = 0, nranks = 1;
+  int device = 0;
+  int* scratch = nullptr;  // one device int: the payload of the stream-ordered barrier
+};
+
+// An output buffer bound to an NVLink SHARP (NVLS) multicast object: every rank of the comm owns
+// `bytes` of its own HBM (`uc`, its unicast view) and all ranks share one multicast address range
+// (`mc`): a multimem.st there writes every rank's copy, a multimem.red.add is reduced in the
+// NVSwitch and lands in every copy.  SURVEY §8(f)-2.
+struct fcoo_mc_s {
+  fcoo_comm_t comm = nullptr;
+  size_t bytes = 0, size = 0;  // requested, and rounded to the multicast granularity
+  CUmemGenericAllocationHandle mem = 0, mcobj = 0;
+  CUdeviceptr uc = 0, mc = 0;
+  bool bound = false, uc_mapped = false, mc_mapped = false;
 };
 
 namespace fcoo {
@@ -26,6 +41,16 @@ fcoo_status comm_allreduce_f64(fcoo_comm_t c, double* buf, size_t count, cudaStr
   if (!c || !c->comm) return FCOO_OK;
   ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, s);
   if (r != ncclSuccess) return fail(FCOO_ERR_NCCL, "ncclAllReduce(f64): %s", ncclGetErrorString(r));
+  count_launch();
+  return FCOO_OK;
+}
+
+// Stream-ordered barrier over the comm: a one-element all-reduce completes on a rank only after
+// every rank has reached it (and, by stream order, finished the work enqueued before it).
+fcoo_status comm_barrier(fcoo_comm_t c, cudaStream_t s) {
+  if (!c || !c->comm) return FCOO_OK;
+  ncclResult_t r = ncclAllReduce(c->scratch, c->scratch, 1, ncclInt, ncclSum, c->comm, s);
+  if (r != ncclSuccess) return fail(FCOO_ERR_NCCL, "barrier: %s", ncclGetErrorString(r));
   count_launch();
   return FCOO_OK;
 }
@@ -57,10 +82,16 @@ fcoo_status fcoo_comm_init(int rank, int nranks, const void* uid128, fcoo_comm_t
   // a 1-rank communicator is a real NCCL communicator too (the handles never attach it: sharding
   // into one shard drops the comm), so the NCCL path can be exercised on a single GPU
   {
+    cudaGetDevice(&c->device);
+    if (cudaMalloc(&c->scratch, sizeof(int)) != cudaSuccess || cudaMemset(c->scratch, 0, sizeof(int)) != cudaSuccess) {
+      delete c;
+      return fcoo::fail(FCOO_ERR_OOM, "comm scratch");
+    }
     ncclUniqueId id;
     memcpy(&id, uid128, sizeof(id));
     ncclResult_t r = ncclCommInitRank(&c->comm, nranks, id, rank);
     if (r != ncclSuccess) {
+      cudaFree(c->scratch);
       delete c;
       return fcoo::fail(FCOO_ERR_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r));
     }
@@ -72,6 +103,7 @@ fcoo_status fcoo_comm_init(int rank, int nranks, const void* uid128, fcoo_comm_t
 fcoo_status fcoo_comm_destroy(fcoo_comm_t c) {
   if (!c) return FCOO_OK;
   if (c->comm) ncclCommDestroy(c->comm);
+  if (c->scratch) cudaFree(c->scratch);
   delete c;
   return FCOO_OK;
 }
@@ -82,3 +114,236 @@ fcoo_status fcoo_allreduce_sum(fcoo_comm_t c, float* buf, size_t count, void* st
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------------------------
+// NVLS multicast output buffers
+namespace fcoo {
+namespace {
+
+struct Drv {
+  decltype(&cuMulticastCreate) mcCreate = nullptr;
+  decltype(&cuMulticastAddDevice) mcAddDevice = nullptr;
+  decltype(&cuMulticastBindMem) mcBindMem = nullptr;
+  decltype(&cuMulticastUnbind) mcUnbind = nullptr;
+  decltype(&cuMulticastGetGranularity) mcGranularity = nullptr;
+  decltype(&cuMemCreate) memCreate = nullptr;
+  decltype(&cuMemRelease) memRelease = nullptr;
+  decltype(&cuMemAddressReserve) addrReserve = nullptr;
+  decltype(&cuMemAddressFree) addrFree = nullptr;
+  decltype(&cuMemMap) memMap = nullptr;
+  decltype(&cuMemUnmap) memUnmap = nullptr;
+  decltype(&cuMemSetAccess) setAccess = nullptr;
+  decltype(&cuMemGetAllocationGranularity) allocGranularity = nullptr;
+  decltype(&cuMemExportToShareableHandle) exportHandle = nullptr;
+  decltype(&cuMemImportFromShareableHandle) importHandle = nullptr;
+  decltype(&cuDeviceGet) deviceGet = nullptr;
+  decltype(&cuDeviceGetAttribute) deviceAttr = nullptr;
+  bool ok = false;
+};
+
+const Drv& drv() {
+  static Drv d = [] {
+    Drv x;
+    bool ok = true;
+    auto get = [&](const char* name, void** fn) {
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint(name, fn, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess ||
+          !*fn)
+        ok = false;
+    };
+    get("cuMulticastCreate", (void**)&x.mcCreate);
+    get("cuMulticastAddDevice", (void**)&x.mcAddDevice);
+    get("cuMulticastBindMem", (void**)&x.mcBindMem);
+    get("cuMulticastUnbind", (void**)&x.mcUnbind);
+    get("cuMulticastGetGranularity", (void**)&x.mcGranularity);
+    get("cuMemCreate", (void**)&x.memCreate);
+    get("cuMemRelease", (void**)&x.memRelease);
+    get("cuMemAddressReserve", (void**)&x.addrReserve);
+    get("cuMemAddressFree", (void**)&x.addrFree);
+    get("cuMemMap", (void**)&x.memMap);
+    get("cuMemUnmap", (void**)&x.memUnmap);
+    get("cuMemSetAccess", (void**)&x.setAccess);
+    get("cuMemGetAllocationGranularity", (void**)&x.allocGranularity);
+    get("cuMemExportToShareableHandle", (void**)&x.exportHandle);
+    get("cuMemImportFromShareableHandle", (void**)&x.importHandle);
+    get("cuDeviceGet", (void**)&x.deviceGet);
+    get("cuDeviceGetAttribute", (void**)&x.deviceAttr);
+    x.ok = ok;
+    return x;
+  }();
+  return d;
+}
+
+void mc_release(fcoo_mc_s* m) {
+  const Drv& d = drv();
+  if (!d.ok || !m) return;
+  if (m->mc_mapped) d.memUnmap(m->mc, m->size);
+  if (m->mc) d.addrFree(m->mc, m->size);
+  if (m->uc_mapped) d.memUnmap(m->uc, m->size);
+  if (m->uc) d.addrFree(m->uc, m->size);
+  if (m->bound) {
+    CUdevice dev;
+    if (d.deviceGet(&dev, m->comm->device) == CUDA_SUCCESS) d.mcUnbind(m->mcobj, dev, 0, m->size);
+  }
+  if (m->mem) d.memRelease(m->mem);
+  if (m->mcobj) d.memRelease(m->mcobj);
+}
+
+// Host-level collective step: every rank's enqueued work done, then a barrier, then wait for it.
+fcoo_status host_barrier(fcoo_comm_t c) {
+  cudaStream_t s = nullptr;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return fail(FCOO_ERR_CUDA, "barrier stream");
+  fcoo_status st = comm_barrier(c, s);
+  cudaError_t e = cudaStreamSynchronize(s);
+  cudaStreamDestroy(s);
+  if (st) return st;
+  if (e != cudaSuccess) return fail(FCOO_ERR_CUDA, "barrier: %s", cudaGetErrorString(e));
+  return FCOO_OK;
+}
+
+// rank `root`'s n bytes to every rank (ncclBroadcast through a device staging buffer)
+fcoo_status bcast_bytes(fcoo_comm_t c, void* host, size_t n, int root) {
+  if (c->nranks == 1) return FCOO_OK;
+  void* dbuf = nullptr;
+  cudaStream_t s = nullptr;
+  if (cudaMalloc(&dbuf, n) != cudaSuccess) return fail(FCOO_ERR_OOM, "bcast staging");
+  fcoo_status st = FCOO_OK;
+  if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) st = fail(FCOO_ERR_CUDA, "bcast stream");
+  if (!st && cudaMemcpyAsync(dbuf, host, n, cudaMemcpyHostToDevice, s) != cudaSuccess) st = fail(FCOO_ERR_CUDA, "bcast h2d");
+  if (!st) {
+    ncclResult_t r = ncclBroadcast(dbuf, dbuf, n, ncclChar, root, c->comm, s);
+    if (r != ncclSuccess) st = fail(FCOO_ERR_NCCL, "ncclBroadcast: %s", ncclGetErrorString(r));
+  }
+  if (!st && cudaMemcpyAsync(host, dbuf, n, cudaMemcpyDeviceToHost, s) != cudaSuccess) st = fail(FCOO_ERR_CUDA, "bcast d2h");
+  if (!st && cudaStreamSynchronize(s) != cudaSuccess) st = fail(FCOO_ERR_CUDA, "bcast sync");
+  if (s) cudaStreamDestroy(s);
+  cudaFree(dbuf);
+  return st;
+}
+
+}  // namespace
+}  // namespace fcoo
+
+extern "C" {
+
+fcoo_status fcoo_mc_alloc(fcoo_comm_t c, size_t bytes, fcoo_mc_t* out) {
+  using namespace fcoo;
+  if (!c || !out || bytes == 0) return fail(FCOO_ERR_ARG, "fcoo_mc_alloc: NULL comm/out or zero bytes");
+  if (!c->comm) return fail(FCOO_ERR_ARG, "fcoo_mc_alloc: comm has no NCCL communicator");
+  const Drv& d = drv();
+  if (!d.ok) return fail(FCOO_ERR_CUDA, "fcoo_mc_alloc: driver entry points unavailable");
+  CUdevice dev;
+  if (d.deviceGet(&dev, c->device) != CUDA_SUCCESS) return fail(FCOO_ERR_CUDA, "cuDeviceGet");
+  int mcs = 0;
+  d.deviceAttr(&mcs, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev);
+  if (!mcs) return fail(FCOO_ERR_ARG, "fcoo_mc_alloc: device does not support NVLS multicast");
+  const bool shared = c->nranks > 1;
+  CUmulticastObjectProp mp;
+  memset(&mp, 0, sizeof(mp));
+  mp.numDevices = (unsigned)c->nranks;
+  mp.handleTypes = shared ? CU_MEM_HANDLE_TYPE_FABRIC : CU_MEM_HANDLE_TYPE_NONE;
+  mp.size = bytes;
+  size_t g_mc = 0, g_mem = 0;
+  if (d.mcGranularity(&g_mc, &mp, CU_MULTICAST_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS)
+    return fail(FCOO_ERR_CUDA, "cuMulticastGetGranularity");
+  CUmemAllocationProp ap;
+  memset(&ap, 0, sizeof(ap));
+  ap.type = CU_MEM_ALLOCATION_TYPE_PINNED;
+  ap.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  ap.location.id = c->device;
+  ap.requestedHandleTypes = CU_MEM_HANDLE_TYPE_NONE;
+  if (d.allocGranularity(&g_mem, &ap, CU_MEM_ALLOC_GRANULARITY_RECOMMENDED) != CUDA_SUCCESS)
+    return fail(FCOO_ERR_CUDA, "cuMemGetAllocationGranularity");
+  const size_t g = g_mc > g_mem ? g_mc : g_mem;
+  fcoo_mc_s* m = new fcoo_mc_s();
+  m->comm = c;
+  m->bytes = bytes;
+  m->size = mp.size = (bytes + g - 1) / g * g;
+  auto bail = [&](fcoo_status st) {
+    mc_release(m);
+    delete m;
+    return st;
+  };
+  // rank 0 creates the multicast object and shares it as a fabric handle (bytes over NCCL)
+  CUmemFabricHandle fh;
+  memset(&fh, 0, sizeof(fh));
+  int ok0 = 1;
+  CUresult cr = CUDA_SUCCESS;
+  if (c->rank == 0) {
+    cr = d.mcCreate(&m->mcobj, &mp);
+    if (cr != CUDA_SUCCESS && !shared) {  // some drivers want a shareable handle type even for one device
+      mp.handleTypes = CU_MEM_HANDLE_TYPE_FABRIC;
+      cr = d.mcCreate(&m->mcobj, &mp);
+    }
+    ok0 = cr == CUDA_SUCCESS;
+    if (ok0 && shared) {
+      cr = d.exportHandle(&fh, m->mcobj, CU_MEM_HANDLE_TYPE_FABRIC, 0);
+      ok0 = cr == CUDA_SUCCESS;
+    }
+  }
+  if (shared) {
+    struct { CUmemFabricHandle h; int ok; } msg;
+    msg.h = fh;
+    msg.ok = ok0;
+    fcoo_status st = bcast_bytes(c, &msg, sizeof(msg), 0);
+    if (st) return bail(st);
+    if (!msg.ok) return bail(fail(FCOO_ERR_CUDA, "cuMulticastCreate/export failed on rank 0 (CUresult %d)", (int)cr));
+    if (c->rank != 0 && d.importHandle(&m->mcobj, &msg.h, CU_MEM_HANDLE_TYPE_FABRIC) != CUDA_SUCCESS)
+      return bail(fail(FCOO_ERR_CUDA, "cuMemImportFromShareableHandle (multicast)"));
+  } else if (!ok0) {
+    return bail(fail(FCOO_ERR_CUDA, "cuMulticastCreate: CUresult %d", (int)cr));
+  }
+  if ((cr = d.mcAddDevice(m->mcobj, dev)) != CUDA_SUCCESS)
+    return bail(fail(FCOO_ERR_CUDA, "cuMulticastAddDevice: CUresult %d", (int)cr));
+  // every device must be added before any rank binds memory
+  fcoo_status st = host_barrier(c);
+  if (st) return bail(st);
+  if (d.memCreate(&m->mem, m->size, &ap, 0) != CUDA_SUCCESS) return bail(fail(FCOO_ERR_OOM, "cuMemCreate"));
+  if ((cr = d.mcBindMem(m->mcobj, 0, m->mem, 0, m->size, 0)) != CUDA_SUCCESS)
+    return bail(fail(FCOO_ERR_CUDA, "cuMulticastBindMem: CUresult %d", (int)cr));
+  m->bound = true;
+  CUmemAccessDesc acc;
+  memset(&acc, 0, sizeof(acc));
+  acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
+  acc.location.id = c->device;
+  acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
+  if (d.addrReserve(&m->uc, m->size, g, 0, 0) != CUDA_SUCCESS) return bail(fail(FCOO_ERR_OOM, "VA reserve (unicast)"));
+  if (d.memMap(m->uc, m->size, 0, m->mem, 0) != CUDA_SUCCESS) return bail(fail(FCOO_ERR_CUDA, "cuMemMap (unicast)"));
+  m->uc_mapped = true;
+  if (d.setAccess(m->uc, m->size, &acc, 1) != CUDA_SUCCESS) return bail(fail(FCOO_ERR_CUDA, "cuMemSetAccess (unicast)"));
+  if (d.addrReserve(&m->mc, m->size, g, 0, 0) != CUDA_SUCCESS) return bail(fail(FCOO_ERR_OOM, "VA reserve (multicast)"));
+  if (d.memMap(m->mc, m->size, 0, m->mcobj, 0) != CUDA_SUCCESS) return bail(fail(FCOO_ERR_CUDA, "cuMemMap (multicast)"));
+  m->mc_mapped = true;
+  if (d.setAccess(m->mc, m->size, &acc, 1) != CUDA_SUCCESS) return bail(fail(FCOO_ERR_CUDA, "cuMemSetAccess (multicast)"));
+  if (cudaMemset((void*)m->uc, 0, m->size) != cudaSuccess) return bail(fail(FCOO_ERR_CUDA, "zero multicast buffer"));
+  st = host_barrier(c);  // every rank bound and mapped before anyone writes through mc
+  if (st) return bail(st);
+  *out = m;
+  return FCOO_OK;
+}
+
+fcoo_status fcoo_mc_ptr(fcoo_mc_t m, void** local, size_t* bytes) {
+  if (!m || !local) return fcoo::fail(FCOO_ERR_ARG, "fcoo_mc_ptr: NULL");
+  *local = (void*)m->uc;
+  if (bytes) *bytes = m->bytes;
+  return FCOO_OK;
+}
+
+fcoo_status fcoo_mc_free(fcoo_mc_t m) {
+  if (!m) return FCOO_OK;
+  cudaDeviceSynchronize();
+  fcoo::mc_release(m);
+  delete m;
+  return FCOO_OK;
+}
+
+}  // extern "C"
+
+namespace fcoo {
+void mc_views(fcoo_mc_t m, float** uc, float** mc, size_t* bytes, fcoo_comm_t* comm) {
+  *uc = reinterpret_cast<float*>(m->uc);
+  *mc = reinterpret_cast<float*>(m->mc);
+  *bytes = m->bytes;
+  *comm = m->comm;
+}
+}  // namespace fcoo

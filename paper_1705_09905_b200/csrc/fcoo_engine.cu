@@ -1,6 +1,8 @@
 // fcoo_engine.cu — host side of the segmented-reduction engine (see fcoo_engine_kernels.cuh):
 // output preparation, kernel dispatch by (product-mode count, rank, accumulator type), and the
 // SpMTTKRP / SpTTM entry points behind the C ABI.
+#include <stdlib.h>
+
 #include "fcoo_engine.cuh"
 
 namespace fcoo {
@@ -37,6 +39,12 @@ cudaError_t launch_engine(const EngineParams& P, int NP, bool vec_ok, cudaStream
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
+// FCOO_ENGINE as launch_one reads it (2 = staged, the default)
+int engine_env() {
+  const char* e = getenv("FCOO_ENGINE");
+  return e ? atoi(e) : 2;
+}
+
 template <class ACC>
 fcoo_status prepare_output(fcoo_s* f, int R, ACC* out, int64_t rows, bool all_rows_are_segments, cudaStream_t s) {
   bool whole = (f->tile_begin == 0 && f->tile_end == f->ntiles);
@@ -58,8 +66,9 @@ fcoo_status prepare_output(fcoo_s* f, int R, ACC* out, int64_t rows, bool all_ro
 
 template <class ACC>
 fcoo_status mttkrp_t(fcoo_s* f, const float* const* factors, int R, ACC* out, cudaStream_t s,
-                     const int* gate = nullptr, int gate_on = 0) {
+                     const int* gate = nullptr, int gate_on = 0, float* out_mc = nullptr) {
   EngineParams P{};
+  P.out_mc = out_mc;
   P.gate = gate;
   P.gate_on = gate_on;
   bool vec_ok = (R % 4 == 0) && R <= 128 && aligned16(out);
@@ -74,9 +83,14 @@ fcoo_status mttkrp_t(fcoo_s* f, const float* const* factors, int R, ACC* out, cu
   P.seg_coord = f->dense_rows ? nullptr : f->seg_coord;
   P.nnz = f->nnz; P.ntiles = f->ntiles; P.tile_begin = f->tile_begin; P.tile_end = f->tile_end;
   P.T = (int)f->T; P.R = R; P.out = out;
-  // all rows are segments (dense_rows): only tile-crossing rows need zeroing
-  fcoo_status st = prepare_output<ACC>(f, R, out, f->dims[f->mode], f->dense_rows != 0, s);
-  if (st) return st;
+  // all rows are segments (dense_rows): only tile-crossing rows need zeroing; the fused-combine
+  // caller zeroes its (multicast-bound) buffer itself
+  if (!out_mc) {
+    fcoo_status st = prepare_output<ACC>(f, R, out, f->dims[f->mode], f->dense_rows != 0, s);
+    if (st) return st;
+  } else if (!vec_ok || R < 16 || engine_env() != 2 || f->n_prod < 2) {
+    return fail(FCOO_ERR_ARG, "fused combine needs the staged float4 engine (order >= 3, R %% 4 == 0, 16 <= R <= 128, aligned)");
+  }
   cudaError_t e = launch_engine<ACC>(P, f->n_prod, vec_ok, s);
   if (e != cudaSuccess) return fail(FCOO_ERR_CUDA, "mttkrp launch: %s", cudaGetErrorString(e));
   return FCOO_OK;
@@ -88,6 +102,24 @@ fcoo_status run_mttkrp(fcoo_s* f, const float* const* factors, int R, float* out
   if (st) return st;
   if (f->comm) return comm_allreduce(f->comm, out, (size_t)f->dims[f->mode] * R, s);
   return FCOO_OK;
+}
+
+// SpMTTKRP with the cross-rank combine fused into the epilogue: zero the local
+// copy, barrier, kernel writing through the multicast address, barrier.
+fcoo_status run_mttkrp_mc(fcoo_s* f, const float* const* factors, int R, fcoo_mc_t mc, cudaStream_t s) {
+  float *uc = nullptr, *mcp = nullptr;
+  size_t bytes = 0;
+  fcoo_comm_t comm = nullptr;
+  mc_views(mc, &uc, &mcp, &bytes, &comm);
+  const size_t need = sizeof(float) * (size_t)f->dims[f->mode] * (size_t)R;
+  if (bytes < need) return fail(FCOO_ERR_ARG, "multicast buffer holds %zu bytes, output needs %zu", bytes, need);
+  if (f->comm && f->comm != comm) return fail(FCOO_ERR_ARG, "handle sharded over a different comm");
+  FCOO_CUDA_TRY(cudaMemsetAsync(uc, 0, need, s));
+  fcoo_status st = comm_barrier(comm, s);
+  if (st) return st;
+  st = mttkrp_t<float>(f, factors, R, uc, s, nullptr, 0, mcp);
+  if (st) return st;
+  return comm_barrier(comm, s);
 }
 
 // fp64-accumulating MTTKRP (CP-ALS fit mode); sharded handles return the LOCAL partial.

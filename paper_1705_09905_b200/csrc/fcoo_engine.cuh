@@ -17,6 +17,9 @@ struct EngineParams {
   int64_t nnz, ntiles, tile_begin, tile_end;
   int T, R;
   void* out;  // float* (fp32 accumulation) or double* (fp64 accumulation)
+  // fused combine (fcoo_mttkrp_mc): multicast address of the output; segment
+  // flushes go to every rank's copy with multimem.st / multimem.red.add (fp32 float4 path only)
+  float* out_mc;
   // device-side gate (CP-ALS fit mode): when non-null the launch does its work only if
   // (*gate != 0) == gate_on, so the fp32/fp64 choice needs no host synchronisation
   const int* gate;

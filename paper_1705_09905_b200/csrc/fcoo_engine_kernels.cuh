@@ -88,6 +88,16 @@ __device__ __forceinline__ void flush_if(bool st, bool rd, float* p, float v) {
       "r"((int)rd), "l"(p), "f"(v)
       : "memory");
 }
+// The same flushes through an NVLS multicast address (fused combine across ranks): a store
+// reaches every rank's copy, a red.add is reduced in the NVSwitch and lands in every copy.
+__device__ __forceinline__ void mc_flush_if(bool st, bool rd, float* p, float4 v) {
+  asm volatile(
+      "{ .reg .pred ps, pr; setp.ne.b32 ps, %0, 0; setp.ne.b32 pr, %1, 0;\n"
+      "  @ps multimem.st.relaxed.sys.global.v4.f32 [%2], {%3,%4,%5,%6};\n"
+      "  @pr multimem.red.relaxed.sys.global.add.v4.f32 [%2], {%3,%4,%5,%6}; }" ::"r"((int)st),
+      "r"((int)rd), "l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+      : "memory");
+}
 __device__ __forceinline__ float4 zero_if(bool z, float4 a) {
   return z ? make_float4(0.f, 0.f, 0.f, 0.f) : a;
 }
@@ -671,11 +681,18 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
   AT acc[CPL];
 #pragma unroll
   for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
+  float* const mcp = NP >= 2 ? P.out_mc : nullptr;  // fused combine (float4 fp32, order >= 3; host checks)
   auto flush = [&](bool store) {
     ACC* o = outp + (size_t)row * (uint32_t)R;
 #pragma unroll
     for (int c = 0; c < CPL; ++c)
       if (cok[c]) {
+        if constexpr (std::is_same<AT, float4>::value && NP >= 2) {  // MTTKRP of order >= 3
+          if (mcp) {
+            mc_flush_if(store, !store, mcp + (size_t)row * (uint32_t)R + col[c], acc[c]);
+            continue;
+          }
+        }
         if (store) A::store(o + col[c], acc[c]);
         else A::red(o + col[c], acc[c]);
       }
@@ -749,7 +766,14 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
           ACC* o = outp + (size_t)row * (uint32_t)R;
 #pragma unroll
           for (int c = 0; c < CPL; ++c) {
-            if (cok[c]) flush_if(cl && own, cl && !own, o + col[c], acc[c]);
+            if (cok[c]) {
+              if constexpr (std::is_same<AT, float4>::value && NP >= 2) {  // MTTKRP of order >= 3
+                if (mcp) mc_flush_if(cl && own, cl && !own, mcp + (size_t)row * (uint32_t)R + col[c], acc[c]);
+                else flush_if(cl && own, cl && !own, o + col[c], acc[c]);
+              } else {
+                flush_if(cl && own, cl && !own, o + col[c], acc[c]);
+              }
+            }
             acc[c] = zero_if(hd, acc[c]);
           }
           own = own || hd;
@@ -792,6 +816,7 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
   }
   const bool right_open = (t + 1 < P.ntiles) && !((P.sf[(t + 1) >> 5] >> ((t + 1) & 31)) & 1u);
   flush(own && !right_open);
+  if (mcp) __threadfence_system();  // multicast writes visible system-wide before the kernel ends
 }
 
 // Engine variant (FCOO_ENGINE env var, read once): 0 = plain, 1 = factored outer mode,

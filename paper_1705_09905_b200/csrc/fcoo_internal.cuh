@@ -81,6 +81,9 @@ fcoo_status run_mttkrp_f64(fcoo_s* f, const float* const* factors, int R, double
 fcoo_status comm_allreduce(fcoo_comm_t comm, float* buf, size_t count, cudaStream_t s);
 fcoo_status comm_allreduce_f64(fcoo_comm_t comm, double* buf, size_t count, cudaStream_t s);
 void comm_rank_size(fcoo_comm_t comm, int* rank, int* nranks);
+fcoo_status comm_barrier(fcoo_comm_t comm, cudaStream_t s);
+void mc_views(fcoo_mc_t m, float** uc, float** mc, size_t* bytes, fcoo_comm_t* comm);
+fcoo_status run_mttkrp_mc(fcoo_s* f, const float* const* factors, int R, fcoo_mc_t out, cudaStream_t s);
 fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s);
 fcoo_status run_ttmc(fcoo_s* f, const float* const* factors, const int* ranks, float* out, cudaStream_t s);
 }  // namespace fcoo

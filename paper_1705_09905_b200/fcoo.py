@@ -71,6 +71,7 @@ class _CpOpts(ctypes.Structure):
 # The exported symbols (every one declared in include/fcoo.h).
 SYMBOLS = ["fcoo_build", "fcoo_build_sharded", "fcoo_mttkrp", "fcoo_ttm", "fcoo_ttmc", "fcoo_info", "fcoo_export", "fcoo_destroy",
            "fcoo_comm_unique_id", "fcoo_comm_init", "fcoo_comm_destroy", "fcoo_allreduce_sum", "fcoo_set_shard",
+           "fcoo_mc_alloc", "fcoo_mc_ptr", "fcoo_mc_free", "fcoo_mttkrp_mc",
            "fcoo_shard_range", "cp_als", "fcoo_tns_read", "fcoo_tns_info", "fcoo_tns_copy", "fcoo_tns_destroy",
            "fcoo_tns_write", "fcoo_status_str", "fcoo_last_error", "fcoo_launch_count"]
 
@@ -101,6 +102,10 @@ def load_library():
     L.fcoo_comm_destroy.argtypes = [vp]
     L.fcoo_allreduce_sum.argtypes = [vp, vp, ctypes.c_size_t, vp]
     L.fcoo_set_shard.argtypes = [vp, ci, ci, vp]
+    L.fcoo_mc_alloc.argtypes = [vp, ctypes.c_size_t, ctypes.POINTER(vp)]
+    L.fcoo_mc_ptr.argtypes = [vp, ctypes.POINTER(vp), ctypes.POINTER(ctypes.c_size_t)]
+    L.fcoo_mc_free.argtypes = [vp]
+    L.fcoo_mttkrp_mc.argtypes = [vp, ctypes.POINTER(vp), ci, vp, vp]
     L.fcoo_shard_range.argtypes = [i64, ci, ci, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.cp_als.argtypes = [ctypes.POINTER(_Coo), ctypes.POINTER(_CpOpts), ctypes.POINTER(vp), vp,
                          ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ci), ctypes.POINTER(_Allocator), vp]
@@ -419,6 +424,53 @@ def fcoo_shard_range(ntiles: int, shard: int, nshards: int):
 def fcoo_set_shard(f: Fcoo, shard: int, nshards: int, comm: Comm | None = None):
     _check(load_library().fcoo_set_shard(f.h, shard, nshards, comm.h if comm else None), "fcoo_set_shard")
     f.info = f._info()
+
+
+class McBuffer:
+    """Output buffer bound to an NVLS multicast object across the ranks of a Comm (fcoo_mc_alloc).
+    `local` is this rank's copy as a CUDA fp32 tensor of `numel` elements (a view, not owning)."""
+
+    def __init__(self, comm: "Comm", numel: int):
+        L = load_library()
+        out = ctypes.c_void_p()
+        _check(L.fcoo_mc_alloc(comm.h, ctypes.c_size_t(4 * numel), ctypes.byref(out)), "fcoo_mc_alloc")
+        self.h = out
+        p = ctypes.c_void_p()
+        n = ctypes.c_size_t()
+        _check(L.fcoo_mc_ptr(self.h, ctypes.byref(p), ctypes.byref(n)), "fcoo_mc_ptr")
+        self.numel = numel
+        self.ptr = p.value
+        self.local = _tensor_view(p.value, numel)
+
+    def free(self):
+        if self.h:
+            load_library().fcoo_mc_free(self.h)
+            self.h = ctypes.c_void_p(None)
+            self.local = None
+
+
+def _tensor_view(ptr: int, numel: int) -> torch.Tensor:
+    """Non-owning CUDA fp32 tensor over device memory the library owns (via __cuda_array_interface__)."""
+    class _A:
+        __cuda_array_interface__ = {"shape": (numel,), "typestr": "<f4", "data": (ptr, False), "version": 3,
+                                    "strides": None}
+    return torch.as_tensor(_A(), device="cuda")
+
+
+def fcoo_mttkrp_mc(f: Fcoo, factors, R: int, out: McBuffer, stream=None) -> torch.Tensor:
+    """SpMTTKRP with the cross-rank combine fused into the epilogue; returns out.local[:I_n*R] as (I_n, R)."""
+    L = load_library()
+    ptrs = []
+    for m, U in enumerate(factors):
+        if U is None:
+            ptrs.append(None)
+            continue
+        _require_cuda(U, torch.float32, f"factors[{m}]")
+        ptrs.append(U.data_ptr())
+    arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
+    _check(L.fcoo_mttkrp_mc(f.h, arr, R, out.h, ctypes.c_void_p(_stream_ptr(stream))), "fcoo_mttkrp_mc")
+    I = f.info.dims[f.info.mode]
+    return out.local[: I * R].view(I, R)
 
 
 def cp_als(coo: Coo, R: int, iters: int, factors, tol: float = 0.0, tile_nnz: int = 0, comm: Comm | None = None,

@@ -57,6 +57,10 @@ def test_host_checked_errors_without_gpu():
     assert L.fcoo_build_sharded(ctypes.byref(coo3), 0, ctypes.byref(opts), None, None, None,
                                 ctypes.byref(out)) == fcoo.ERR_ARG  # NULL comm
     assert L.fcoo_mttkrp(None, None, 8, None, None) == fcoo.ERR_ARG
+    mc = ctypes.c_void_p()
+    assert L.fcoo_mc_alloc(None, 1024, ctypes.byref(mc)) == fcoo.ERR_ARG
+    assert L.fcoo_mttkrp_mc(None, None, 32, None, None) == fcoo.ERR_ARG
+    assert L.fcoo_mc_free(None) == fcoo.OK
     assert L.fcoo_ttm(None, None, 8, None, None) == fcoo.ERR_ARG
     assert L.fcoo_status_str(fcoo.ERR_DUPLICATE) == b"FCOO_ERR_DUPLICATE"
     assert b"tile_nnz" in L.fcoo_last_error() or len(L.fcoo_last_error()) > 0

@@ -89,3 +89,89 @@ def test_cp_als_with_comm_matches_without(pg):
     for x, y in zip(a, b):
         assert torch.allclose(x, y, rtol=0, atol=1e-4)
     comm.destroy()
+
+
+def _mc_buffer(P, comm, numel):
+    """A multicast-bound buffer, or skip: NVLS multicast objects need the NVSwitch fabric, and a
+    box that exposes one GPU without it refuses cuMulticastCreate (tools/probe_mc.py)."""
+    try:
+        return P.McBuffer(comm, numel)
+    except P.FcooError as e:
+        if "cuMulticastCreate" in str(e):
+            pytest.skip(f"NVLS multicast unavailable on this box: {e}")
+        raise
+
+
+@pytest.mark.parametrize("R", [16, 32, 64])
+def test_fused_combine_multicast_epilogue(pg, R):
+    """fcoo_mttkrp_mc: the epilogue writes through an NVLS multicast address
+    (multimem.st for owned segments, multimem.red.add for shared ones); on a 1-rank comm the local
+    copy must equal the oracle, as fcoo_mttkrp's output does."""
+    import torch
+    import paper_1705_09905_b200 as P
+    comm = P.comm_from_process_group()
+    dims = (700, 400, 300)
+    idx, val = gen.coo(dims, 60000, (0.5, 0.5, 0.5), 45)
+    fs = gen.factors(dims, R, 6, signed=True)
+    coo = P.Coo.from_numpy(dims, idx, val)
+    ft = [torch.from_numpy(f).cuda() for f in fs]
+    buf = _mc_buffer(P, comm, max(dims) * R)
+    for mode in range(3):
+        h = P.fcoo_build_sharded(coo, mode, comm, tile_nnz=64)
+        got = P.fcoo_mttkrp_mc(h, ft, R, buf)
+        torch.cuda.synchronize()
+        M, D = oracle.mttkrp(dims, idx, val, mode, fs, nthreads=8)
+        assert_parity(got.cpu().numpy(), M, D, what=f"multicast mode={mode} R={R}")
+        ref = torch.empty((dims[mode], R), device="cuda")
+        P.fcoo_mttkrp(h, ft, R, ref)
+        torch.cuda.synchronize()
+        assert torch.allclose(got, ref, rtol=0, atol=1e-5)
+        h.destroy()
+    buf.free()
+    comm.destroy()
+
+
+@pytest.mark.parametrize("shards", [2, 3, 7])
+def test_fused_combine_shard_boundaries(pg, shards):
+    """Shards run one after another through the multicast epilogue (each call zeroes the buffer):
+    summed on the host they equal the whole, so rows cut by a shard boundary are red.add-ed and
+    rows a shard owns are stored exactly once."""
+    import torch
+    import paper_1705_09905_b200 as P
+    comm = P.comm_from_process_group()
+    dims = (150, 900, 800)
+    idx, val = gen.coo(dims, 50000, (1.0, 0.5, 0.5), 46)
+    R = 32
+    fs = gen.factors(dims, R, 7, signed=True)
+    coo = P.Coo.from_numpy(dims, idx, val)
+    ft = [torch.from_numpy(f).cuda() for f in fs]
+    buf = _mc_buffer(P, comm, max(dims) * R)
+    for mode in range(3):
+        h = P.fcoo_build(coo, mode, tile_nnz=64)
+        acc = torch.zeros((dims[mode], R), dtype=torch.float64, device="cuda")
+        for g in range(shards):
+            P.fcoo_set_shard(h, g, shards, comm)
+            acc += P.fcoo_mttkrp_mc(h, ft, R, buf).double()
+        torch.cuda.synchronize()
+        M, D = oracle.mttkrp(dims, idx, val, mode, fs, nthreads=8)
+        assert_parity(acc.cpu().numpy(), M, D, what=f"multicast shards={shards} mode={mode}")
+        h.destroy()
+    buf.free()
+    comm.destroy()
+
+
+def test_fused_combine_rejects_unsupported_rank(pg):
+    import torch
+    import paper_1705_09905_b200 as P
+    comm = P.comm_from_process_group()
+    dims = (50, 40, 30)
+    idx, val = gen.coo(dims, 1000, None, 47)
+    coo = P.Coo.from_numpy(dims, idx, val)
+    ft = [torch.from_numpy(f).cuda() for f in gen.factors(dims, 8, 1)]
+    buf = _mc_buffer(P, comm, 50 * 8)
+    h = P.fcoo_build_sharded(coo, 0, comm)
+    with pytest.raises(P.FcooError):
+        P.fcoo_mttkrp_mc(h, ft, 8, buf)  # R = 8 runs the unstaged engine: no multicast epilogue
+    h.destroy()
+    buf.free()
+    comm.destroy()
