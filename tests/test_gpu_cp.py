@@ -86,3 +86,28 @@ def test_tol_early_stop(F):
     init = gen.factors(dims, 3, 901)
     _, _, tr_g = _cp(F, dims, cells, val, 3, 200, init, tol=1e-6, T=32)
     assert len(tr_g) < 200 and tr_g[-1] > 0.99
+
+
+def test_order4_full_size_properties(F):
+    """BASELINE configs[4] on one GPU: the 4-order 150M-nonzero tensor, CP-ALS R=32 for 20
+    iterations (tol 0, the captured-graph path).  At this size the oracle cannot run the loop, so
+    the properties Alg. 1 guarantees are checked: the fit trace is non-decreasing (each step is an
+    exact least-squares solve; 1e-7 slack for fp32 MTTKRP rounding), finite and in [0, 1]; every
+    factor column has unit 2-norm (line 7 of Alg. 1, reading Q13); lambda > 0.  (The trace itself
+    is pinned to the oracle on smaller tensors above.)"""
+    import torch
+    w = gen.WORKLOADS["order4"]
+    idx, val = gen.coo(w.dims, w.nnz, w.alpha, w.seed)
+    coo = F.Coo.from_numpy(w.dims, idx, val)
+    R = 32
+    init = gen.factors(w.dims, R, 9)
+    fs = [torch.from_numpy(f).cuda() for f in init]
+    lam, trace = F.cp_als(coo, R, 20, fs)
+    torch.cuda.synchronize()
+    trace = np.asarray(trace)
+    assert trace.shape == (20,) and np.all(np.isfinite(trace)) and np.all((trace >= 0) & (trace <= 1))
+    assert np.all(np.diff(trace) >= -1e-7), trace
+    for U in fs:
+        n = torch.linalg.vector_norm(U.double(), dim=0).cpu().numpy()
+        assert np.allclose(n, 1.0, rtol=0, atol=1e-5)
+    assert bool((lam > 0).all())

@@ -120,3 +120,25 @@ def test_long_segment_accumulation(F):
         got = _run(F, dims, idx, val, 0, fs, T=2048)
         Y, D = oracle.ttmc(dims, idx, val, 0, [None, fs[1], fs[2]])
         assert_parity(got, Y, D, what=f"long segment ranks={ranks}")
+
+
+def test_nell2_full_size_sampled_rows(F):
+    """SURVEY §8(f)-3 at BASELINE configs[1]'s full size (76.9M nonzeros, every mode, R=16 and 32,
+    automatic tile as tools/ops_bench.py times it): an output row of Eq.(4) depends only on its own
+    slice's nonzeros, so the oracle computes 24 sampled rows per mode (the heaviest slices, the
+    lightest, and random ones) from those nonzeros alone; compared element by element."""
+    w = gen.WORKLOADS["nell2"]
+    idx, val = gen.coo(w.dims, w.nnz, w.alpha, w.seed)
+    rng = np.random.default_rng(5)
+    for R in (16, 32):
+        fs = gen.factors(w.dims, R, 7, signed=True)
+        for mode in range(3):
+            got = _run(F, w.dims, idx, val, mode, fs, T=0)
+            counts = np.bincount(idx[mode], minlength=w.dims[mode])
+            order = np.argsort(counts, kind="stable")
+            rows = np.unique(np.concatenate([order[-8:], order[:8], rng.choice(w.dims[mode], 8, replace=False)]))
+            sel = np.isin(idx[mode], rows)
+            sub_idx, sub_val = np.ascontiguousarray(idx[:, sel]), np.ascontiguousarray(val[sel])
+            fs_m = [None if m == mode else fs[m] for m in range(3)]
+            Y, D = oracle.ttmc(w.dims, sub_idx, sub_val, mode, fs_m)
+            assert_parity(got[rows], Y[rows], D[rows], what=f"nell2 ttmc R={R} mode={mode} sampled rows")
