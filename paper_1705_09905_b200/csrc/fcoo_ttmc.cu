@@ -352,7 +352,7 @@ bool try_staged(const TtmcParams& P, bool v16, cudaStream_t s, cudaError_t* err)
   return true;
 }
 
-// Tensor-core variant for RA, RB multiples of 16 and 8: per segment Y(i_n) = A^T B with
+// Tensor-core variant for RA in {8, 16, 32, 64} and RB a multiple of 8: per segment Y(i_n) = A^T B with
 // A(k, p) = v_k U_a(i_a(k), p) and B(k, q) = U_b(i_b(k), q), K = the segment's nonzeros, is a dense
 // contraction, so each K-chunk of 8 staged nonzeros feeds mma.sync m16n8k8 TF32 tiles.  fp32
 // accuracy comes from the 3xTF32 split (x = hi + lo, both TF32; A·B ≈ hi·hi + hi·lo + lo·hi,
@@ -361,10 +361,16 @@ bool try_staged(const TtmcParams& P, bool v16, cudaStream_t s, cudaError_t* err)
 // tensor core.  Staging (rows, values, indices via cp.async) is as in k_ttmc_staged, with row
 // strides padded by 8 words so the fragment loads are bank-conflict free.  A segment head inside a
 // chunk splits it: the sub-ranges run with the other nonzeros' values masked to 0.
+// Row stride (words) of a staged factor row: a fragment load reads rows k0 + tq (tq < 4) at 8
+// consecutive columns, so the stride must be 8 or 24 (mod 32) for the four rows to land on disjoint
+// bank octets: R = 8 needs no padding, R = 16, 32, 64 take +8.
+constexpr int mma_stride(int R) { return (R % 16 == 8) ? R : R + 8; }
+
+// RA = 8 runs as one m16 tile whose rows 8..15 are zero (never staged, never stored).
 template <int RA, int RB>
 struct MmaGeom {
-  static constexpr int MT = RA / 16, NT = RB / 8;
-  static constexpr int SA = RA + 8, SB = RB + 8;  // padded row strides (words)
+  static constexpr int MT = (RA + 15) / 16, NT = RB / 8;
+  static constexpr int SA = mma_stride(RA), SB = mma_stride(RB);  // padded row strides (words)
   static constexpr int ROWS = kNB * (SA + SB) + kNB;  // one row buffer: A rows, B rows, values
   static constexpr int WARP = 2 * ROWS;
 };
@@ -419,12 +425,13 @@ __global__ void __launch_bounds__(kStagedWarps * 32) k_ttmc_mma(const TtmcParams
       for (int j = 0; j < NT; ++j) {
         float* o0 = o + (16 * i + g) * RB + 8 * j + 2 * tq;
         float* o1 = o0 + 8 * RB;
+        constexpr bool hi_rows = RA >= 16;  // rows 16i+g+8 exist
         if (store) {
           *reinterpret_cast<float2*>(o0) = make_float2(acc[i][j][0], acc[i][j][1]);
-          *reinterpret_cast<float2*>(o1) = make_float2(acc[i][j][2], acc[i][j][3]);
+          if (hi_rows) *reinterpret_cast<float2*>(o1) = make_float2(acc[i][j][2], acc[i][j][3]);
         } else {
           atomicAdd(o0, acc[i][j][0]); atomicAdd(o0 + 1, acc[i][j][1]);
-          atomicAdd(o1, acc[i][j][2]); atomicAdd(o1 + 1, acc[i][j][3]);
+          if (hi_rows) { atomicAdd(o1, acc[i][j][2]); atomicAdd(o1 + 1, acc[i][j][3]); }
         }
       }
   };
@@ -492,9 +499,13 @@ __global__ void __launch_bounds__(kStagedWarps * 32) k_ttmc_mma(const TtmcParams
     for (int i = 0; i < MT; ++i) {
       const int m = 16 * i + g;
       split_tf32(va * sA[ka * SA + m], ah[i][0], al[i][0]);
-      split_tf32(va * sA[ka * SA + m + 8], ah[i][1], al[i][1]);
       split_tf32(vb * sA[kb * SA + m], ah[i][2], al[i][2]);
-      split_tf32(vb * sA[kb * SA + m + 8], ah[i][3], al[i][3]);
+      if constexpr (RA >= 16) {
+        split_tf32(va * sA[ka * SA + m + 8], ah[i][1], al[i][1]);
+        split_tf32(vb * sA[kb * SA + m + 8], ah[i][3], al[i][3]);
+      } else {  // rows 8..15 of the m16 tile are padding
+        ah[i][1] = al[i][1] = ah[i][3] = al[i][3] = 0u;
+      }
     }
 #pragma unroll
     for (int j = 0; j < NT; ++j) {
@@ -601,7 +612,8 @@ cudaError_t launch_staged(const TtmcParams& P, bool* done, cudaStream_t s) {
     cudaError_t e = cudaSuccess;
     if (try_mma<32, 32>(P, s, &e) || try_mma<16, 16>(P, s, &e) || try_mma<16, 32>(P, s, &e) ||
         try_mma<32, 16>(P, s, &e) || try_mma<16, 64>(P, s, &e) || try_mma<64, 16>(P, s, &e) ||
-        try_mma<16, 8>(P, s, &e) || try_mma<32, 8>(P, s, &e) || try_mma<64, 8>(P, s, &e)) {
+        try_mma<16, 8>(P, s, &e) || try_mma<32, 8>(P, s, &e) || try_mma<64, 8>(P, s, &e) ||
+        try_mma<8, 8>(P, s, &e) || try_mma<8, 16>(P, s, &e) || try_mma<8, 32>(P, s, &e)) {
       *done = true;
       return e;
     }

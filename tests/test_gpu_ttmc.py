@@ -53,7 +53,7 @@ def test_worked_case(F):
 
 
 @pytest.mark.parametrize("ranks", [(16, 16), (8, 8), (4, 4), (32, 32), (3, 5), (16, 64), (64, 16), (1, 1), (2, 16),
-                                   (8, 12), (2, 48), (32, 16)])
+                                   (8, 12), (2, 48), (32, 16), (8, 16), (8, 32), (16, 8), (64, 8)])
 def test_ranks_all_modes(F, ranks):
     dims = (300, 200, 250)
     idx, val = gen.coo(dims, 30000, (0.5, 0.5, 0.5), 111)
