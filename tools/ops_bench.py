@@ -61,7 +61,7 @@ def main():
     ap.add_argument("--ops", default="ttm,ttmc,cp")
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--oracle-s", type=float, default=4.0)
-    ap.add_argument("--ttmc-R", default="16,32")
+    ap.add_argument("--ttmc-R", default="8,16,32")
     a = ap.parse_args()
     import numpy as np
     import torch
