@@ -62,7 +62,12 @@ __device__ __forceinline__ void ld_batch(const void* p, uint32_t (&w)[B]) {
 template <int NP, int VEC, int CPL>
 constexpr int batch_size() {
   constexpr int regs = NP * VEC * CPL;
+#ifdef FCOO_BATCH_MAX  // experiment builds: cap the batch (memory-level-parallelism probe)
+  constexpr int b = regs * 8 <= 64 ? 8 : regs * 4 <= 64 ? 4 : regs * 2 <= 64 ? 2 : 1;
+  return b < FCOO_BATCH_MAX ? b : FCOO_BATCH_MAX;
+#else
   return regs * 8 <= 64 ? 8 : regs * 4 <= 64 ? 4 : regs * 2 <= 64 ? 2 : 1;
+#endif
 }
 
 __device__ __forceinline__ void red_add_v4(float* p, float4 v) {
