@@ -185,7 +185,10 @@ fcoo_status fcoo_destroy(fcoo_t f);
 
 /* ---- multi-GPU ("multiple-GPUs can be used") ----
  * One process per GPU.  Rank 0 calls fcoo_comm_unique_id and broadcasts the 128 bytes (the
- * Python binding uses torch.distributed); every rank calls fcoo_comm_init on its device. */
+ * Python binding uses torch.distributed); every rank calls fcoo_comm_init with its device current
+ * (collective: NCCL communicator init, also for nranks == 1, so the NCCL path can be exercised on
+ * one GPU; handles never attach a 1-rank comm).  Errors: ARG, OOM, NCCL.  fcoo_comm_destroy frees
+ * it (NULL is OK); no handle or multicast buffer may still use it. */
 fcoo_status fcoo_comm_unique_id(void* out128);
 fcoo_status fcoo_comm_init(int rank, int nranks, const void* uid128, fcoo_comm_t* out);
 fcoo_status fcoo_comm_destroy(fcoo_comm_t comm);
