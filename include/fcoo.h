@@ -256,11 +256,16 @@ typedef struct {
   int tile_nnz;     /* 0 -> automatic (see fcoo_build_opts) */
   fcoo_comm_t comm; /* NULL = single GPU */
   int rank, nranks; /* shard of this process (ignored when comm == NULL) */
+  uint64_t seed;    /* != 0: the library seeds the factors itself (below); 0: caller's init */
 } fcoo_cp_opts;
 
 /*
  * cp_als — factors: host array of `order` DEVICE pointers to I_m x R fp32 buffers holding the
- * initial factors on entry (caller-seeded) and the unit-column factors on exit.
+ * initial factors on entry (opts->seed == 0: caller-seeded) and the unit-column factors on exit.
+ * opts->seed != 0 overwrites them first, on the device, with entry e of mode m =
+ * (h(seed, 1000 + m, e) >> 40) * 2^-24 in [0, 1), h the counter-based splitmix64 hash of
+ * DESIGN.md §4 (the same values as the test generator's factors(dims, R, seed)), so every rank of
+ * a sharded run starts from identical factors without a host round trip.
  * lambda: device [R] fp32 (out).  fit_trace: host [iters] (out).  iters_done: host (out).
  * Synchronises `stream` once per iteration when tol > 0 (to read the fit for the stopping rule),
  * otherwise once at the end (the fit trace stays on the device until then).

@@ -413,6 +413,21 @@ __global__ void k_scale(float* __restrict__ U, int64_t I, int R, const double* _
 
 __global__ void k_set_int(int* p, int v0, int v1, int v2) { p[0] = v0; p[1] = v1; p[2] = v2; }
 
+// Seeded initial factor (opts->seed != 0): U[e] = (h(seed, stream, e) >> 40) * 2^-24 with the
+// counter-based h(seed, stream, ctr) = splitmix64(splitmix64(splitmix64(seed) ^ stream) ^ ctr)
+// (DESIGN.md §4), i.e. 24-bit uniform values in [0, 1), exact in fp32.
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  uint64_t z = x + 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__global__ void k_seed_uniform(float* __restrict__ U, int64_t n, uint64_t seed, uint64_t stream) {
+  const uint64_t base = splitmix64(splitmix64(seed) ^ stream);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x)
+    U[e] = (float)(splitmix64(base ^ (uint64_t)e) >> 40) * (1.0f / 16777216.0f);
+}
+
 // part[c] = sum_{i in chunk c} sum_r lambda_r M[i,r] U[i,r]   (M from the fp64 buffer when *use64;
 // nothing at all when run_if is given and *run_if == 0)
 __global__ void k_inner_partial(const float* __restrict__ M32, const double* __restrict__ M64,
@@ -603,6 +618,14 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
     return FCOO_OK;
   };
   fcoo_status st = FCOO_OK;
+  if (o->seed) {  // library-seeded initial factors (stream 1000 + m, as the test generator)
+    for (int m = 0; m < N; ++m) {
+      const int64_t n = X->dims[m] * R;
+      k_seed_uniform<<<(unsigned)std::min<int64_t>(4096, (n + kCT - 1) / kCT), kCT, 0, s>>>(factors[m], n, o->seed,
+                                                                                          1000u + (uint64_t)m);
+      FCOO_LAUNCH_CHECK();
+    }
+  }
   // initial Grams of the given factors; |X|^2
   for (int m = 0; m < N && !st; ++m) st = gram(factors[m], X->dims[m], Gs.as<double>() + (int64_t)m * RR);
   int nx = (int)std::min<int64_t>(maxchunks, std::max<int64_t>(1, (X->nnz + 65535) / 65536));
