@@ -74,6 +74,13 @@ typedef struct {
  * the default ascending order of reading Q5: the last (per-nonzero random) product mode is then
  * the smallest factor.  Same segments, same sum, another canonical permutation. */
 #define FCOO_BUILD_PRODUCT_DESC 2u
+/* Bitwise-reproducible SpMTTKRP / SpTTM on this handle (SURVEY §8(b) DETERMINISTIC): instead of
+ * red.global.add, a tile writes the partial sums of the (at most two) segments it shares with its
+ * neighbours to a per-call scratch array (2 x R per tile, through the handle's allocator), and a
+ * second kernel adds the partials of each tile-crossing segment in tile order and stores the row.
+ * Same sum, a fixed association: repeated calls give identical bits.  SpTTMc and the CP-ALS
+ * fit-mode fp64 pass keep red.add. */
+#define FCOO_BUILD_DETERMINISTIC 4u
 
 /* Build options.  NULL -> {FCOO_OP_MTTKRP, 0 (automatic), 0}.
  * tile_nnz = T, the partition length ("threadlen", P:L272 / P:L426): a multiple of 32 in

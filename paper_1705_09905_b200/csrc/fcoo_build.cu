@@ -330,6 +330,7 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
   f->build_stream = s;
   cudaGetDevice(&f->device);
   f->T = T;
+  f->deterministic = (flags & FCOO_BUILD_DETERMINISTIC) ? 1 : 0;
   f->nnz = coo->nnz;
   f->ntiles = (f->nnz + T - 1) / T;
   f->nnz_pad = f->ntiles * T;

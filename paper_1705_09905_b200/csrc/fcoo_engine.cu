@@ -22,7 +22,57 @@ __global__ void k_zero_boundary_rows(const uint32_t* __restrict__ sf, const uint
   for (int c = 0; c < R; ++c) o[c] = ACC(0);
 }
 
+// Deterministic handles (FCOO_BUILD_DETERMINISTIC): one warp per tile t of the shard starts the
+// ordered sum of every tile-crossing segment that begins in t (slot 1: t's own right-open last
+// segment) or enters the shard at t = tile_begin (slot 0), adds slot 0 of each following tile the
+// segment covers, in tile order, and stores the row; lanes stride over the R columns.
+template <class ACC>
+__global__ void k_combine_boundaries(const uint32_t* __restrict__ sf, const uint32_t* __restrict__ seg_base,
+                                     const uint32_t* __restrict__ seg_coord, int64_t ntiles, int64_t tile_begin,
+                                     int64_t tile_end, int R, const ACC* __restrict__ dpart, ACC* __restrict__ out) {
+  const int64_t t = tile_begin + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
+  const int lane = threadIdx.x & 31;
+  if (t >= tile_end) return;
+  auto sfbit = [&](int64_t u) { return (sf[u >> 5] >> (u & 31)) & 1u; };
+  auto right_open = [&](int64_t u) { return u + 1 < ntiles && !sfbit(u + 1); };
+  const uint32_t h0 = seg_base[t], h1 = seg_base[t + 1];  // heads before tile t / before t + 1
+  for (int which = 0; which < 2; ++which) {
+    uint32_t ord;
+    bool cont;
+    if (which == 0) {  // the shard's first tile, entered by a segment that began in an earlier shard
+      if (!(t == tile_begin && t > 0 && !sfbit(t))) continue;
+      ord = h0 - 1u;
+      cont = (h1 == h0) && right_open(t);
+    } else {  // a segment that starts in t and continues into t + 1
+      if (!(h1 > h0 && right_open(t))) continue;
+      ord = h1 - 1u;
+      cont = true;
+    }
+    const int64_t row = seg_coord ? (int64_t)seg_coord[ord] : (int64_t)ord;
+    for (int c = lane; c < R; c += 32) {
+      ACC sum = dpart[((size_t)t * 2 + (which == 0 ? 0 : 1)) * (uint32_t)R + c];
+      bool more = cont;
+      for (int64_t u = t + 1; more && u < tile_end; ++u) {
+        sum += dpart[(size_t)u * 2 * (uint32_t)R + c];
+        more = (seg_base[u + 1] == seg_base[u]) && right_open(u);
+      }
+      out[row * R + c] = sum;
+    }
+  }
+}
+
 namespace {
+
+template <class ACC>
+fcoo_status combine_boundaries(fcoo_s* f, int R, const ACC* dpart, ACC* out, cudaStream_t s) {
+  const int64_t nt = f->tile_end - f->tile_begin;
+  if (nt <= 0) return FCOO_OK;
+  k_combine_boundaries<ACC><<<(unsigned)((nt * 32 + 255) / 256), 256, 0, s>>>(
+      f->sf, f->seg_base, (f->op == FCOO_OP_MTTKRP && !f->dense_rows) ? f->seg_coord : nullptr, f->ntiles,
+      f->tile_begin, f->tile_end, R, dpart, out);
+  FCOO_LAUNCH_CHECK();
+  return FCOO_OK;
+}
 
 template <class ACC>
 cudaError_t launch_engine(const EngineParams& P, int NP, bool vec_ok, cudaStream_t s) {
@@ -91,8 +141,12 @@ fcoo_status mttkrp_t(fcoo_s* f, const float* const* factors, int R, ACC* out, cu
   } else if (!vec_ok || R < 16 || engine_env() != 2 || f->n_prod < 2) {
     return fail(FCOO_ERR_ARG, "fused combine needs the staged float4 engine (order >= 3, R %% 4 == 0, 16 <= R <= 128, aligned)");
   }
+  Buf dpart(&f->alloc, f->deterministic ? sizeof(ACC) * (size_t)f->ntiles * 2 * (size_t)R : 0, s);
+  if (!dpart.ok()) return fail(FCOO_ERR_OOM, "deterministic partials");
+  P.dpart = dpart.p;
   cudaError_t e = launch_engine<ACC>(P, f->n_prod, vec_ok, s);
   if (e != cudaSuccess) return fail(FCOO_ERR_CUDA, "mttkrp launch: %s", cudaGetErrorString(e));
+  if (f->deterministic) return combine_boundaries<ACC>(f, R, dpart.as<ACC>(), out, s);
   return FCOO_OK;
 }
 
@@ -114,6 +168,7 @@ fcoo_status run_mttkrp_mc(fcoo_s* f, const float* const* factors, int R, fcoo_mc
   const size_t need = sizeof(float) * (size_t)f->dims[f->mode] * (size_t)R;
   if (bytes < need) return fail(FCOO_ERR_ARG, "multicast buffer holds %zu bytes, output needs %zu", bytes, need);
   if (f->comm && f->comm != comm) return fail(FCOO_ERR_ARG, "handle sharded over a different comm");
+  if (f->deterministic) return fail(FCOO_ERR_ARG, "fused combine: the multicast reduction order is not fixed (deterministic handle)");
   FCOO_CUDA_TRY(cudaMemsetAsync(uc, 0, need, s));
   fcoo_status st = comm_barrier(comm, s);
   if (st) return st;
@@ -139,8 +194,15 @@ fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s
   P.T = (int)f->T; P.R = R; P.out = out;
   fcoo_status st = prepare_output<float>(f, R, out, f->nsegs, true, s);
   if (st) return st;
+  Buf dpart(&f->alloc, f->deterministic ? sizeof(float) * (size_t)f->ntiles * 2 * (size_t)R : 0, s);
+  if (!dpart.ok()) return fail(FCOO_ERR_OOM, "deterministic partials");
+  P.dpart = dpart.p;
   cudaError_t e = launch_engine<float>(P, 1, vec_ok, s);
   if (e != cudaSuccess) return fail(FCOO_ERR_CUDA, "ttm launch: %s", cudaGetErrorString(e));
+  if (f->deterministic) {
+    st = combine_boundaries<float>(f, R, dpart.as<float>(), out, s);
+    if (st) return st;
+  }
   if (f->comm) return comm_allreduce(f->comm, out, (size_t)f->nsegs * R, s);
   return FCOO_OK;
 }

@@ -20,6 +20,9 @@ struct EngineParams {
   // fused combine (fcoo_mttkrp_mc): multicast address of the output; segment
   // flushes go to every rank's copy with multimem.st / multimem.red.add (fp32 float4 path only)
   float* out_mc;
+  // deterministic handles: per-tile partials of the shared segments, ACC[ntiles][2][R] (slot 0:
+  // the tile's left-open first segment, slot 1: its own right-open last segment); nullptr = red.add
+  void* dpart;
   // device-side gate (CP-ALS fit mode): when non-null the launch does its work only if
   // (*gate != 0) == gate_on, so the fp32/fp64 choice needs no host synchronisation
   const int* gate;

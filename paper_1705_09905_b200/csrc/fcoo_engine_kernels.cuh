@@ -107,6 +107,23 @@ __device__ __forceinline__ float4 zero_if(bool z, float4 a) {
   return z ? make_float4(0.f, 0.f, 0.f, 0.f) : a;
 }
 __device__ __forceinline__ float zero_if(bool z, float a) { return z ? 0.f : a; }
+// Deterministic handles: the shared-segment flush goes to the tile's partial slot (plain store)
+__device__ __forceinline__ void store2_if(bool s0, float* p0, bool s1, float* p1, float4 v) {
+  asm volatile(
+      "{ .reg .pred ps, pr; setp.ne.b32 ps, %0, 0; setp.ne.b32 pr, %1, 0;\n"
+      "  @ps st.global.v4.f32 [%2], {%4,%5,%6,%7};\n"
+      "  @pr st.global.v4.f32 [%3], {%4,%5,%6,%7}; }" ::"r"((int)s0),
+      "r"((int)s1), "l"(p0), "l"(p1), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w)
+      : "memory");
+}
+__device__ __forceinline__ void store2_if(bool s0, float* p0, bool s1, float* p1, float v) {
+  asm volatile(
+      "{ .reg .pred ps, pr; setp.ne.b32 ps, %0, 0; setp.ne.b32 pr, %1, 0;\n"
+      "  @ps st.global.f32 [%2], %4;\n"
+      "  @pr st.global.f32 [%3], %4; }" ::"r"((int)s0),
+      "r"((int)s1), "l"(p0), "l"(p1), "f"(v)
+      : "memory");
+}
 
 // Per-lane column slot: VEC consecutive fp32 factor entries (float4 on the vector path) and an
 // accumulator of type ACC (fp32 for the product path; fp64 for the CP-ALS fit mode, where the
@@ -354,10 +371,14 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
   for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
   auto flush = [&](bool store) {
     ACC* o = reinterpret_cast<ACC*>(P.out) + row * (int64_t)R;
+    // deterministic handles: a shared segment goes to the tile's partial slot (0: left-open first
+    // segment, 1: own right-open last segment), combined later in tile order
+    ACC* dp = P.dpart ? reinterpret_cast<ACC*>(P.dpart) + ((size_t)t * 2 + (own ? 1 : 0)) * (uint32_t)R : nullptr;
 #pragma unroll
     for (int c = 0; c < CPL; ++c)
       if (cok[c]) {
         if (store) A::store(o + col[c], acc[c]);
+        else if (dp) A::store(dp + col[c], acc[c]);
         else A::red(o + col[c], acc[c]);
       }
   };
@@ -480,10 +501,14 @@ __global__ void __launch_bounds__(256) k_segreduce_fact(const EngineParams P) {
 
   auto flush = [&](bool store) {
     ACC* o = reinterpret_cast<ACC*>(P.out) + row * (int64_t)R;
+    // deterministic handles: a shared segment goes to the tile's partial slot (0: left-open first
+    // segment, 1: own right-open last segment), combined later in tile order
+    ACC* dp = P.dpart ? reinterpret_cast<ACC*>(P.dpart) + ((size_t)t * 2 + (own ? 1 : 0)) * (uint32_t)R : nullptr;
 #pragma unroll
     for (int c = 0; c < CPL; ++c)
       if (cok[c]) {
         if (store) A::store(o + col[c], acc[c]);
+        else if (dp) A::store(dp + col[c], acc[c]);
         else A::red(o + col[c], acc[c]);
       }
   };
@@ -687,11 +712,19 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
 #pragma unroll
   for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
   float* const mcp = NP >= 2 ? P.out_mc : nullptr;  // fused combine (float4 fp32, order >= 3; host checks)
+  // deterministic handles, branch-free path: the only shared flush there is the left-open segment,
+  // to slot 0 of this tile (address formed at the flush from the kernel parameter)
+  auto dpt0 = [&]() { return reinterpret_cast<ACC*>(P.dpart) + (size_t)t * 2 * (uint32_t)R; };
   auto flush = [&](bool store) {
     ACC* o = outp + (size_t)row * (uint32_t)R;
+    ACC* dp = P.dpart ? reinterpret_cast<ACC*>(P.dpart) + ((size_t)t * 2 + (own ? 1 : 0)) * (uint32_t)R : nullptr;
 #pragma unroll
     for (int c = 0; c < CPL; ++c)
       if (cok[c]) {
+        if (!store && dp) {
+          A::store(dp + col[c], acc[c]);
+          continue;
+        }
         if constexpr (std::is_same<AT, float4>::value && NP >= 2) {  // MTTKRP of order >= 3
           if (mcp) {
             mc_flush_if(store, !store, mcp + (size_t)row * (uint32_t)R + col[c], acc[c]);
@@ -764,29 +797,39 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
         // segment is flushed by a predicated store (owned) or red.add (shared with the left tile),
         // the accumulator is reset by select and the segment ordinal advances by the head bit
         const bool first = (ci == 0 && bi == 0);  // the tile's first nonzero opens, never closes
+        // FM: 0 = store / red.add, 1 = store / tile partial (deterministic handle), 2 = multicast
+        // (fused combine); chosen once per batch so the per-nonzero path carries no extra branch
+        auto headed = [&](auto fm_tag) {
+          constexpr int FM = decltype(fm_tag)::value;
 #pragma unroll
-        for (int e = 0; e < B; ++e) {
-          const bool hd = (heads >> e) & 1u;
-          const bool cl = hd && (e != 0 || !first);
-          ACC* o = outp + (size_t)row * (uint32_t)R;
+          for (int e = 0; e < B; ++e) {
+            const bool hd = (heads >> e) & 1u;
+            const bool cl = hd && (e != 0 || !first);
+            ACC* o = outp + (size_t)row * (uint32_t)R;
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            if (cok[c]) {
-              if constexpr (std::is_same<AT, float4>::value && NP >= 2) {  // MTTKRP of order >= 3
-                if (mcp) mc_flush_if(cl && own, cl && !own, mcp + (size_t)row * (uint32_t)R + col[c], acc[c]);
-                else flush_if(cl && own, cl && !own, o + col[c], acc[c]);
-              } else {
-                flush_if(cl && own, cl && !own, o + col[c], acc[c]);
+            for (int c = 0; c < CPL; ++c) {
+              if (cok[c]) {
+                if constexpr (FM == 2) {
+                  if constexpr (std::is_same<AT, float4>::value && NP >= 2)
+                    mc_flush_if(cl && own, cl && !own, mcp + (size_t)row * (uint32_t)R + col[c], acc[c]);
+                } else if constexpr (FM == 1) {
+                  store2_if(cl && own, o + col[c], cl && !own, dpt0() + col[c], acc[c]);
+                } else {
+                  flush_if(cl && own, cl && !own, o + col[c], acc[c]);
+                }
               }
+              acc[c] = zero_if(hd, acc[c]);
             }
-            acc[c] = zero_if(hd, acc[c]);
-          }
-          own = own || hd;
-          s += hd ? 1u : 0u;
-          if (hd) row = P.seg_coord ? P.seg_coord[s] : s;
+            own = own || hd;
+            s += hd ? 1u : 0u;
+            if (hd) row = P.seg_coord ? P.seg_coord[s] : s;
 #pragma unroll
-          for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), r[e][c]);
-        }
+            for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), r[e][c]);
+          }
+        };
+        if (mcp) headed(std::integral_constant<int, 2>{});
+        else if (P.dpart) headed(std::integral_constant<int, 1>{});
+        else headed(std::integral_constant<int, 0>{});
       } else {
 #pragma unroll
         for (int e = 0; e < B; ++e) {
@@ -856,7 +899,7 @@ template <int NP, int G, int VEC, int CPL, class ACC>
 cudaError_t launch_one(const EngineParams& P, cudaStream_t s) {
   const bool full = (P.R == G * VEC * CPL);
   const int variant = engine_variant();
-  const bool fact = NP >= 2 && variant == 1;
+  const bool fact = NP >= 2 && variant == 1 && !P.dpart;
   const bool staged = variant == 2 && G >= 4;
   const int TB = 256;
   void (*kern)(const EngineParams);

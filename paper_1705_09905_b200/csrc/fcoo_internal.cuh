@@ -51,6 +51,7 @@ struct fcoo_s {
   int64_t dims[fcoo::kMaxOrder] = {0};
   int64_t nnz = 0, nnz_pad = 0, ntiles = 0, nsegs = 0, T = 256;
   int dense_rows = 0;
+  int deterministic = 0;  // FCOO_BUILD_DETERMINISTIC: tile partials + ordered combine, no red.add
   // device arrays
   uint32_t* pidx = nullptr;      // n_prod x nnz_pad (row a = product mode prod_modes[a])
   float* val = nullptr;          // nnz_pad

@@ -22,6 +22,7 @@ ERR_ARG, ERR_ORDER, ERR_MODE, ERR_INDEX_RANGE, ERR_DUPLICATE, ERR_EMPTY, ERR_KEY
 OP_MTTKRP, OP_TTM = 0, 1
 BUILD_KEEP_PERM = 1
 BUILD_PRODUCT_DESC = 2
+BUILD_DETERMINISTIC = 4
 
 
 class FcooError(RuntimeError):
@@ -288,9 +289,10 @@ class Fcoo:
 
 
 def fcoo_build(coo: Coo, mode: int, op: int = OP_MTTKRP, tile_nnz: int = 0, keep_perm: bool = False,
-               product_desc: bool = False, stream=None) -> Fcoo:
+               product_desc: bool = False, stream=None, deterministic: bool = False) -> Fcoo:
     L = load_library()
-    opts = _BuildOpts(op, tile_nnz, (BUILD_KEEP_PERM if keep_perm else 0) | (BUILD_PRODUCT_DESC if product_desc else 0))
+    opts = _BuildOpts(op, tile_nnz, (BUILD_KEEP_PERM if keep_perm else 0) | (BUILD_PRODUCT_DESC if product_desc else 0)
+                      | (BUILD_DETERMINISTIC if deterministic else 0))
     out = ctypes.c_void_p()
     _check(L.fcoo_build(ctypes.byref(coo.c), mode, ctypes.byref(opts), ctypes.byref(_ALLOCATOR),
                         ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out)), "fcoo_build")
@@ -298,10 +300,10 @@ def fcoo_build(coo: Coo, mode: int, op: int = OP_MTTKRP, tile_nnz: int = 0, keep
 
 
 def fcoo_build_sharded(coo: Coo, mode: int, comm: "Comm", op: int = OP_MTTKRP, tile_nnz: int = 0,
-                       keep_perm: bool = False, stream=None) -> Fcoo:
+                       keep_perm: bool = False, stream=None, deterministic: bool = False) -> Fcoo:
     """fcoo_build + fcoo_set_shard(comm.rank, comm.nranks, comm) in one C call."""
     L = load_library()
-    opts = _BuildOpts(op, tile_nnz, BUILD_KEEP_PERM if keep_perm else 0)
+    opts = _BuildOpts(op, tile_nnz, (BUILD_KEEP_PERM if keep_perm else 0) | (BUILD_DETERMINISTIC if deterministic else 0))
     out = ctypes.c_void_p()
     _check(L.fcoo_build_sharded(ctypes.byref(coo.c), mode, ctypes.byref(opts), comm.h, ctypes.byref(_ALLOCATOR),
                                 ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out)), "fcoo_build_sharded")

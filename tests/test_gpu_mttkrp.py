@@ -195,3 +195,69 @@ def test_nell1_full_size_wide_keys(F):
         got = _run(F, w.dims, idx, val, mode, fs, 8, 0)
         M, D = oracle.mttkrp(w.dims, idx, val, mode, fs, nthreads=os.cpu_count() or 8)
         assert_parity(got, M, D, what=f"nell1 mode {mode}")
+
+
+@pytest.mark.parametrize("T", [32, 64, 256, 2048])
+def test_deterministic_flag_bitwise_and_parity(F, T):
+    """FCOO_BUILD_DETERMINISTIC: tile partials of shared segments combined in tile
+    order instead of red.add — repeated calls are bitwise identical (also with shards, whose
+    partial rows are then summed on the host in rank order), and the result matches the oracle.
+    Heavy power law so single slices span many tiles."""
+    import torch
+    dims = (60, 700, 500)
+    idx, val = gen.coo(dims, 120000, (1.2, 0.5, 0.5), 49)
+    R = 32
+    fs = gen.factors(dims, R, 8, signed=True)
+    ft = [torch.from_numpy(f).cuda() for f in fs]
+    coo = F.Coo.from_numpy(dims, idx, val)
+    for mode in range(3):
+        h = F.fcoo_build(coo, mode, tile_nnz=T, deterministic=True)
+        outs = []
+        for _ in range(3):
+            o = torch.full((dims[mode], R), float("nan"), device="cuda")
+            F.fcoo_mttkrp(h, ft, R, o)
+            outs.append(o)
+        torch.cuda.synchronize()
+        assert all(torch.equal(outs[0], o) for o in outs[1:])
+        M, D = oracle.mttkrp(dims, idx, val, mode, fs, nthreads=8)
+        assert_parity(outs[0].cpu().numpy(), M, D, what=f"deterministic T={T} mode={mode}")
+        parts = []
+        for g in range(3):
+            F.fcoo_set_shard(h, g, 3)
+            o = torch.full((dims[mode], R), float("nan"), device="cuda")
+            F.fcoo_mttkrp(h, ft, R, o)
+            parts.append(o.double())
+        torch.cuda.synchronize()
+        assert_parity((parts[0] + parts[1] + parts[2]).cpu().numpy(), M, D, what=f"deterministic shards T={T}")
+        h.destroy()
+
+
+@pytest.mark.parametrize("R", [8, 16, 5])
+def test_deterministic_flag_other_paths(F, R):
+    """The unstaged engine (R < 16, scalar R) and SpTTM on deterministic handles."""
+    import torch
+    dims = (80, 600, 400)
+    idx, val = gen.coo(dims, 50000, (1.0, 0.5, 0.5), 50)
+    fs = gen.factors(dims, R, 9, signed=True)
+    ft = [torch.from_numpy(f).cuda() for f in fs]
+    coo = F.Coo.from_numpy(dims, idx, val)
+    h = F.fcoo_build(coo, 0, tile_nnz=64, deterministic=True)
+    a = torch.empty((dims[0], R), device="cuda")
+    b = torch.empty((dims[0], R), device="cuda")
+    F.fcoo_mttkrp(h, ft, R, a)
+    F.fcoo_mttkrp(h, ft, R, b)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)
+    M, D = oracle.mttkrp(dims, idx, val, 0, fs, nthreads=8)
+    assert_parity(a.cpu().numpy(), M, D, what=f"deterministic unstaged R={R}")
+    h.destroy()
+    t = F.fcoo_build(coo, 1, op=F.OP_TTM, tile_nnz=64, deterministic=True)
+    y1 = torch.empty((t.info.nsegs, R), device="cuda")
+    y2 = torch.empty((t.info.nsegs, R), device="cuda")
+    F.fcoo_ttm(t, ft[1], R, y1)
+    F.fcoo_ttm(t, ft[1], R, y2)
+    torch.cuda.synchronize()
+    assert torch.equal(y1, y2)
+    coords, Y, Dy = oracle.ttm(dims, idx, val, 1, fs[1])
+    assert_parity(y1.cpu().numpy(), Y, Dy, what=f"deterministic ttm R={R}")
+    t.destroy()
