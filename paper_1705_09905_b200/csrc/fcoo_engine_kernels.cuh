@@ -655,7 +655,7 @@ struct Stage {
 // HBM latency of the stream is off the critical path; only the L2-resident factor gathers remain
 // exposed.  This is the "shared-memory staging of the nonzero stream" of the north star; the
 // factor rows still go through L1 (most of the unified carveout stays L1).
-template <int NP, int G, int VEC, int CPL, class ACC, bool FULL>
+template <int NP, int G, int VEC, int CPL, class ACC, bool FULL, bool DET>
 // L1 policy of the factor-row gathers in the staged kernel (see Ld<4>::load_pol): the last
 // product position is the per-nonzero random gather, the others are sorted within a segment.
 #ifndef FCOO_L1POL_INNER
@@ -717,13 +717,14 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
   auto dpt0 = [&]() { return reinterpret_cast<ACC*>(P.dpart) + (size_t)t * 2 * (uint32_t)R; };
   auto flush = [&](bool store) {
     ACC* o = outp + (size_t)row * (uint32_t)R;
-    ACC* dp = P.dpart ? reinterpret_cast<ACC*>(P.dpart) + ((size_t)t * 2 + (own ? 1 : 0)) * (uint32_t)R : nullptr;
 #pragma unroll
     for (int c = 0; c < CPL; ++c)
       if (cok[c]) {
-        if (!store && dp) {
-          A::store(dp + col[c], acc[c]);
-          continue;
+        if constexpr (DET) {  // deterministic handle: shared segment -> the tile's partial slot
+          if (!store) {
+            A::store(reinterpret_cast<ACC*>(P.dpart) + ((size_t)t * 2 + (own ? 1 : 0)) * (uint32_t)R + col[c], acc[c]);
+            continue;
+          }
         }
         if constexpr (std::is_same<AT, float4>::value && NP >= 2) {  // MTTKRP of order >= 3
           if (mcp) {
@@ -827,9 +828,12 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
             for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), r[e][c]);
           }
         };
-        if (mcp) headed(std::integral_constant<int, 2>{});
-        else if (P.dpart) headed(std::integral_constant<int, 1>{});
-        else headed(std::integral_constant<int, 0>{});
+        if constexpr (DET) {
+          headed(std::integral_constant<int, 1>{});
+        } else {
+          if (mcp) headed(std::integral_constant<int, 2>{});
+          else headed(std::integral_constant<int, 0>{});
+        }
       } else {
 #pragma unroll
         for (int e = 0; e < B; ++e) {
@@ -905,7 +909,10 @@ cudaError_t launch_one(const EngineParams& P, cudaStream_t s) {
   void (*kern)(const EngineParams);
   size_t smem = 0;
   if (staged) {
-    kern = full ? k_segreduce_staged<NP, G, VEC, CPL, ACC, true> : k_segreduce_staged<NP, G, VEC, CPL, ACC, false>;
+    if (P.dpart)
+      kern = full ? k_segreduce_staged<NP, G, VEC, CPL, ACC, true, true> : k_segreduce_staged<NP, G, VEC, CPL, ACC, false, true>;
+    else
+      kern = full ? k_segreduce_staged<NP, G, VEC, CPL, ACC, true, false> : k_segreduce_staged<NP, G, VEC, CPL, ACC, false, false>;
     smem = sizeof(uint32_t) * (size_t)(TB / G) * Stage<NP>::STRIDE;
   } else if constexpr (NP >= 2) {
     if (fact) kern = full ? k_segreduce_fact<NP, G, VEC, CPL, ACC, true> : k_segreduce_fact<NP, G, VEC, CPL, ACC, false>;
@@ -913,9 +920,10 @@ cudaError_t launch_one(const EngineParams& P, cudaStream_t s) {
   } else {
     kern = full ? k_segreduce<NP, G, VEC, CPL, ACC, true> : k_segreduce<NP, G, VEC, CPL, ACC, false>;
   }
-  static bool configured[2][3] = {{false, false, false}, {false, false, false}};
+  static bool configured[2][3][2] = {};  // [full][variant][deterministic]: one entry per kernel
   const int ci = staged ? 2 : fact ? 1 : 0;
-  if (!configured[full][ci]) {
+  const int di = (staged && P.dpart) ? 1 : 0;
+  if (!configured[full][ci][di]) {
     if (staged) {  // small staging buffers: ask for just enough carveout, keep the rest as L1
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       const int ctas = staged_ctas_per_sm(reinterpret_cast<const void*>(kern));
@@ -924,7 +932,7 @@ cudaError_t launch_one(const EngineParams& P, cudaStream_t s) {
     } else {  // no shared memory: give the whole unified carveout to L1 (factor rows)
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     }
-    configured[full][ci] = true;
+    configured[full][ci][di] = true;
   }
   int64_t groups = P.tile_end - P.tile_begin;
   int64_t threads = groups * G;
