@@ -264,6 +264,8 @@ typedef struct {
   fcoo_comm_t comm; /* NULL = single GPU */
   int rank, nranks; /* shard of this process (ignored when comm == NULL) */
   uint64_t seed;    /* != 0: the library seeds the factors itself (below); 0: caller's init */
+  int deterministic; /* != 0: build every mode with FCOO_BUILD_DETERMINISTIC, so repeated runs
+                        give bitwise-identical factors, lambda and fit trace */
 } fcoo_cp_opts;
 
 /*

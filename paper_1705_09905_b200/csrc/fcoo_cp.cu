@@ -513,7 +513,8 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
   std::vector<fcoo_t> H(N, nullptr);
   auto cleanup = [&]() { for (auto& h : H) { fcoo_destroy(h); h = nullptr; } };
   struct Guard { decltype(cleanup)& c; ~Guard() { c(); } } guard{cleanup};  // early returns too
-  fcoo_build_opts bo{FCOO_OP_MTTKRP, o->tile_nnz > 0 ? o->tile_nnz : 0, 0u};
+  fcoo_build_opts bo{FCOO_OP_MTTKRP, o->tile_nnz > 0 ? o->tile_nnz : 0,
+                     o->deterministic ? FCOO_BUILD_DETERMINISTIC : 0u};
   for (int n = 0; n < N; ++n) {
     fcoo_status st = fcoo_build(X, n, &bo, alloc, (void*)s, &H[n]);
     if (st) { cleanup(); return st; }

@@ -139,3 +139,27 @@ def test_library_seeded_init_matches_generator(F):
     torch.cuda.synchronize()
     for a, b in zip(seeded_then_one, host):
         assert torch.allclose(a, b, rtol=0, atol=1e-5)
+
+
+def test_deterministic_cp_als_bitwise(F):
+    """fcoo_cp_opts.deterministic: every handle is built with FCOO_BUILD_DETERMINISTIC, so two runs
+    (12 iterations, T = 32 so slices span many tiles) give bitwise-identical factors, lambda and fit
+    trace, and the trace still matches the oracle."""
+    import torch
+    dims = (40, 30, 20)
+    R = 4
+    rng_f = [gen.uniform((I, R), 61, m) for m, I in enumerate(dims)]
+    idx, _ = gen.coo(dims, 6000, None, 62)
+    val = gen.kruskal_coo(rng_f, np.ones(R), idx)
+    coo = F.Coo.from_numpy(dims, idx, val)
+    init = gen.factors(dims, R, 63)
+    runs = []
+    for _ in range(2):
+        fs = [torch.from_numpy(f).cuda() for f in init]
+        lam, trace = F.cp_als(coo, R, 12, fs, tile_nnz=32, deterministic=True)
+        torch.cuda.synchronize()
+        runs.append(([f.cpu() for f in fs], lam.cpu(), list(trace)))
+    (fa, la, ta), (fb, lb, tb) = runs
+    assert ta == tb and torch.equal(la, lb) and all(torch.equal(x, y) for x, y in zip(fa, fb))
+    _, _, ot = oracle.cp_als(dims, idx, val, R, 12, init)
+    assert np.allclose(ta, ot, rtol=0, atol=1e-4)
