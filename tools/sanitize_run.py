@@ -1,5 +1,5 @@
 """Small end-to-end run that reaches every engine specialisation used at scale (staged float4 path at
-R=16/32/64, scalar path, TTM, fp64 CP fit mode, sharded handles) — the workload for
+R=16/32/64, scalar path, TTM, fp64 CP fit mode, sharded handles, deterministic handles) — the workload for
 compute-sanitizer memcheck / racecheck / synccheck.
 
 compute-sanitizer --tool racecheck python tools/sanitize_run.py
@@ -54,6 +54,23 @@ def main():
     # CP-ALS: eager first iteration, the captured graph for the rest, the exact-fit recompute
     fs = [torch.from_numpy(f).cuda() for f in gen.factors(dims, 8, 5)]
     P.cp_als(coo, 8, 4, fs, tile_nnz=64)
+    # deterministic handles: tile partials + k_combine_boundaries (staged, unstaged, shards, SpTTM,
+    # CP-ALS with its fp64 pass), and the library-seeded CP init
+    for R in (32, 8):
+        fsr = [torch.from_numpy(f).cuda() for f in gen.factors(dims, R, 4)]
+        for n in range(3):
+            h = P.fcoo_build(coo, n, tile_nnz=64, deterministic=True)
+            out = torch.empty((dims[n], R), device="cuda")
+            P.fcoo_mttkrp(h, fsr, R, out)
+            P.fcoo_set_shard(h, 1, 3)
+            P.fcoo_mttkrp(h, fsr, R, out)
+            h.destroy()
+        t = P.fcoo_build(coo, 1, op=P.OP_TTM, tile_nnz=64, deterministic=True)
+        yo = torch.empty((t.info.nsegs, R), device="cuda")
+        P.fcoo_ttm(t, fsr[1], R, yo)
+        t.destroy()
+    fs = [torch.empty((d, 8), device="cuda") for d in dims]
+    P.cp_als(coo, 8, 4, fs, tile_nnz=64, seed=3, deterministic=True)
     torch.cuda.synchronize()
     print("sanitize_run OK")
 
