@@ -46,6 +46,8 @@ def _load():
         L.orc_storage_bytes.argtypes = [i64, ci, i64]
         L.orc_build.argtypes = [ci, vp, i64, vp, vp, ci, ci, i64, vp, vp, vp, vp, vp, vp, vp, vp]
         L.orc_build_ex.argtypes = [ci, vp, i64, vp, vp, ci, ci, i64, ci, vp, vp, vp, vp, vp, vp, vp, vp]
+        L.orc_build_blocked.argtypes = [ci, vp, i64, vp, vp, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                        i64, vp, vp, vp]
         L.orc_mode_spec_ex.argtypes = [ci, vp, ci, ci, ci, vp, vp, vp, vp]
         L.orc_mttkrp.argtypes = [ci, vp, i64, vp, vp, ci, vp, ci, vp, vp, ci]
         L.orc_ttm.argtypes = [ci, vp, i64, vp, vp, ci, vp, ci, vp, vp, vp, vp]
@@ -129,6 +131,69 @@ def build_fcoo(dims, idx, val, op: int, mode: int, T: int, desc: bool = False) -
     nsegs = ns.value
     return Fcoo(im, pm, perm, bf[: (nnz + 7) // 8], sf[: (((nnz + T - 1) // T) + 31) // 32],
                 seg_base[: (nnz + T - 1) // T], seg_coord[:nsegs].copy(), pidx, pval, nsegs, T)
+
+
+@dataclass
+class FcooBlocked:
+    """Oracle blocked F-COO (orc_build_blocked): stream arrays have nstream positions."""
+    index_modes: list
+    product_modes: list
+    perm: np.ndarray        # u32[nstream], 0xFFFFFFFF at padding
+    bf: np.ndarray          # u8[ceil(nstream/8)]
+    sf: np.ndarray          # u32[ceil(ntiles/32)]
+    seg_base: np.ndarray    # u32[ntiles]
+    seg_coord: np.ndarray   # u32[nsegs, n_idx]
+    pidx: np.ndarray        # u32[n_prod, nstream] (global product coords, 0 at padding)
+    val: np.ndarray         # f32[nstream] (0 at padding)
+    pk: np.ndarray          # u32[nstream] packed (outer_local << IB) | last
+    blk_start: np.ndarray   # i64[nblocks + 1]
+    blk_end: np.ndarray     # i64[nblocks]
+    nsegs: int
+    nstream: int
+    nblocks: int
+    T: int
+    BR: int
+    IB: int
+
+    def bf_bits(self) -> np.ndarray:
+        return np.unpackbits(self.bf, bitorder="little")[: self.nstream]
+
+
+def build_fcoo_blocked(dims, idx, val, mode: int, T: int, BR: int) -> FcooBlocked:
+    L = _load()
+    d, idx, val = _coo(dims, idx, val)
+    nnz = val.shape[0]
+    order = len(d)
+    if order < 2 or order > 8:
+        raise OracleError(ERR_ORDER, "build_blocked")
+    im, pm = mode_spec(d, OP_MTTKRP, mode)
+    nblocks = max(1, (int(d[pm[0]]) + BR - 1) // BR)
+    cap = nnz + nblocks * (T - 1)
+    ntiles_cap = max(1, cap // T + 1)
+    perm = np.zeros(cap, np.uint32)
+    bf = np.zeros(max(1, (cap + 7) // 8), np.uint8)
+    sf = np.zeros(max(1, (ntiles_cap + 31) // 32), np.uint32)
+    seg_base = np.zeros(ntiles_cap, np.uint32)
+    seg_coord = np.zeros((max(1, nnz), len(im)), np.uint32)
+    pidx = np.zeros(len(pm) * cap, np.uint32)
+    pval = np.zeros(cap, np.float32)
+    pk = np.zeros(cap, np.uint32)
+    bs = np.zeros(nblocks + 1, np.int64)
+    be = np.zeros(nblocks, np.int64)
+    nsg, nst, nbl = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+    rc = L.orc_build_blocked(order, _ptr(d), nnz, _ptr(idx), _ptr(val), mode, T, BR, _ptr(perm), _ptr(bf), _ptr(sf),
+                             _ptr(seg_base), _ptr(seg_coord), _ptr(pidx), _ptr(pval), _ptr(pk), _ptr(bs), _ptr(be),
+                             cap, ctypes.byref(nsg), ctypes.byref(nst), ctypes.byref(nbl))
+    if rc:
+        raise OracleError(rc, "build_blocked")
+    ns, ntiles = nst.value, nst.value // T
+    IB = 0
+    while (1 << IB) < int(d[pm[-1]]):
+        IB += 1
+    return FcooBlocked(im, pm, perm[:ns].copy(), bf[: (ns + 7) // 8].copy(), sf[: (ntiles + 31) // 32].copy(),
+                       seg_base[:ntiles].copy(), seg_coord[: nsg.value].copy(),
+                       pidx[: len(pm) * ns].reshape(len(pm), ns).copy(), pval[:ns].copy(), pk[:ns].copy(), bs, be,
+                       nsg.value, ns, nbl.value, T, BR, IB if len(pm) >= 2 else 0)
 
 
 def mttkrp(dims, idx, val, mode: int, factors, R: int | None = None, with_D: bool = True, nthreads: int = 1):

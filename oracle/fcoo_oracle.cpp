@@ -172,6 +172,120 @@ int orc_build(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, 
 }
 
 /* ------------------------------------------------------------------------- */
+/* c1b. Blocked F-COO for SpMTTKRP (DESIGN.md §5 "blocked layout", reading Q22).
+ * The F-COO of Fig. 2 / P:L246-282 applied to the sub-tensors X_b = { nonzeros q :
+ * floor(i_outer(q) / BR) == b }, b = 0, 1, ..., where "outer" is the FIRST product mode of Q5
+ * (smallest extent), concatenated in b order, each padded with empty positions to a multiple of
+ * T.  By linearity of Eq.(6), MTTKRP(X) = sum_b MTTKRP(X_b).  Written out:
+ *   key(q) = (b(q), index coords, product coords), sorted ascending (std::sort on (key, q));
+ *   block b occupies stream positions [blk_start[b], blk_start[b+1]), blk_start[0] = 0,
+ *     blk_start[b+1] = blk_start[b] + ceil(n_b / T) * T  (n_b = #nonzeros of X_b; an empty block
+ *     takes no positions); its real nonzeros are [blk_start[b], blk_end[b] = blk_start[b] + n_b);
+ *   padding positions: perm = 0xFFFFFFFF, pidx = pk = 0, val = +0.0, bf = 0;
+ *   bf[p] = 1 iff p is real and (p == blk_start[b] or the index coords differ from p-1's);
+ *   sf[t] = bf[t*T]; seg_base[t] = #heads in [0, t*T); seg_coord[s] = index coords of head s;
+ *   pidx[a][p] = product coord a (global index, Q5 order) of the nonzero at p;
+ *   pk[p] = ((i_outer - b*BR) << IB) | i_last  with IB = ceil(log2(I_last)) (n_prod >= 2), where
+ *     "last" is the last product mode of Q5; pk[p] = i_outer - b*BR when n_prod == 1.
+ * Inputs as orc_build_ex (op = MTTKRP), plus BR >= 1.  Capacities: stream arrays hold
+ * nnz + nblocks*(T-1) positions (nblocks = ceil(I_outer / BR)), seg_coord nnz*n_idx.
+ * Errors as orc_build_ex; ORC_ERR_ARG if the packed word does not fit in 32 bits. */
+int orc_build_blocked(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, const float* val, int mode,
+                      int64_t T, int64_t BR, uint32_t* perm, uint8_t* bf, uint32_t* sf, uint32_t* seg_base,
+                      uint32_t* seg_coord, uint32_t* pidx, float* pval, uint32_t* pk, int64_t* blk_start,
+                      int64_t* blk_end, int64_t cap, int64_t* nsegs_out, int64_t* nstream_out,
+                      int64_t* nblocks_out) {
+  int idx_modes[8], prod_modes[8], n_idx = 0, n_prod = 0;
+  int rc = orc_mode_spec_ex(order, dims, ORC_OP_MTTKRP, mode, 0, idx_modes, &n_idx, prod_modes, &n_prod);
+  if (rc) return rc;
+  if (T < 1 || BR < 1) return ORC_ERR_ARG;
+  if (nnz <= 0) return ORC_ERR_EMPTY;
+  for (int m = 0; m < order; ++m)
+    for (int64_t q = 0; q < nnz; ++q)
+      if ((int64_t)idx[(int64_t)m * nnz + q] >= dims[m]) return ORC_ERR_INDEX_RANGE;
+  const int outer = prod_modes[0], last = prod_modes[n_prod - 1];
+  int IB = 0, LB = 0;
+  while (((int64_t)1 << IB) < dims[last]) ++IB;
+  while (((int64_t)1 << LB) < BR) ++LB;
+  if (n_prod >= 2 && LB + IB > 32) return ORC_ERR_ARG;
+  const int64_t nblocks = (dims[outer] + BR - 1) / BR;
+
+  int key_modes[8];
+  for (int a = 0; a < n_idx; ++a) key_modes[a] = idx_modes[a];
+  for (int a = 0; a < n_prod; ++a) key_modes[n_idx + a] = prod_modes[a];
+  auto coord = [&](int64_t q, int a) { return idx[(int64_t)key_modes[a] * nnz + q]; };
+  auto blk = [&](int64_t q) { return (int64_t)idx[(int64_t)outer * nnz + q] / BR; };
+  std::vector<int64_t> ord(nnz);
+  for (int64_t q = 0; q < nnz; ++q) ord[q] = q;
+  std::sort(ord.begin(), ord.end(), [&](int64_t x, int64_t y) {
+    if (blk(x) != blk(y)) return blk(x) < blk(y);
+    for (int a = 0; a < order; ++a) {
+      uint32_t cx = coord(x, a), cy = coord(y, a);
+      if (cx != cy) return cx < cy;
+    }
+    return x < y;
+  });
+  for (int64_t p = 1; p < nnz; ++p) { /* Q6 */
+    bool same = true;
+    for (int a = 0; a < order && same; ++a) same = coord(ord[p], a) == coord(ord[p - 1], a);
+    if (same) return ORC_ERR_DUPLICATE;
+  }
+  /* block sizes and stream positions */
+  std::vector<int64_t> nb(nblocks, 0);
+  for (int64_t q = 0; q < nnz; ++q) nb[blk(q)]++;
+  blk_start[0] = 0;
+  for (int64_t b = 0; b < nblocks; ++b) {
+    blk_end[b] = blk_start[b] + nb[b];
+    blk_start[b + 1] = blk_start[b] + (nb[b] + T - 1) / T * T;
+  }
+  const int64_t ns = blk_start[nblocks];
+  if (ns > cap) return ORC_ERR_ARG;
+  const int64_t ntiles = ns / T;
+  memset(bf, 0, (size_t)((ns + 7) / 8));
+  memset(sf, 0, sizeof(uint32_t) * (size_t)((ntiles + 31) / 32));
+  for (int64_t p = 0; p < ns; ++p) {
+    perm[p] = 0xFFFFFFFFu;
+    pval[p] = 0.0f;
+    pk[p] = 0u;
+    for (int a = 0; a < n_prod; ++a) pidx[(int64_t)a * ns + p] = 0u;
+  }
+  /* place the sorted nonzeros: the k-th nonzero of block b goes to blk_start[b] + k */
+  std::vector<int64_t> pos_of(nnz);
+  {
+    int64_t k = 0;
+    for (int64_t b = 0; b < nblocks; ++b)
+      for (int64_t r = 0; r < nb[b]; ++r, ++k) pos_of[k] = blk_start[b] + r;
+  }
+  std::vector<int64_t> at(ns, -1); /* stream position -> sorted rank, -1 = padding */
+  for (int64_t k = 0; k < nnz; ++k) at[pos_of[k]] = k;
+  int64_t nsegs = 0;
+  for (int64_t p = 0; p < ns; ++p) {
+    if (p % T == 0) seg_base[p / T] = (uint32_t)nsegs;
+    const int64_t k = at[p];
+    if (k < 0) continue;
+    const int64_t q = ord[k];
+    const int64_t b = blk(q);
+    bool head = (p == blk_start[b]);
+    for (int a = 0; a < n_idx && !head; ++a) head = coord(q, a) != coord(ord[k - 1], a);
+    if (head) {
+      bf[p >> 3] |= (uint8_t)(1u << (p & 7));
+      for (int a = 0; a < n_idx; ++a) seg_coord[nsegs * n_idx + a] = coord(q, a);
+      nsegs++;
+      if (p % T == 0) sf[(p / T) >> 5] |= 1u << ((p / T) & 31);
+    }
+    perm[p] = (uint32_t)q;
+    for (int a = 0; a < n_prod; ++a) pidx[(int64_t)a * ns + p] = coord(q, n_idx + a);
+    memcpy(&pval[p], &val[q], sizeof(float));
+    const uint32_t local = (uint32_t)(idx[(int64_t)outer * nnz + q] - b * BR);
+    pk[p] = n_prod >= 2 ? (uint32_t)(((uint64_t)local << IB) | idx[(int64_t)last * nnz + q]) : local;
+  }
+  *nsegs_out = nsegs;
+  *nstream_out = ns;
+  *nblocks_out = nblocks;
+  return ORC_OK;
+}
+
+/* ------------------------------------------------------------------------- */
 /* c2. SpMTTKRP, Eq.(5)/(6), Table I row 2, order-N (Q17):
  *   M(i_n, r) = sum_q v_q * prod_{m != n} U_m(i_m(q), r)
  * in fp64, in input order.  D(i_n, r) = sum_q |v_q * prod U| is the normaliser of

@@ -168,3 +168,130 @@ def test_product_desc_option_invariants():
         keys = np.stack([idx[m][b.perm] for m in b.index_modes + b.product_modes]).astype(np.int64)
         for p in range(1, val.shape[0]):
             assert tuple(keys[:, p - 1]) < tuple(keys[:, p])
+
+
+# ---------------------------------------------------------------------------------------------
+# Blocked F-COO (orc_build_blocked; DESIGN.md §5 "blocked layout", reading Q22): the F-COO of
+# each sub-tensor X_b = {q : i_outer(q) // BR == b}, concatenated, each padded to a multiple of T.
+# Pinned against the (separately pinned) F-COO definition of each X_b, the single-block special
+# case, brute-force orderings, and the dense definition of Eq.(5) evaluated from the stream.
+
+def _blocked_cases():
+    yield (3, (23, 17, 29), 400, 0, 8, 32)
+    yield (3, (23, 17, 29), 400, 1, 5, 64)
+    yield (3, (23, 17, 29), 400, 2, 4, 32)
+    yield (4, (9, 6, 11, 7), 500, 0, 2, 32)
+    yield (4, (9, 6, 11, 7), 500, 3, 3, 96)
+    yield (2, (31, 40), 300, 0, 7, 32)
+    yield (2, (31, 40), 300, 1, 16, 64)
+
+
+@pytest.mark.parametrize("case", list(_blocked_cases()))
+def test_blocked_blocks_are_fcoo_of_subtensors(case):
+    order, dims, nnz, mode, BR, T = case
+    idx, val = gen.coo(dims, nnz, None, 40 + order + mode)
+    f = oracle.build_fcoo_blocked(dims, idx, val, mode, T, BR)
+    outer, last = f.product_modes[0], f.product_modes[-1]
+    assert f.nblocks == (dims[outer] + BR - 1) // BR
+    assert f.blk_start[0] == 0 and f.blk_start[-1] == f.nstream and f.nstream % T == 0
+    bits = f.bf_bits()
+    for b in range(f.nblocks):
+        s0, e0, s1 = int(f.blk_start[b]), int(f.blk_end[b]), int(f.blk_start[b + 1])
+        sel = np.nonzero(idx[outer] // BR == b)[0]
+        assert e0 - s0 == sel.size and s1 - s0 == -(-sel.size // T) * T
+        # padding: empty positions
+        assert np.all(f.perm[e0:s1] == 0xFFFFFFFF) and np.all(f.val[e0:s1] == 0) and np.all(f.pk[e0:s1] == 0)
+        assert not bits[e0:s1].any() and np.all(f.pidx[:, e0:s1] == 0)
+        if sel.size == 0:
+            continue
+        # the real positions are the (unblocked, pinned) F-COO of X_b, tile length irrelevant
+        sub = oracle.build_fcoo(dims, idx[:, sel], val[sel], oracle.OP_MTTKRP, mode, T)
+        assert np.array_equal(f.perm[s0:e0], sel[sub.perm])
+        assert np.array_equal(bits[s0:e0], sub.bf_bits())
+        assert np.array_equal(f.pidx[:, s0:e0], sub.pidx)
+        assert np.array_equal(f.val[s0:e0].view(np.uint32), sub.val.view(np.uint32))
+        # packed word: (outer - b*BR) << IB | last  (order 2: the local outer index alone)
+        loc = idx[outer][f.perm[s0:e0]].astype(np.int64) - b * BR
+        assert np.all((loc >= 0) & (loc < BR))
+        want = (loc << f.IB) | idx[last][f.perm[s0:e0]] if order > 2 else loc
+        assert np.array_equal(f.pk[s0:e0].astype(np.int64), want)
+    # tile flags and segment tables follow from bf exactly as in the unblocked build
+    ntiles = f.nstream // T
+    for t in range(ntiles):
+        assert ((int(f.sf[t >> 5]) >> (t & 31)) & 1) == bits[t * T]
+        assert f.seg_base[t] == bits[: t * T].sum()
+    hp = np.nonzero(bits)[0]
+    assert hp.size == f.nsegs
+    assert np.array_equal(f.seg_coord[:, 0], idx[mode][f.perm[hp]])
+
+
+def test_blocked_single_block_equals_fcoo():
+    """BR >= I_outer and T | nnz: one block, no padding -> exactly the F-COO build."""
+    dims = (13, 11, 17)
+    idx, val = gen.coo(dims, 256, None, 77)
+    for mode in range(3):
+        f = oracle.build_fcoo(dims, idx, val, oracle.OP_MTTKRP, mode, 32)
+        g = oracle.build_fcoo_blocked(dims, idx, val, mode, 32, 64)
+        assert g.nblocks == 1 and g.nstream == 256
+        for a in ("perm", "bf", "sf", "seg_base", "seg_coord", "pidx"):
+            assert np.array_equal(getattr(f, a), getattr(g, a)), a
+        assert np.array_equal(f.val.view(np.uint32), g.val.view(np.uint32))
+
+
+def test_blocked_bruteforce_orderings():
+    """nnz <= 6: the real positions are the unique ordering increasing under (block, key)."""
+    dims = (3, 5, 4)
+    idx, val = gen.coo(dims, 6, None, 9)
+    for mode in range(3):
+        im, pm = oracle.mode_spec(dims, oracle.OP_MTTKRP, mode)
+        BR = 2
+        f = oracle.build_fcoo_blocked(dims, idx, val, mode, 2, BR)
+        real = [int(p) for p in f.perm if p != 0xFFFFFFFF]
+        orders = []
+        for perm in itertools.permutations(range(6)):
+            ks = [(int(idx[pm[0]][q]) // BR,) + tuple(int(idx[m][q]) for m in im + pm) for q in perm]
+            if all(ks[a] < ks[a + 1] for a in range(5)):
+                orders.append(perm)
+        assert len(orders) == 1 and tuple(real) == orders[0]
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_blocked_stream_mttkrp_matches_dense(mode):
+    """Eq.(5) evaluated by walking the blocked stream (segments -> rows, summed over blocks) equals
+    the dense unfolding x Khatri-Rao definition (tests/dense_defs.py)."""
+    import dense_defs
+    dims = (6, 7, 5)
+    R = 3
+    idx, val = gen.coo(dims, 90, None, 31)
+    fs = [np.asarray(f, np.float64) for f in gen.factors(dims, R, 4, signed=True)]
+    f = oracle.build_fcoo_blocked(dims, idx, val, mode, 8, 2)
+    M = np.zeros((dims[mode], R))
+    bits = f.bf_bits()
+    s = -1
+    for p in range(f.nstream):
+        if f.perm[p] == 0xFFFFFFFF:
+            continue
+        if bits[p]:
+            s += 1
+        row = int(f.seg_coord[s, 0])
+        h = float(f.val[p]) * np.ones(R)
+        for a, m in enumerate(f.product_modes):
+            h = h * fs[m][int(f.pidx[a, p])]
+        M[row] += h
+    X = dense_defs.dense_from_coo(dims, idx, val)
+    ref = dense_defs.mttkrp_dense(X, fs, mode)
+    assert np.allclose(M, ref, rtol=1e-12, atol=1e-12)
+
+
+def test_blocked_errors():
+    dims = (4, 4, 4)
+    dup = np.array([[0, 0], [1, 1], [2, 2]], np.uint32)
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.build_fcoo_blocked(dims, dup, np.ones(2, np.float32), 0, 4, 2)
+    assert e.value.code == oracle.ERR_DUPLICATE
+    # the packed word needs ceil(log2 BR) + ceil(log2 I_last) <= 32 bits
+    big = (4, 3, 1 << 30)
+    idx = np.array([[0, 1], [0, 1], [5, 7]], np.uint32)
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.build_fcoo_blocked(big, idx, np.ones(2, np.float32), 0, 4, 8)
+    assert e.value.code == oracle.ERR_ARG

@@ -1,8 +1,13 @@
-"""Run the X1 gather-ceiling microbenchmark on cuda:0 and print JSON lines.
+"""Run the X1 gather-ceiling microbenchmark (tools/gather_ceiling.cu) on cuda:0; one JSON line per cell.
 
-python tools/gather_ceiling.py  ->  rows/s and GB/s of random R-wide fp32 row gathers for table
-sizes from L1-resident to beyond L2, uniform and Zipf(0.5) index laws.
+The on-chip roofline of the SpMTTKRP factor-row gathers as a hardware property (VERDICT r1 item
+1a): rows/clk/SM for random R-wide fp32 row gathers, per access shape (float4 / float2 / float
+lanes), per data path (LDG, texture, shared memory, and their mixes), per table size (L1/smem-
+resident, L2-resident, HBM) and per fraction of active lane-groups.
+
+  python tools/gather_ceiling.py [--quick]
 """
+import argparse
 import ctypes
 import json
 import os
@@ -10,9 +15,8 @@ import subprocess
 import sys
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-ROOT = os.path.dirname(HERE)
-sys.path.insert(0, ROOT)
 LIB = os.path.join(HERE, "libgather.so")
+PATHS = {0: "LDG", 1: "TEX", 2: "LDS", 3: "LDG+TEX", 4: "LDG+LDS", 5: "LDS+TEX", 6: "LDG+LDS+TEX"}
 
 
 def build():
@@ -24,39 +28,47 @@ def build():
 
 
 def main():
-    import numpy as np
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--clock-mhz", type=float, default=1965.0)
+    a = ap.parse_args()
     import torch
-
-    import gen
     L = ctypes.CDLL(build())
-    L.gather_bench.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.c_int, ctypes.c_void_p,
-                               ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_float)]
-    n = 64 * 1024 * 1024
-    out = torch.zeros(1 << 20, device="cuda")
+    L.gather_bench2.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                ctypes.c_uint32, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+                                ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_float),
+                                ctypes.POINTER(ctypes.c_double)]
+    nsm = torch.cuda.get_device_properties(0).multi_processor_count
+    out = torch.zeros(1 << 22, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
-    for R in (16, 32, 64):
-        for rows in (256, 1024, 4096, 16384, 65536, 262144, 1048576, 4194304):
-            if rows * R * 4 > 2 << 30:
-                continue
-            table = torch.rand(rows, R, device="cuda")
-            for law, alpha in (("uniform", 0.0), ("zipf0.5", 0.5)):
-                if law == "uniform":
-                    idx = torch.randint(0, rows, (n,), device="cuda", dtype=torch.int32)
-                else:
-                    # Zipf(alpha) ranks by inverse CDF on the device, then a random relabelling
-                    p = torch.arange(1, rows + 1, dtype=torch.float64, device="cuda") ** -alpha
-                    c = torch.cumsum(p, 0) / p.sum()
-                    u = torch.rand(n, dtype=torch.float64, device="cuda")
-                    r = torch.clamp(torch.searchsorted(c, u), max=rows - 1)
-                    perm = torch.randperm(rows, device="cuda")
-                    idx = perm[r].to(torch.int32).contiguous()
-                ms = ctypes.c_float(0)
-                rc = L.gather_bench(table.data_ptr(), idx.data_ptr(), n, R, out.data_ptr(), s, 5, ctypes.byref(ms))
-                t = ms.value / 1e3
-                print(json.dumps({"R": R, "rows": rows, "table_MB": rows * R * 4 / 1e6, "law": law,
-                                  "grows_per_s": n / t / 1e9, "gather_TBps": n * R * 4 / t / 1e12, "rc": rc}),
-                      flush=True)
-                del idx
+
+    def cell(R, rows, vec, path, act4=4, srows=0, bps=4, steps=400):
+        table = torch.rand(rows, R, device="cuda")
+        ms, nr = ctypes.c_float(0), ctypes.c_double(0)
+        rc = L.gather_bench2(table.data_ptr(), rows, R, vec, path, srows, act4, bps, steps, out.data_ptr(), s, 5,
+                             ctypes.byref(ms), ctypes.byref(nr))
+        t = ms.value / 1e3
+        rps = nr.value / t
+        line = {"R": R, "rows": rows, "table_MB": rows * R * 4 / 1e6, "lanes_per_row": R // vec, "vec": vec,
+                "path": PATHS[path], "smem_rows": srows, "active_groups": act4 / 4, "ctas_per_sm": bps,
+                "grows_per_s": rps / 1e9, "rows_per_clk_sm": rps / (nsm * a.clock_mhz * 1e6),
+                "bytes_per_clk_sm": rps * R * 4 / (nsm * a.clock_mhz * 1e6), "rc": rc}
+        print(json.dumps(line), flush=True)
+
+    Rs = (32,) if a.quick else (16, 32, 64)
+    for R in Rs:
+        srows = 12288 // R  # 48 KB of shared memory: 4 CTAs/SM
+        for rows in ((srows, 9184, 28818) if a.quick else (srows, 9184, 28818, 480189)):
+            for vec in (4, 2, 1):
+                if R // vec > 32:
+                    continue
+                cell(R, rows, vec, 0)
+        for path in (1, 2, 3, 4, 5, 6):
+            for rows in (srows, 28818):
+                cell(R, rows, 4, path, srows=srows if path in (2, 4, 5, 6) else 0, bps=4)
+        for act4 in (1, 2, 3):
+            cell(R, 28818, 4, 0, act4=act4)
+            cell(R, srows, 4, 2, act4=act4, srows=srows, bps=4)
 
 
 if __name__ == "__main__":
