@@ -39,6 +39,10 @@ def parse():
     ap.add_argument("--workload", default="nell2")
     ap.add_argument("--R", type=int, default=32)
     ap.add_argument("--tile", type=int, default=0, help="tile_nnz; 0 = the library's automatic choice")
+    ap.add_argument("--layout", default="blocked", choices=["blocked", "fcoo"],
+                    help="blocked: FCOO_BUILD_BLOCKED (outer factor block in shared memory, DESIGN.md §5); "
+                         "fcoo: the plain F-COO of the paper")
+    ap.add_argument("--block-rows", type=int, default=0, help="block_rows for --layout blocked (0 = default)")
     ap.add_argument("--nnz", type=int, default=None, help="override nnz (debug only; not a bench number)")
     ap.add_argument("--fused-combine", action="store_true",
                     help="N > 1: combine the ranks' partial outputs in the MTTKRP epilogue through an NVLS "
@@ -123,6 +127,17 @@ class ClockSampler:
         return bool(self.reasons & self.BAD)
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cpu_oracle_baseline(dims, idx, val, R, budget_s=12.0):
     """The oracle as it stands (oracle.mttkrp, fp64, OpenMP over os.cpu_count() threads) on a
     bounded prefix sample of the same workload, every mode.  Returns a cpu_baseline dict."""
@@ -145,7 +160,7 @@ def cpu_oracle_baseline(dims, idx, val, R, budget_s=12.0):
         oracle.mttkrp(dims, si, sv, mode, fs, with_D=False, nthreads=cores)
         t += time.perf_counter() - t0
     flops = len(dims) * R * s * len(dims)
-    return {"value": flops / t / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle",
+    return {"value": flops / t / 1e9, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
             "sample": f"first {s} of {nnz} nonzeros (draw order), SpMTTKRP every mode, R={R}, fp64, "
                       f"{cores} OpenMP threads, {t:.2f} s"}
 
@@ -195,7 +210,8 @@ def run_reference(a):
         "dtype": "f64", "data": "synthetic", "impl": "reference",
         "config": {"workload": f"{w.name}-shaped {'x'.join(map(str, w.dims))}, {nnz} nnz, alpha {list(w.alpha)}",
                    "R": R, "modes": list(range(N))},
-        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": v, "unit": "GFLOP/s", "cores": cores, "kind": "oracle", "cpu_model": cpu_model(),
+                         "sample": sample},
         "e2e": {"value": v, "unit": "GFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }))
     return 0
@@ -231,11 +247,13 @@ def main():
     torch.cuda.synchronize()
 
     comm = P.comm_from_process_group() if world > 1 else None
-    P.fcoo_build(coo, 0, tile_nnz=T).destroy()  # warm-up: module load, allocator, CUB tuning
+    blocked = a.layout == "blocked"
+    bkw = dict(blocked=blocked, block_rows=a.block_rows) if blocked else {}
+    P.fcoo_build(coo, 0, tile_nnz=T, **bkw).destroy()  # warm-up: module load, allocator, CUB tuning
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     # N > 1: fcoo_build_sharded = the redundant build + this rank's tile-aligned slice
-    H = [P.fcoo_build_sharded(coo, n, comm, tile_nnz=T) if world > 1 else P.fcoo_build(coo, n, tile_nnz=T)
+    H = [P.fcoo_build_sharded(coo, n, comm, tile_nnz=T, **bkw) if world > 1 else P.fcoo_build(coo, n, tile_nnz=T, **bkw)
          for n in range(N)]
     T = H[0].info.tile_nnz  # the tile actually used (0 = automatic)
     torch.cuda.synchronize()
@@ -310,38 +328,50 @@ def main():
     value = flops_step * a.steps / (ms / 1e3) / 1e9
     peak, peak_src = hbm_peak()
     bytes_modes = [compulsory_bytes(dims, nnz, n, R, T) for n in range(N)]
-    # dominant kernel: the MTTKRP segmented reduction; per-launch algorithmic bytes / launch time
+    # dominant kernel: the MTTKRP segmented reduction; per-launch algorithmic bytes / launch time.
+    # N > 1: the N ranks move the whole job's bytes in the max-rank time, against N GPUs' HBM
     achieved = sum(bytes_modes) / (sum(per_mode_ms) / 1e3) / 1e9
-    if world > 1:  # per rank, a launch moves its shard of the stream plus the factors/outputs
-        achieved = achieved  # reported on the whole-job bytes over the max-rank time
+    peak_job = peak * world
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tpath):
         try:
             tj = json.load(open(tpath))
-            key = f"{a.workload}/R{R}/T{T}"
+            key = f"{a.workload}/R{R}/T{T}" + ("/blocked" if blocked else "")
             if key in tj:
                 traffic = tj[key]
         except Exception:
             pass
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "traffic": traffic, "peak_source": peak_src, "kernel": "k_segreduce_staged (fcoo_mttkrp)",
-                "bytes_per_launch": {f"mode{n}": int(b) for n, b in enumerate(bytes_modes)}}
-    # the binding on-chip ceiling: random R-wide factor-row gathers from L2, measured
-    # by tools/gather_ceiling.py (profiles/round1/gather_ceiling.jsonl)
+    kname = "k_mttkrp_blocked (fcoo_mttkrp, blocked layout)" if blocked else "k_segreduce_staged (fcoo_mttkrp)"
+    roofline = {"bound": "hbm", "achieved": achieved, "peak": peak_job, "unit": "GB/s", "frac": achieved / peak_job,
+                "traffic": traffic, "peak_source": peak_src + (f" x {world} GPUs" if world > 1 else ""),
+                "kernel": kname, "bytes_per_launch": {f"mode{n}": int(b) for n, b in enumerate(bytes_modes)},
+                "bytes_definition": "SURVEY §8(d): Table II F-COO stream + each factor once + output once"}
+    if world > 1:
+        roofline["per_rank_frac"] = achieved / world / peak
+    if blocked:  # what the blocked stream actually holds (packed words + values + bf + sf)
+        roofline["stream_bytes_per_launch"] = {f"mode{n}": int(H[n].info.nstream * (4 * H[n].info.n_words + 4)
+                                                                + H[n].info.nstream // 8) for n in range(N)}
+    # the binding on-chip ceiling: the L1TEX data pipe that row gathers go through,
+    # measured as a hardware property by tools/gather_ceiling.py (profiles/round2/gather_ceiling_
+    # shapes.jsonl): random R-wide rows, float4 lanes, L2-resident table; the blocked kernel reads
+    # one row per nonzero from shared memory and N-2 from L2 (path LDG+LDS), the plain F-COO
+    # kernel N-1 from L2 (path LDG)
     gceil = None
     try:
-        rows = [json.loads(l) for l in open(os.path.join(ROOT, "profiles", "round1", "gather_ceiling.jsonl"))
+        rows = [json.loads(l) for l in open(os.path.join(ROOT, "profiles", "round2", "gather_ceiling_shapes.jsonl"))
                 if l.startswith("{")]
-        cands = [r["grows_per_s"] for r in rows if r["R"] == R and 1.0 <= r["table_MB"] <= 70.0]
+        want = "LDG+LDS" if blocked and N == 3 else "LDG"
+        cands = [r["grows_per_s"] for r in rows if r["R"] == R and r["path"] == want and r["rows"] >= 9184
+                 and r["active_groups"] == 1.0 and r["lanes_per_row"] == R // 4]
         gceil = max(cands) if cands else None
     except Exception:
         pass
     rows_per_s = nnz * (N - 1) * N / (sum(per_mode_ms) / 1e3) / 1e9
-    result_gather = {"bound": "l2_gather", "achieved": rows_per_s, "peak": gceil, "unit": "G rows/s",
+    result_gather = {"bound": "l1tex_gather", "achieved": rows_per_s, "peak": gceil, "unit": "G rows/s",
                      "frac": (rows_per_s / gceil) if gceil else None,
-                     "note": "(N-1) factor-row gathers per nonzero; peak = best L2-resident random-row gather "
-                             "rate measured by tools/gather_ceiling.py at this R"}
+                     "note": "(N-1) factor rows per nonzero; peak = random-row rate of the same access mix "
+                             "measured by tools/gather_ceiling.py at this R (L2-resident table)"}
 
     result = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": a.steps,
@@ -349,7 +379,8 @@ def main():
         "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{w.name}-shaped {'x'.join(map(str, dims))}, {nnz} nnz, Zipf alpha {list(w.alpha)}, "
                                f"seed {w.seed}",
-                   "R": R, "modes": list(range(N)), "tile_nnz": T,
+                   "R": R, "modes": list(range(N)), "tile_nnz": T, "layout": a.layout,
+                   "block_rows": H[0].info.block_rows if blocked else None,
                    "parallelism": (f"nnz-sharded x{world}, factors replicated, "
                                    + ("combine fused into the MTTKRP epilogue (NVLS multicast)" if mc is not None
                                       else "NCCL all-reduce per mode")) if world > 1
@@ -358,7 +389,7 @@ def main():
                          % (bytes_modes[0] / 1e9)},
         "nnz_per_s": nnz * N * a.steps / (ms / 1e3),
         "per_mode_ms": [float(x) for x in per_mode_ms],
-        "per_mode_hbm_frac": [float(b / (t / 1e3) / 1e9 / peak) for b, t in zip(bytes_modes, per_mode_ms)],
+        "per_mode_hbm_frac": [float(b / (t / 1e3) / 1e9 / peak_job) for b, t in zip(bytes_modes, per_mode_ms)],
         "roofline": roofline, "roofline_gather": result_gather, "gpu_launches": int(launches),
         "clocks": clk.summary(), "build_ms_all_modes": build_ms,
     }
@@ -387,7 +418,7 @@ def main():
                     t = float(tt.item())
                 b = compulsory_bytes(dims, nnz, n, Rs, T)
                 sweep.append({"R": Rs, "mode": n, "ms": t, "gflops": N * Rs * nnz / (t / 1e3) / 1e9,
-                              "hbm_frac": b / (t / 1e3) / 1e9 / peak})
+                              "hbm_frac": b / (t / 1e3) / 1e9 / peak_job})
         result["per_mode"] = sweep
 
     def timed_host(step, steps):
@@ -466,8 +497,8 @@ def main():
             val_d = val_h.to(dev, non_blocking=True)
             fd = [f.to(dev, non_blocking=True) for f in f_h]
             c = P.Coo(dims, idx_d, val_d)
-            hs = [P.fcoo_build_sharded(c, n, comm, tile_nnz=T, stream=stream) if world > 1
-                  else P.fcoo_build(c, n, tile_nnz=T, stream=stream) for n in range(N)]
+            hs = [P.fcoo_build_sharded(c, n, comm, tile_nnz=T, stream=stream, **bkw) if world > 1
+                  else P.fcoo_build(c, n, tile_nnz=T, stream=stream, **bkw) for n in range(N)]
             for n in range(N):
                 P.fcoo_mttkrp(hs[n], fd, R, outs[n], stream)
                 o_h[n].copy_(outs[n], non_blocking=True)

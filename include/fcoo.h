@@ -81,6 +81,20 @@ typedef struct {
  * Same sum, a fixed association: repeated calls give identical bits.  SpTTMc and the CP-ALS
  * fit-mode fp64 pass keep red.add. */
 #define FCOO_BUILD_DETERMINISTIC 4u
+/* Blocked F-COO (FCOO_OP_MTTKRP only, reading Q22): the stream is the concatenation,
+ * over b = 0, 1, ..., of the F-COO of the sub-tensor X_b = {nonzeros with floor(i_outer / BR) == b},
+ * "outer" = the first product mode of reading Q5 (smallest extent), BR = block_rows; each block is
+ * padded with empty positions to a multiple of T, so every tile belongs to one block.  Eq.(6) is
+ * linear in X, so MTTKRP(X) = sum_b MTTKRP(X_b): the SpMTTKRP kernel keeps block b's BR outer
+ * factor rows in shared memory (one TMA bulk copy per CTA) and gathers only the other product
+ * modes from L2; every segment flush is a red.global.add (a row recurs once per block).
+ * Per nonzero the stream holds ONE packed word (i_outer - b*BR) << IB | i_last (IB =
+ * ceil(log2 I_last), "last" = last product mode of Q5; order 2: the local outer index alone),
+ * plus, for order >= 4, the global index of each middle product mode: 8 B/nnz + flags for a
+ * 3-order tensor instead of Table II's 12.  Requires 2 <= order <= 5 and ceil(log2 BR) + IB <= 32
+ * (else FCOO_ERR_ARG); incompatible with DETERMINISTIC and PRODUCT_DESC (ARG); fcoo_ttmc rejects
+ * blocked handles (SHAPE).  The build synchronises the host twice (block sizes, then errors). */
+#define FCOO_BUILD_BLOCKED 8u
 
 /* Build options.  NULL -> {FCOO_OP_MTTKRP, 0 (automatic), 0}.
  * tile_nnz = T, the partition length ("threadlen", P:L272 / P:L426): a multiple of 32 in
@@ -91,6 +105,7 @@ typedef struct {
   int op;          /* fcoo_op */
   int tile_nnz;    /* T */
   unsigned flags;  /* FCOO_BUILD_* */
+  int block_rows;  /* BR for FCOO_BUILD_BLOCKED: 0 = 512; otherwise in [32, 65536] (ignored without the flag) */
 } fcoo_build_opts;
 
 typedef struct fcoo_s* fcoo_t;
@@ -165,15 +180,25 @@ typedef struct {
   int64_t device_bytes;    /* everything the handle holds on the device (with padding) */
   int shard, nshards;      /* tile range in use: [tile_begin, tile_end) */
   int64_t tile_begin, tile_end;
+  int blocked;             /* built with FCOO_BUILD_BLOCKED */
+  int block_rows;          /* BR (blocked handles; 0 otherwise) */
+  int64_t nblocks;         /* ceil(I_outer / BR) (blocked handles; 0 otherwise) */
+  int64_t nstream;         /* stream positions (blocked: nnz + padding = ntiles * tile_nnz; else nnz) */
+  int pk_shift;            /* IB of the packed word (blocked handles) */
+  int n_words;             /* packed words per nonzero (blocked handles: 1 + max(0, n_prod - 2)) */
 } fcoo_info_t;
 
 /* fcoo_info — host-side metadata; no device work. */
 fcoo_status fcoo_info(fcoo_t f, fcoo_info_t* info);
 
 /* Host view for fcoo_export: each non-NULL pointer receives a copy (host memory, caller-owned).
- * Sizes: perm u32[nnz] (only with FCOO_BUILD_KEEP_PERM), bf u8[ceil(nnz/8)] (LSB-first, pad 0),
- * sf u32[ceil(ntiles/32)], seg_base u32[ntiles], seg_coord u32[nsegs*n_idx],
- * pidx u32[n_prod*nnz] (product modes in prod_modes order), val f32[nnz]. */
+ * Sizes (S = fcoo_info nstream: nnz, or nnz + padding for a blocked handle):
+ * perm u32[S] (only with FCOO_BUILD_KEEP_PERM; 0xFFFFFFFF at padding), bf u8[ceil(S/8)]
+ * (LSB-first, pad 0), sf u32[ceil(ntiles/32)], seg_base u32[ntiles], seg_coord u32[nsegs*n_idx],
+ * pidx u32[n_prod*S] (product modes in prod_modes order, GLOBAL indices; a blocked handle's packed
+ * words are decoded on the device; 0 at padding), val f32[S] (0 at padding);
+ * blocked handles only: pk u32[n_words*S] (the packed words as stored), blk_start i64[nblocks+1]
+ * (first stream position of each block; last = S), blk_end i64[nblocks] (end of its nonzeros). */
 typedef struct {
   uint32_t* perm;
   uint8_t* bf;
@@ -182,6 +207,9 @@ typedef struct {
   uint32_t* seg_coord;
   uint32_t* pidx;
   float* val;
+  uint32_t* pk;
+  int64_t* blk_start;
+  int64_t* blk_end;
 } fcoo_host_view;
 
 /* fcoo_export — copy the handle's arrays to host buffers; synchronises `stream`. */

@@ -19,7 +19,7 @@ EXTRA = os.environ.get("FCOO_NVCC_EXTRA", "").split()
 LIB = os.path.join(PKG, f"libfcoo_{TAG}.so" if TAG else "libfcoo.so")
 OBJ = os.path.join(PKG, f"build_{TAG}" if TAG else "build")
 SOURCES = ["fcoo_api.cu", "fcoo_build.cu", "fcoo_engine.cu", "fcoo_cp.cu", "fcoo_comm.cu", "fcoo_ttmc.cu", "fcoo_tns.cpp"] + [
-    f"fcoo_engine_np{k}.cu" for k in range(1, 8)]
+    f"fcoo_engine_np{k}.cu" for k in range(1, 8)] + [f"fcoo_blocked_np{k}_{a}.cu" for k in range(1, 5) for a in ("f32", "f64")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -37,11 +37,27 @@ def _flags():
                    ] + EXTRA
 
 
+def _deps(path: str, seen=None) -> set:
+    """The source and every in-tree header it includes, transitively (#include "...")."""
+    import re
+    seen = set() if seen is None else seen
+    if path in seen or not os.path.exists(path):
+        return seen
+    seen.add(path)
+    with open(path) as f:
+        for m in re.finditer(r'^\s*#\s*include\s+"([^"]+)"', f.read(), re.M):
+            for d in (os.path.dirname(path), CSRC, os.path.join(ROOT, "include")):
+                h = os.path.join(d, m.group(1))
+                if os.path.exists(h):
+                    _deps(h, seen)
+                    break
+    return seen
+
+
 def _compile(src: str) -> str:
     obj = os.path.join(OBJ, os.path.splitext(src)[0] + ".o")
     path = os.path.join(CSRC, src)
-    deps = [path, os.path.join(ROOT, "include", "fcoo.h")] + [
-        os.path.join(CSRC, h) for h in os.listdir(CSRC) if h.endswith(".cuh")]
+    deps = sorted(_deps(path))
     if os.path.exists(obj) and os.path.getmtime(obj) >= max(os.path.getmtime(d) for d in deps):
         return obj
     cmd = [NVCC] + _flags() + ["-c", path, "-o", obj]

@@ -48,6 +48,28 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
                        cudaStream_t s, fcoo_t* out);
 void destroy_impl(fcoo_s* f);
 
+// fcoo_export of a blocked handle: decode the packed words into global product indices
+// (outer = local + b*BR, last = low bits, middles as stored); padding positions give 0.
+__global__ void k_unpack_blocked(const uint32_t* __restrict__ pk, const int64_t* __restrict__ blk_start,
+                                 const int64_t* __restrict__ blk_end, int64_t nblocks, int64_t ns, int n_prod,
+                                 int shift, int BR, uint32_t* __restrict__ pidx) {
+  const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= ns) return;
+  int64_t lo = 0, hi = nblocks;  // blk_start[lo] <= q < blk_start[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (blk_start[mid] <= q) lo = mid; else hi = mid;
+  }
+  const bool live = q < blk_end[lo];
+  const uint32_t w0 = pk[q];
+  const uint32_t local = n_prod >= 2 ? (w0 >> shift) : w0;
+  pidx[q] = live ? local + (uint32_t)(lo * BR) : 0u;
+  if (n_prod >= 2) {
+    for (int a = 1; a + 1 < n_prod; ++a) pidx[(int64_t)a * ns + q] = live ? pk[(int64_t)a * ns + q] : 0u;
+    pidx[(int64_t)(n_prod - 1) * ns + q] = live ? (w0 & ((1u << shift) - 1u)) : 0u;
+  }
+}
+
 }  // namespace fcoo
 
 extern "C" {
@@ -125,6 +147,7 @@ fcoo_status fcoo_ttm(fcoo_t f, const float* U, int R, float* out, void* stream) 
 fcoo_status fcoo_ttmc(fcoo_t f, const float* const* factors, const int* ranks, float* out, void* stream) {
   if (!f || !factors || !ranks || !out) return fcoo::fail(FCOO_ERR_ARG, "NULL handle/factors/ranks/out");
   if (f->op != FCOO_OP_MTTKRP) return fcoo::fail(FCOO_ERR_SHAPE, "SpTTMc needs a handle built for FCOO_OP_MTTKRP");
+  if (f->blocked) return fcoo::fail(FCOO_ERR_SHAPE, "SpTTMc needs an unblocked handle (built without FCOO_BUILD_BLOCKED)");
   return fcoo::run_ttmc(f, factors, ranks, out, (cudaStream_t)stream);
 }
 
@@ -146,12 +169,47 @@ fcoo_status fcoo_info(fcoo_t f, fcoo_info_t* info) {
                                  f->bytes_seg_coord + f->bytes_perm);
   info->shard = f->shard; info->nshards = f->nshards;
   info->tile_begin = f->tile_begin; info->tile_end = f->tile_end;
+  info->blocked = f->blocked;
+  info->block_rows = f->blocked ? f->block_rows : 0;
+  info->nblocks = f->blocked ? f->nblocks : 0;
+  info->nstream = f->blocked ? f->nnz_pad : f->nnz;
+  info->pk_shift = f->pk_shift;
+  info->n_words = f->n_words;
+  if (f->blocked)  // packed words + values + bf over the padded stream, block tables
+    info->device_bytes += (int64_t)f->bytes_blk;
   return FCOO_OK;
 }
 
 fcoo_status fcoo_export(fcoo_t f, fcoo_host_view* v, void* stream) {
   if (!f || !v) return fcoo::fail(FCOO_ERR_ARG, "NULL handle/view");
   cudaStream_t s = (cudaStream_t)stream;
+  if (f->blocked) {
+    const int64_t ns = f->nnz_pad;
+    if (v->perm) {
+      if (!f->perm) return fcoo::fail(FCOO_ERR_ARG, "perm requested but the handle was built without KEEP_PERM");
+      FCOO_CUDA_TRY(cudaMemcpyAsync(v->perm, f->perm, 4 * ns, cudaMemcpyDeviceToHost, s));
+    }
+    if (v->bf) FCOO_CUDA_TRY(cudaMemcpyAsync(v->bf, f->bf, (ns + 7) / 8, cudaMemcpyDeviceToHost, s));
+    if (v->sf) FCOO_CUDA_TRY(cudaMemcpyAsync(v->sf, f->sf, 4 * ((f->ntiles + 31) / 32), cudaMemcpyDeviceToHost, s));
+    if (v->seg_base) FCOO_CUDA_TRY(cudaMemcpyAsync(v->seg_base, f->seg_base, 4 * f->ntiles, cudaMemcpyDeviceToHost, s));
+    if (v->seg_coord && f->nsegs > 0)
+      FCOO_CUDA_TRY(cudaMemcpyAsync(v->seg_coord, f->seg_coord, 4 * f->nsegs * f->n_idx, cudaMemcpyDeviceToHost, s));
+    if (v->val) FCOO_CUDA_TRY(cudaMemcpyAsync(v->val, f->val, 4 * ns, cudaMemcpyDeviceToHost, s));
+    if (v->pk) FCOO_CUDA_TRY(cudaMemcpyAsync(v->pk, f->pidx, 4 * ns * f->n_words, cudaMemcpyDeviceToHost, s));
+    if (v->blk_start) memcpy(v->blk_start, f->h_blk_start.data(), sizeof(int64_t) * (f->nblocks + 1));
+    if (v->blk_end) memcpy(v->blk_end, f->h_blk_end.data(), sizeof(int64_t) * f->nblocks);
+    if (v->pidx) {
+      fcoo::Buf tmp(&f->alloc, sizeof(uint32_t) * (size_t)(ns * f->n_prod), s);
+      if (!tmp.ok()) return fcoo::fail(FCOO_ERR_OOM, "export scratch");
+      fcoo::k_unpack_blocked<<<(unsigned)((ns + 255) / 256), 256, 0, s>>>(
+          f->pidx, f->blk_start, f->blk_end, f->nblocks, ns, f->n_prod, f->pk_shift, f->block_rows, tmp.as<uint32_t>());
+      FCOO_LAUNCH_CHECK();
+      FCOO_CUDA_TRY(cudaMemcpyAsync(v->pidx, tmp.p, 4 * ns * f->n_prod, cudaMemcpyDeviceToHost, s));
+      FCOO_CUDA_TRY(cudaStreamSynchronize(s));
+    }
+    FCOO_CUDA_TRY(cudaStreamSynchronize(s));
+    return FCOO_OK;
+  }
   const int64_t nnz = f->nnz;
   if (v->perm) {
     if (!f->perm) return fcoo::fail(FCOO_ERR_ARG, "perm requested but the handle was built without KEEP_PERM");

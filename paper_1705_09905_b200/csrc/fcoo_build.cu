@@ -32,6 +32,10 @@ struct KeyLayout {
   uint64_t mask[kMaxOrder];
   int n_idx;
   int prod_bits;              // bits below the index part
+  // blocked layout (BR > 0): block id floor(i_outer / BR) above every coordinate, at blk_shift;
+  // the outer mode is key position n_idx (the first product mode of reading Q5)
+  uint32_t BR;
+  int blk_shift;
 };
 
 struct IdxPtrs {
@@ -56,6 +60,7 @@ __global__ void k_pack_keys(IdxPtrs idx, KeyLayout L, int64_t nnz, const float* 
     }
   }
   if (bad) atomicOr(err, ERRF_INDEX_RANGE);
+  if (L.BR) key |= (K)(idx.p[L.n_idx][q] / L.BR) << L.blk_shift;
   keys[q] = key;
   ord[q] = val_in ? __float_as_uint(val_in[q]) : (uint32_t)q;
 }
@@ -136,6 +141,98 @@ __global__ void k_seg_coord(const K* __restrict__ keys, const uint32_t* __restri
   for (int a = 0; a < L.n_idx; ++a) seg_coord[(int64_t)s * L.n_idx + a] = (uint32_t)((key >> L.shift[a]) & L.mask[a]);
 }
 
+// ---- blocked layout (FCOO_BUILD_BLOCKED) ----
+// start[b] = first sorted position whose block id is >= b (start[nblocks] = nnz): thread p writes
+// start[b] for every b in (block(p-1), block(p)], so each entry is written exactly once.
+template <class K>
+__global__ void k_blk_bounds(const K* __restrict__ keys, int64_t nnz, int blk_shift, int64_t nblocks,
+                             int64_t* __restrict__ start) {
+  int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > nnz) return;
+  const int64_t bp = p < nnz ? (int64_t)(keys[p] >> blk_shift) : nblocks;
+  const int64_t bq = p > 0 ? (int64_t)(keys[p - 1] >> blk_shift) : -1;
+  for (int64_t b = bq + 1; b <= bp; ++b) start[b] = p;
+}
+
+// qmap[q] = sorted position of stream position q, or 0xffffffff for padding (binary search of the
+// block of q in pstart[0..nblocks]).
+__global__ void k_blk_qmap(const int64_t* __restrict__ pstart, const int64_t* __restrict__ start, int64_t nblocks,
+                           int64_t nstream, uint32_t* __restrict__ qmap) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nstream) return;
+  int64_t lo = 0, hi = nblocks;  // pstart[lo] <= q < pstart[hi]
+  while (hi - lo > 1) {
+    const int64_t mid = (lo + hi) >> 1;
+    if (pstart[mid] <= q) lo = mid; else hi = mid;
+  }
+  const int64_t r = q - pstart[lo];
+  qmap[q] = r < start[lo + 1] - start[lo] ? (uint32_t)(start[lo] + r) : 0xffffffffu;
+}
+
+// One thread per stream position q (nstream % 32 == 0: whole warps): packed words, values, bf,
+// per-word head counts, perm; a head is a real position whose (block, index tuple) differs from
+// the previous sorted key (the block id sits above the index part of the key).
+template <class K>
+__global__ void k_flags_blocked(const K* __restrict__ keys, const uint32_t* __restrict__ ord,
+                                const float* __restrict__ val_in, KeyLayout L, int n_prod, int pk_shift,
+                                const uint32_t* __restrict__ qmap, int64_t nstream, uint32_t* __restrict__ pk,
+                                float* __restrict__ val, uint32_t* __restrict__ bf, uint32_t* __restrict__ wcount,
+                                uint32_t* __restrict__ perm, uint32_t* __restrict__ err) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nstream) return;
+  const uint32_t p = qmap[q];
+  const bool live = p != 0xffffffffu;
+  const int n_words = n_prod >= 2 ? n_prod - 1 : 1;
+  bool head = false;
+  if (live) {
+    const K key = keys[p];
+    if (p == 0) {
+      head = true;
+    } else {
+      const K prev = keys[p - 1];
+      head = index_part(key, L.prod_bits) != index_part(prev, L.prod_bits);
+      if (key == prev) atomicOr(err, ERRF_DUPLICATE);
+    }
+    const int ko = L.n_idx, kl = L.n_idx + n_prod - 1;
+    const uint32_t b = (uint32_t)(key >> L.blk_shift);
+    const uint32_t local = (uint32_t)((key >> L.shift[ko]) & L.mask[ko]) - b * L.BR;
+    const uint32_t last = (uint32_t)((key >> L.shift[kl]) & L.mask[kl]);
+    pk[q] = n_prod >= 2 ? (local << pk_shift) | last : local;
+    for (int a = 1; a + 1 < n_prod; ++a)
+      pk[(int64_t)a * nstream + q] = (uint32_t)((key >> L.shift[ko + a]) & L.mask[ko + a]);
+    const uint32_t o = ord[p];
+    if (perm) {
+      val[q] = val_in[o];
+      perm[q] = o;
+    } else {
+      val[q] = __uint_as_float(o);
+    }
+  } else {
+    for (int a = 0; a < n_words; ++a) pk[(int64_t)a * nstream + q] = 0u;
+    val[q] = 0.0f;
+    if (perm) perm[q] = 0xffffffffu;
+  }
+  const uint32_t word = __ballot_sync(0xffffffffu, head);
+  if ((threadIdx.x & 31) == 0) {
+    bf[q >> 5] = word;
+    wcount[q >> 5] = __popc(word);
+  }
+}
+
+template <class K>
+__global__ void k_seg_coord_blocked(const K* __restrict__ keys, const uint32_t* __restrict__ qmap,
+                                    const uint32_t* __restrict__ bf, const uint32_t* __restrict__ wbase, KeyLayout L,
+                                    int64_t nstream, uint32_t* __restrict__ seg_coord) {
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nstream) return;
+  const uint32_t word = bf[q >> 5];
+  const int b = (int)(q & 31);
+  if (!((word >> b) & 1u)) return;
+  const uint32_t s = wbase[q >> 5] + __popc(word & ((1u << b) - 1u));
+  const K key = keys[qmap[q]];
+  for (int a = 0; a < L.n_idx; ++a) seg_coord[(int64_t)s * L.n_idx + a] = (uint32_t)((key >> L.shift[a]) & L.mask[a]);
+}
+
 int bits_for(int64_t n) {
   int b = 0;
   while (b < 63 && ((int64_t)1 << b) < n) ++b;
@@ -157,6 +254,11 @@ void free_handle_arrays(fcoo_s* f) {
   if (f->seg_base) f->alloc.put(f->seg_base, f->bytes_seg_base, s);
   if (f->seg_coord) f->alloc.put(f->seg_coord, f->bytes_seg_coord, s);
   if (f->perm) f->alloc.put(f->perm, f->bytes_perm, s);
+  if (f->blk_start) f->alloc.put(f->blk_start, f->bytes_blk, s);
+  for (int k = 0; k < 10; ++k)
+    if (f->items[k]) f->alloc.put(f->items[k], sizeof(int2) * f->h_items[k].size(), s);
+  for (int k = 0; k < 10; ++k) f->items[k] = nullptr;
+  f->blk_start = nullptr; f->blk_end = nullptr;
   f->pidx = nullptr; f->val = nullptr; f->bf = nullptr; f->sf = nullptr;
   f->seg_base = nullptr; f->seg_coord = nullptr; f->perm = nullptr;
 }
@@ -286,6 +388,150 @@ fcoo_status sort_and_flag(fcoo_s* f, const fcoo_coo* coo, const KeyLayout& L, co
   return FCOO_OK;
 }
 
+// Work tables of the blocked SpMTTKRP: for gpc = 1 << k, one item (b, t0) per run of up to gpc
+// consecutive tiles of block b (every tile of a blocked stream lies in exactly one block).
+static fcoo_status make_items(fcoo_s* f, cudaStream_t s) {
+  for (int k = 3; k < 10; ++k) {
+    const int64_t gpc = (int64_t)1 << k;
+    std::vector<int2>& v = f->h_items[k];
+    v.clear();
+    for (int64_t b = 0; b < f->nblocks; ++b)
+      for (int64_t t = f->h_blk_start[b] / f->T; t < f->h_blk_start[b + 1] / f->T; t += gpc)
+        v.push_back(make_int2((int)b, (int)t));
+    if (v.empty()) continue;
+    f->items[k] = reinterpret_cast<int2*>(f->alloc.get(sizeof(int2) * v.size(), s));
+    if (!f->items[k]) return fail(FCOO_ERR_OOM, "work table allocation");
+    FCOO_CUDA_TRY(cudaMemcpyAsync(f->items[k], v.data(), sizeof(int2) * v.size(), cudaMemcpyHostToDevice, s));
+  }
+  return FCOO_OK;
+}
+
+// Blocked build (FCOO_BUILD_BLOCKED): keys carry the block id above every coordinate; after the sort
+// one host sync reads the block boundaries, the stream is laid out with every block padded to a
+// multiple of T, and the flags/segment steps run over the padded stream through qmap.
+template <class K>
+fcoo_status sort_and_flag_blocked(fcoo_s* f, const fcoo_coo* coo, const KeyLayout& L, const IdxPtrs& ip, int total,
+                                  unsigned flags, cudaStream_t s) {
+  const int64_t nnz = f->nnz, T = f->T, nblocks = f->nblocks;
+  Buf keys0(&f->alloc, sizeof(K) * nnz, s), keys1(&f->alloc, sizeof(K) * nnz, s);
+  Buf ord0(&f->alloc, sizeof(uint32_t) * nnz, s), ord1(&f->alloc, sizeof(uint32_t) * nnz, s);
+  Buf errb(&f->alloc, sizeof(uint32_t) * 2, s);
+  Buf startb(&f->alloc, sizeof(int64_t) * (nblocks + 1), s);
+  if (!keys0.ok() || !keys1.ok() || !ord0.ok() || !ord1.ok() || !errb.ok() || !startb.ok())
+    return fail(FCOO_ERR_OOM, "build scratch allocation failed");
+  cudaError_t ce;
+  if ((ce = cudaMemsetAsync(errb.p, 0, sizeof(uint32_t) * 2, s)) != cudaSuccess)
+    return fail(FCOO_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
+  const int TB = 256;
+  const bool keep_perm = (flags & FCOO_BUILD_KEEP_PERM) != 0;
+  k_pack_keys<<<(unsigned)((nnz + TB - 1) / TB), TB, 0, s>>>(ip, L, nnz, keep_perm ? nullptr : coo->val,
+                                                             keys0.as<K>(), ord0.as<uint32_t>(), errb.as<uint32_t>());
+  count_launch();
+  if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_pack_keys: %s", cudaGetErrorString(ce));
+  cub::DoubleBuffer<K> dk(keys0.as<K>(), keys1.as<K>());
+  cub::DoubleBuffer<uint32_t> dv(ord0.as<uint32_t>(), ord1.as<uint32_t>());
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, (int64_t)nnz, 0, total, s);
+  {
+    Buf cubtmp(&f->alloc, tmp_bytes, s);
+    if (!cubtmp.ok()) return fail(FCOO_ERR_OOM, "radix sort scratch");
+    if ((ce = cub::DeviceRadixSort::SortPairs(cubtmp.p, tmp_bytes, dk, dv, (int64_t)nnz, 0, total, s)) != cudaSuccess)
+      return fail(FCOO_ERR_CUDA, "radix sort: %s", cudaGetErrorString(ce));
+    count_launch(2 + (total + 7) / 8);
+  }
+  const K* keys = dk.Current();
+  const uint32_t* ord = dv.Current();
+  k_blk_bounds<K><<<(unsigned)((nnz + 1 + TB - 1) / TB), TB, 0, s>>>(keys, nnz, L.blk_shift, nblocks,
+                                                                      startb.as<int64_t>());
+  count_launch();
+  if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_blk_bounds: %s", cudaGetErrorString(ce));
+  // host sync 1 of 2: block boundaries and the index-range flag
+  std::vector<int64_t> start(nblocks + 1);
+  uint32_t err0 = 0;
+  if ((ce = cudaMemcpyAsync(start.data(), startb.p, sizeof(int64_t) * (nblocks + 1), cudaMemcpyDeviceToHost, s)) !=
+          cudaSuccess ||
+      (ce = cudaMemcpyAsync(&err0, errb.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+      (ce = cudaStreamSynchronize(s)) != cudaSuccess)
+    return fail(FCOO_ERR_CUDA, "build sync: %s", cudaGetErrorString(ce));
+  if (err0 & ERRF_INDEX_RANGE) return fail(FCOO_ERR_INDEX_RANGE, "a coordinate is >= its mode extent");
+  f->h_blk_start.assign(nblocks + 1, 0);
+  f->h_blk_end.assign(nblocks, 0);
+  for (int64_t b = 0; b < nblocks; ++b) {
+    const int64_t nb = start[b + 1] - start[b];
+    f->h_blk_end[b] = f->h_blk_start[b] + nb;
+    f->h_blk_start[b + 1] = f->h_blk_start[b] + (nb + T - 1) / T * T;
+  }
+  const int64_t ns = f->h_blk_start[nblocks], nwords = ns / 32;
+  if (ns >= 4294967295LL) return fail(FCOO_ERR_ARG, "blocked stream of %lld positions needs < 2^32", (long long)ns);
+  f->nnz_pad = ns;
+  f->ntiles = ns / T;
+  f->tile_begin = 0;
+  f->tile_end = f->ntiles;
+  const int64_t ntiles = f->ntiles;
+  const int n_words = f->n_words;
+  f->pidx = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)(n_words * ns), s, &f->bytes_pidx);
+  f->val = grab<float>(f, sizeof(float) * (size_t)ns, s, &f->bytes_val);
+  f->bf = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)nwords, s, &f->bytes_bf);
+  f->sf = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)((ntiles + 31) / 32 + 1), s, &f->bytes_sf);
+  f->seg_base = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)(ntiles + 1), s, &f->bytes_seg_base);
+  f->blk_start = grab<int64_t>(f, sizeof(int64_t) * (size_t)(2 * nblocks + 1), s, &f->bytes_blk);
+  if (keep_perm) f->perm = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)ns, s, &f->bytes_perm);
+  if (!f->pidx || !f->val || !f->bf || !f->sf || !f->seg_base || !f->blk_start || (keep_perm && !f->perm))
+    return fail(FCOO_ERR_OOM, "handle allocation failed");
+  f->blk_end = f->blk_start + nblocks + 1;
+  FCOO_CUDA_TRY(cudaMemcpyAsync(f->blk_start, f->h_blk_start.data(), sizeof(int64_t) * (nblocks + 1),
+                                cudaMemcpyHostToDevice, s));
+  FCOO_CUDA_TRY(cudaMemcpyAsync(f->blk_end, f->h_blk_end.data(), sizeof(int64_t) * nblocks, cudaMemcpyHostToDevice, s));
+  fcoo_status st = make_items(f, s);
+  if (st) return st;
+
+  Buf qmap(&f->alloc, sizeof(uint32_t) * ns, s);
+  Buf wcount(&f->alloc, sizeof(uint32_t) * (nwords + 1), s), wbase(&f->alloc, sizeof(uint32_t) * (nwords + 1), s);
+  if (!qmap.ok() || !wcount.ok() || !wbase.ok()) return fail(FCOO_ERR_OOM, "build scratch allocation failed");
+  if ((ce = cudaMemsetAsync(wcount.p, 0, sizeof(uint32_t) * (nwords + 1), s)) != cudaSuccess)
+    return fail(FCOO_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
+  k_blk_qmap<<<(unsigned)((ns + TB - 1) / TB), TB, 0, s>>>(f->blk_start, startb.as<int64_t>(), nblocks, ns,
+                                                          qmap.as<uint32_t>());
+  count_launch();
+  k_flags_blocked<K><<<(unsigned)((ns + TB - 1) / TB), TB, 0, s>>>(keys, ord, coo->val, L, f->n_prod, f->pk_shift,
+                                                                    qmap.as<uint32_t>(), ns, f->pidx, f->val, f->bf,
+                                                                    wcount.as<uint32_t>(), f->perm, errb.as<uint32_t>());
+  count_launch();
+  if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_flags_blocked: %s", cudaGetErrorString(ce));
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, wcount.as<uint32_t>(), wbase.as<uint32_t>(), (int64_t)(nwords + 1), s);
+  {
+    Buf scantmp(&f->alloc, scan_bytes, s);
+    if (!scantmp.ok()) return fail(FCOO_ERR_OOM, "scan scratch");
+    if ((ce = cub::DeviceScan::ExclusiveSum(scantmp.p, scan_bytes, wcount.as<uint32_t>(), wbase.as<uint32_t>(),
+                                            (int64_t)(nwords + 1), s)) != cudaSuccess)
+      return fail(FCOO_ERR_CUDA, "scan: %s", cudaGetErrorString(ce));
+    count_launch(2);
+  }
+  const int64_t tthreads = ((ntiles + 1 + 31) / 32) * 32;
+  k_tiles<<<(unsigned)((tthreads + TB - 1) / TB), TB, 0, s>>>(f->bf, wbase.as<uint32_t>(), ntiles, T / 32, nwords,
+                                                             f->sf, f->seg_base);
+  count_launch();
+  if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_tiles: %s", cudaGetErrorString(ce));
+  // host sync 2 of 2: duplicates and the segment count
+  uint32_t host[2] = {0, 0};
+  if ((ce = cudaMemcpyAsync(&host[0], errb.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+      (ce = cudaMemcpyAsync(&host[1], wbase.as<uint32_t>() + nwords, sizeof(uint32_t), cudaMemcpyDeviceToHost, s)) != cudaSuccess ||
+      (ce = cudaStreamSynchronize(s)) != cudaSuccess)
+    return fail(FCOO_ERR_CUDA, "build sync: %s", cudaGetErrorString(ce));
+  if (host[0] & ERRF_DUPLICATE) return fail(FCOO_ERR_DUPLICATE, "duplicate coordinates");
+  f->nsegs = host[1];
+  f->dense_rows = 0;  // a row recurs once per block: seg_coord is always used
+  f->seg_coord = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)std::max<int64_t>(1, f->nsegs * f->n_idx), s,
+                                &f->bytes_seg_coord);
+  if (!f->seg_coord) return fail(FCOO_ERR_OOM, "seg_coord allocation");
+  k_seg_coord_blocked<K><<<(unsigned)((ns + TB - 1) / TB), TB, 0, s>>>(keys, qmap.as<uint32_t>(), f->bf,
+                                                                        wbase.as<uint32_t>(), L, ns, f->seg_coord);
+  count_launch();
+  if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_seg_coord_blocked: %s", cudaGetErrorString(ce));
+  return FCOO_OK;
+}
+
 fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opts, const fcoo_allocator* alloc,
                        cudaStream_t s, fcoo_t* out) {
   if (!coo || !out) return fail(FCOO_ERR_ARG, "NULL coo/out");
@@ -299,6 +545,24 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
   fcoo_s tmp;
   fcoo_status st = plan_modes(&tmp, coo->order, coo->dims, op, mode, (flags & FCOO_BUILD_PRODUCT_DESC) != 0);
   if (st) return st;
+  const bool blocked = (flags & FCOO_BUILD_BLOCKED) != 0;
+  int BR = 0;
+  if (blocked) {
+    BR = (opts && opts->block_rows) ? opts->block_rows : 512;
+    if (op != FCOO_OP_MTTKRP) return fail(FCOO_ERR_ARG, "FCOO_BUILD_BLOCKED is for FCOO_OP_MTTKRP handles");
+    if (coo->order > 5) return fail(FCOO_ERR_ARG, "FCOO_BUILD_BLOCKED supports order <= 5 (got %d)", coo->order);
+    if (flags & (FCOO_BUILD_DETERMINISTIC | FCOO_BUILD_PRODUCT_DESC))
+      return fail(FCOO_ERR_ARG, "FCOO_BUILD_BLOCKED excludes DETERMINISTIC and PRODUCT_DESC");
+    if (BR < 32 || BR > 65536) return fail(FCOO_ERR_ARG, "block_rows %d outside [32, 65536]", BR);
+    tmp.blocked = 1;
+    tmp.block_rows = BR;
+    tmp.nblocks = (coo->dims[tmp.prod_modes[0]] + BR - 1) / BR;
+    tmp.n_words = tmp.n_prod >= 2 ? tmp.n_prod - 1 : 1;
+    const int ib = tmp.n_prod >= 2 ? bits_for(coo->dims[tmp.prod_modes[tmp.n_prod - 1]]) : 0;
+    tmp.pk_shift = ib;
+    if (tmp.n_prod >= 2 && bits_for(BR) + ib > 32)
+      return fail(FCOO_ERR_ARG, "blocked word needs ceil(log2 %d) + %d > 32 bits", BR, ib);
+  }
   if (coo->nnz <= 0) return fail(FCOO_ERR_EMPTY, "nnz == 0");
   if (coo->nnz >= 4294967295LL) return fail(FCOO_ERR_ARG, "nnz must be < 2^32");
   for (int m = 0; m < coo->order; ++m) if (!coo->idx[m]) return fail(FCOO_ERR_ARG, "idx[%d] is NULL", m);
@@ -311,7 +575,8 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
   for (int a = 0; a < tmp.n_prod; ++a) L.key_modes[tmp.n_idx + a] = tmp.prod_modes[a];
   int total = 0, bits[kMaxOrder];
   for (int a = 0; a < L.order; ++a) { bits[a] = bits_for(coo->dims[L.key_modes[a]]); total += bits[a]; }
-  if (total > 128) return fail(FCOO_ERR_KEY_BITS, "sort key needs %d bits > 128", total);
+  const int blk_bits = blocked ? bits_for(tmp.nblocks) : 0;
+  if (total + blk_bits > 128) return fail(FCOO_ERR_KEY_BITS, "sort key needs %d bits > 128", total + blk_bits);
   int sh = 0;
   for (int a = L.order - 1; a >= 0; --a) {
     L.shift[a] = sh;
@@ -322,6 +587,8 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
   }
   L.prod_bits = 0;
   for (int a = tmp.n_idx; a < L.order; ++a) L.prod_bits += bits[a];
+  L.BR = (uint32_t)BR;
+  L.blk_shift = total;
   IdxPtrs ip{};
   for (int a = 0; a < L.order; ++a) ip.p[a] = coo->idx[L.key_modes[a]];
 
@@ -338,6 +605,14 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
   const int64_t nnz = f->nnz, nnz_pad = f->nnz_pad, nwords = nnz_pad / 32, ntiles = f->ntiles;
 
   auto bail = [&](fcoo_status e) { free_handle_arrays(f); delete f; return e; };
+  if (blocked) {
+    const int tb = total + blk_bits;
+    st = tb <= 64 ? sort_and_flag_blocked<uint64_t>(f, coo, L, ip, tb, flags, s)
+                  : sort_and_flag_blocked<unsigned __int128>(f, coo, L, ip, tb, flags, s);
+    if (st) return bail(st);
+    *out = f;
+    return FCOO_OK;
+  }
 
   f->pidx = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)(f->n_prod * nnz_pad), s, &f->bytes_pidx);
   f->val = grab<float>(f, sizeof(float) * (size_t)nnz_pad, s, &f->bytes_val);

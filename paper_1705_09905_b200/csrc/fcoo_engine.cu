@@ -3,6 +3,7 @@
 // SpMTTKRP / SpTTM entry points behind the C ABI.
 #include <stdlib.h>
 
+#include "fcoo_blocked.cuh"
 #include "fcoo_engine.cuh"
 
 namespace fcoo {
@@ -115,8 +116,56 @@ fcoo_status prepare_output(fcoo_s* f, int R, ACC* out, int64_t rows, bool all_ro
 }  // namespace
 
 template <class ACC>
+cudaError_t launch_blocked(const BlockedParams& P, int NP, int nitems, bool vec_ok, cudaStream_t s) {
+  switch (NP) {
+    case 1: return launch_blocked_np<1, ACC>(P, nitems, vec_ok, s);
+    case 2: return launch_blocked_np<2, ACC>(P, nitems, vec_ok, s);
+    case 3: return launch_blocked_np<3, ACC>(P, nitems, vec_ok, s);
+    default: return launch_blocked_np<4, ACC>(P, nitems, vec_ok, s);
+  }
+}
+
+// SpMTTKRP on a blocked handle (fcoo_blocked.cuh): zero the output (a row recurs once per block,
+// every flush is a red.add), pick the work table for the launch shape, restrict it to the shard.
+template <class ACC>
+fcoo_status mttkrp_blocked(fcoo_s* f, const float* const* factors, int R, ACC* out, cudaStream_t s, const int* gate,
+                           int gate_on, float* out_mc) {
+  BlockedParams P{};
+  bool vec_ok = (R % 4 == 0) && R <= 128 && aligned16(out);
+  for (int a = 0; a < f->n_prod; ++a) {
+    const int m = f->prod_modes[a];
+    if (!factors[m]) return fail(FCOO_ERR_ARG, "factors[%d] is NULL", m);
+    P.U[a] = factors[m];
+    vec_ok = vec_ok && aligned16(factors[m]);
+  }
+  if (out_mc && (!vec_ok || !std::is_same<ACC, float>::value))
+    return fail(FCOO_ERR_ARG, "fused combine needs the float4 path (R %% 4 == 0, R <= 128, aligned)");
+  P.pk = f->pidx; P.val = f->val; P.bf = f->bf; P.sf = f->sf; P.seg_base = f->seg_base; P.seg_coord = f->seg_coord;
+  P.blk_start = f->blk_start; P.blk_end = f->blk_end;
+  P.nstream = f->nnz_pad; P.ntiles = f->ntiles; P.tile_begin = f->tile_begin; P.tile_end = f->tile_end;
+  P.T = (int)f->T; P.R = R; P.BR = f->block_rows; P.Io = (int)f->dims[f->prod_modes[0]]; P.shift = f->pk_shift;
+  P.out = out; P.out_mc = out_mc; P.gate = gate; P.gate_on = gate_on;
+  if (!out_mc) FCOO_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(ACC) * (size_t)f->dims[f->mode] * R, s));
+  const BlockedShape sh = blocked_shape(f->n_prod, R, f->block_rows, vec_ok);
+  int k = 0;
+  while ((1 << k) < sh.TB / sh.G) ++k;
+  const std::vector<int2>& items = f->h_items[k];
+  // items whose tiles [t0, t0 + gpc) meet the shard's [tile_begin, tile_end) (sorted by t0)
+  const int gpc = 1 << k;
+  int64_t i0 = 0, i1 = (int64_t)items.size();
+  while (i0 < i1 && (int64_t)items[i0].y + gpc <= f->tile_begin) ++i0;
+  while (i1 > i0 && (int64_t)items[i1 - 1].y >= f->tile_end) --i1;
+  P.items = f->items[k];
+  P.item0 = i0;
+  cudaError_t e = launch_blocked<ACC>(P, f->n_prod, (int)(i1 - i0), vec_ok, s);
+  if (e != cudaSuccess) return fail(FCOO_ERR_CUDA, "blocked mttkrp launch: %s", cudaGetErrorString(e));
+  return FCOO_OK;
+}
+
+template <class ACC>
 fcoo_status mttkrp_t(fcoo_s* f, const float* const* factors, int R, ACC* out, cudaStream_t s,
                      const int* gate = nullptr, int gate_on = 0, float* out_mc = nullptr) {
+  if (f->blocked) return mttkrp_blocked<ACC>(f, factors, R, out, s, gate, gate_on, out_mc);
   EngineParams P{};
   P.out_mc = out_mc;
   P.gate = gate;
@@ -168,6 +217,13 @@ fcoo_status run_mttkrp_mc(fcoo_s* f, const float* const* factors, int R, fcoo_mc
   const size_t need = sizeof(float) * (size_t)f->dims[f->mode] * (size_t)R;
   if (bytes < need) return fail(FCOO_ERR_ARG, "multicast buffer holds %zu bytes, output needs %zu", bytes, need);
   if (f->comm && f->comm != comm) return fail(FCOO_ERR_ARG, "handle sharded over a different comm");
+  {  // every rank must process exactly its own shard, or shared rows would be added nranks times
+    int rank = 0, nranks = 1;
+    comm_rank_size(comm, &rank, &nranks);
+    if (f->nshards != nranks || f->shard != rank)
+      return fail(FCOO_ERR_ARG, "fused combine: handle shard %d/%d does not match comm rank %d/%d", f->shard,
+                  f->nshards, rank, nranks);
+  }
   if (f->deterministic) return fail(FCOO_ERR_ARG, "fused combine: the multicast reduction order is not fixed (deterministic handle)");
   FCOO_CUDA_TRY(cudaMemsetAsync(uc, 0, need, s));
   fcoo_status st = comm_barrier(comm, s);

@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <string>
+#include <vector>
 
 #include "fcoo.h"
 
@@ -62,6 +63,18 @@ struct fcoo_s {
   uint32_t* perm = nullptr;      // nnz (KEEP_PERM only)
   size_t bytes_pidx = 0, bytes_val = 0, bytes_bf = 0, bytes_sf = 0, bytes_seg_base = 0, bytes_seg_coord = 0,
          bytes_perm = 0;
+  // blocked layout (FCOO_BUILD_BLOCKED): pidx holds n_words packed words per
+  // position (word 0: (i_outer - b*BR) << pk_shift | i_last; words 1..: middle product modes)
+  int blocked = 0, block_rows = 0, pk_shift = 0, n_words = 0;
+  int64_t nblocks = 0;
+  int64_t* blk_start = nullptr;  // device [nblocks + 1]: first stream position of block b
+  int64_t* blk_end = nullptr;    // device [nblocks]: end of block b's nonzeros
+  size_t bytes_blk = 0;
+  std::vector<int64_t> h_blk_start, h_blk_end;  // host copies (work tables, export)
+  // work items of the blocked SpMTTKRP, one table per groups-per-CTA value gpc = 1 << k (k < 10):
+  // item = (block b, first tile t0), t0 = first tile of b + j*gpc; device int2 + host copy
+  int2* items[10] = {nullptr};
+  std::vector<int2> h_items[10];
   // shard
   int shard = 0, nshards = 1;
   int64_t tile_begin = 0, tile_end = 0;

@@ -23,6 +23,7 @@ OP_MTTKRP, OP_TTM = 0, 1
 BUILD_KEEP_PERM = 1
 BUILD_PRODUCT_DESC = 2
 BUILD_DETERMINISTIC = 4
+BUILD_BLOCKED = 8
 
 
 class FcooError(RuntimeError):
@@ -45,7 +46,7 @@ class _Allocator(ctypes.Structure):
 
 
 class _BuildOpts(ctypes.Structure):
-    _fields_ = [("op", ctypes.c_int), ("tile_nnz", ctypes.c_int), ("flags", ctypes.c_uint)]
+    _fields_ = [("op", ctypes.c_int), ("tile_nnz", ctypes.c_int), ("flags", ctypes.c_uint), ("block_rows", ctypes.c_int)]
 
 
 class _Info(ctypes.Structure):
@@ -55,13 +56,16 @@ class _Info(ctypes.Structure):
                 ("ntiles", ctypes.c_int64), ("tile_nnz", ctypes.c_int64), ("dense_rows", ctypes.c_int),
                 ("storage_bytes", ctypes.c_int64), ("seg_table_bytes", ctypes.c_int64),
                 ("device_bytes", ctypes.c_int64), ("shard", ctypes.c_int), ("nshards", ctypes.c_int),
-                ("tile_begin", ctypes.c_int64), ("tile_end", ctypes.c_int64)]
+                ("tile_begin", ctypes.c_int64), ("tile_end", ctypes.c_int64), ("blocked", ctypes.c_int),
+                ("block_rows", ctypes.c_int), ("nblocks", ctypes.c_int64), ("nstream", ctypes.c_int64),
+                ("pk_shift", ctypes.c_int), ("n_words", ctypes.c_int)]
 
 
 class _HostView(ctypes.Structure):
     _fields_ = [("perm", ctypes.c_void_p), ("bf", ctypes.c_void_p), ("sf", ctypes.c_void_p),
                 ("seg_base", ctypes.c_void_p), ("seg_coord", ctypes.c_void_p), ("pidx", ctypes.c_void_p),
-                ("val", ctypes.c_void_p)]
+                ("val", ctypes.c_void_p), ("pk", ctypes.c_void_p), ("blk_start", ctypes.c_void_p),
+                ("blk_end", ctypes.c_void_p)]
 
 
 class _CpOpts(ctypes.Structure):
@@ -257,6 +261,12 @@ class Info:
     nshards: int
     tile_begin: int
     tile_end: int
+    blocked: bool = False
+    block_rows: int = 0
+    nblocks: int = 0
+    nstream: int = 0
+    pk_shift: int = 0
+    n_words: int = 0
 
 
 class Fcoo:
@@ -274,7 +284,8 @@ class Fcoo:
         return Info(o, inf.op, inf.mode, inf.n_idx, inf.n_prod, list(inf.idx_modes[: inf.n_idx]),
                     list(inf.prod_modes[: inf.n_prod]), list(inf.dims[:o]), inf.nnz, inf.nsegs, inf.ntiles,
                     inf.tile_nnz, bool(inf.dense_rows), inf.storage_bytes, inf.seg_table_bytes, inf.device_bytes,
-                    inf.shard, inf.nshards, inf.tile_begin, inf.tile_end)
+                    inf.shard, inf.nshards, inf.tile_begin, inf.tile_end, bool(inf.blocked), inf.block_rows,
+                    inf.nblocks, inf.nstream, inf.pk_shift, inf.n_words)
 
     def destroy(self):
         if self.h:
@@ -288,11 +299,17 @@ class Fcoo:
             pass
 
 
+def _flags(keep_perm=False, product_desc=False, deterministic=False, blocked=False) -> int:
+    return ((BUILD_KEEP_PERM if keep_perm else 0) | (BUILD_PRODUCT_DESC if product_desc else 0)
+            | (BUILD_DETERMINISTIC if deterministic else 0) | (BUILD_BLOCKED if blocked else 0))
+
+
 def fcoo_build(coo: Coo, mode: int, op: int = OP_MTTKRP, tile_nnz: int = 0, keep_perm: bool = False,
-               product_desc: bool = False, stream=None, deterministic: bool = False) -> Fcoo:
+               product_desc: bool = False, stream=None, deterministic: bool = False, blocked: bool = False,
+               block_rows: int = 0) -> Fcoo:
+    """blocked=True: the blocked F-COO of FCOO_BUILD_BLOCKED (block_rows 0 = the library default)."""
     L = load_library()
-    opts = _BuildOpts(op, tile_nnz, (BUILD_KEEP_PERM if keep_perm else 0) | (BUILD_PRODUCT_DESC if product_desc else 0)
-                      | (BUILD_DETERMINISTIC if deterministic else 0))
+    opts = _BuildOpts(op, tile_nnz, _flags(keep_perm, product_desc, deterministic, blocked), block_rows)
     out = ctypes.c_void_p()
     _check(L.fcoo_build(ctypes.byref(coo.c), mode, ctypes.byref(opts), ctypes.byref(_ALLOCATOR),
                         ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out)), "fcoo_build")
@@ -300,27 +317,48 @@ def fcoo_build(coo: Coo, mode: int, op: int = OP_MTTKRP, tile_nnz: int = 0, keep
 
 
 def fcoo_build_sharded(coo: Coo, mode: int, comm: "Comm", op: int = OP_MTTKRP, tile_nnz: int = 0,
-                       keep_perm: bool = False, stream=None, deterministic: bool = False) -> Fcoo:
+                       keep_perm: bool = False, stream=None, deterministic: bool = False, blocked: bool = False,
+                       block_rows: int = 0) -> Fcoo:
     """fcoo_build + fcoo_set_shard(comm.rank, comm.nranks, comm) in one C call."""
     L = load_library()
-    opts = _BuildOpts(op, tile_nnz, (BUILD_KEEP_PERM if keep_perm else 0) | (BUILD_DETERMINISTIC if deterministic else 0))
+    opts = _BuildOpts(op, tile_nnz, _flags(keep_perm, False, deterministic, blocked), block_rows)
     out = ctypes.c_void_p()
     _check(L.fcoo_build_sharded(ctypes.byref(coo.c), mode, ctypes.byref(opts), comm.h, ctypes.byref(_ALLOCATOR),
                                 ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out)), "fcoo_build_sharded")
     return Fcoo(out.value, coo)
 
 
-def fcoo_mttkrp(f: Fcoo, factors, R: int, out: torch.Tensor, stream=None) -> torch.Tensor:
-    """factors: list of `order` CUDA fp32 (I_m, R) tensors (entry [mode] may be None)."""
-    L = load_library()
+def _factor_ptrs(f: "Fcoo", factors, R: int, skip_mode: int):
+    """Device pointers of `order` factors, each checked to be a contiguous fp32 CUDA (dims[m], R)
+    tensor (the C ABI carries no sizes: a wrong shape would read out of bounds)."""
+    i = f.info
+    if len(factors) != i.order:
+        raise ValueError(f"expected {i.order} factors, got {len(factors)}")
     ptrs = []
     for m, U in enumerate(factors):
         if U is None:
+            if m != skip_mode:
+                raise ValueError(f"factors[{m}] is None")
             ptrs.append(None)
             continue
         _require_cuda(U, torch.float32, f"factors[{m}]")
+        if m != skip_mode and tuple(U.shape) != (i.dims[m], R):
+            raise ValueError(f"factors[{m}] has shape {tuple(U.shape)}, expected {(i.dims[m], R)}")
         ptrs.append(U.data_ptr())
-    _require_cuda(out, torch.float32, "out")
+    return ptrs
+
+
+def _check_out(out: torch.Tensor, rows: int, cols: int, name: str = "out"):
+    _require_cuda(out, torch.float32, name)
+    if out.numel() < rows * cols:
+        raise ValueError(f"{name} holds {out.numel()} elements, needs {rows} x {cols}")
+
+
+def fcoo_mttkrp(f: Fcoo, factors, R: int, out: torch.Tensor, stream=None) -> torch.Tensor:
+    """factors: list of `order` CUDA fp32 (I_m, R) tensors (entry [mode] may be None)."""
+    L = load_library()
+    ptrs = _factor_ptrs(f, factors, R, f.info.mode)
+    _check_out(out, f.info.dims[f.info.mode], R)
     arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
     _check(L.fcoo_mttkrp(f.h, arr, R, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))),
            "fcoo_mttkrp")
@@ -330,7 +368,9 @@ def fcoo_mttkrp(f: Fcoo, factors, R: int, out: torch.Tensor, stream=None) -> tor
 def fcoo_ttm(f: Fcoo, U: torch.Tensor, R: int, out: torch.Tensor, stream=None) -> torch.Tensor:
     L = load_library()
     _require_cuda(U, torch.float32, "U")
-    _require_cuda(out, torch.float32, "out")
+    if tuple(U.shape) != (f.info.dims[f.info.mode], R):
+        raise ValueError(f"U has shape {tuple(U.shape)}, expected {(f.info.dims[f.info.mode], R)}")
+    _check_out(out, f.info.nsegs, R)
     _check(L.fcoo_ttm(f.h, ctypes.c_void_p(U.data_ptr()), R, ctypes.c_void_p(out.data_ptr()),
                       ctypes.c_void_p(_stream_ptr(stream))), "fcoo_ttm")
     return out
@@ -340,6 +380,9 @@ def fcoo_ttmc(f: Fcoo, factors, out: torch.Tensor, stream=None) -> torch.Tensor:
     """SpTTMc (Eq.(4)) on an MTTKRP handle of an order-3 tensor.  factors: list of `order` CUDA fp32
     (I_m, R_m) tensors (entry [mode] may be None); out: (I_mode, prod of the other R_m)."""
     L = load_library()
+    i = f.info
+    if len(factors) != i.order:
+        raise ValueError(f"expected {i.order} factors, got {len(factors)}")
     ptrs, ranks = [], []
     for m, U in enumerate(factors):
         if U is None:
@@ -347,9 +390,15 @@ def fcoo_ttmc(f: Fcoo, factors, out: torch.Tensor, stream=None) -> torch.Tensor:
             ranks.append(0)
             continue
         _require_cuda(U, torch.float32, f"factors[{m}]")
+        if U.dim() != 2 or (m != i.mode and U.shape[0] != i.dims[m]):
+            raise ValueError(f"factors[{m}] has shape {tuple(U.shape)}, expected ({i.dims[m]}, R_{m})")
         ptrs.append(U.data_ptr())
         ranks.append(int(U.shape[1]))
-    _require_cuda(out, torch.float32, "out")
+    ncol = 1
+    for m in range(i.order):
+        if m != i.mode:
+            ncol *= ranks[m]
+    _check_out(out, i.dims[i.mode], ncol)
     arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
     rk = (ctypes.c_int * len(ranks))(*ranks)
     _check(L.fcoo_ttmc(f.h, arr, rk, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))),
@@ -358,21 +407,28 @@ def fcoo_ttmc(f: Fcoo, factors, out: torch.Tensor, stream=None) -> torch.Tensor:
 
 
 def fcoo_export(f: Fcoo, perm: bool = False, stream=None) -> dict:
+    """Host copies of the handle's arrays (stream length = info.nstream: nnz, or nnz + padding on a
+    blocked handle, whose export also has the packed words "pk" and the block tables)."""
     import numpy as np
     i = f.info
-    nnz = i.nnz
+    ns = i.nstream
     d = {
-        "bf": np.zeros((nnz + 7) // 8, np.uint8),
+        "bf": np.zeros((ns + 7) // 8, np.uint8),
         "sf": np.zeros((i.ntiles + 31) // 32, np.uint32),
         "seg_base": np.zeros(i.ntiles, np.uint32),
         "seg_coord": np.zeros((i.nsegs, i.n_idx), np.uint32),
-        "pidx": np.zeros((i.n_prod, nnz), np.uint32),
-        "val": np.zeros(nnz, np.float32),
+        "pidx": np.zeros((i.n_prod, ns), np.uint32),
+        "val": np.zeros(ns, np.float32),
     }
+    if i.blocked:
+        d["pk"] = np.zeros((i.n_words, ns), np.uint32)
+        d["blk_start"] = np.zeros(i.nblocks + 1, np.int64)
+        d["blk_end"] = np.zeros(i.nblocks, np.int64)
     if perm:
-        d["perm"] = np.zeros(nnz, np.uint32)
+        d["perm"] = np.zeros(ns, np.uint32)
     v = _HostView(*(d[k].ctypes.data if k in d else None
-                    for k in ("perm", "bf", "sf", "seg_base", "seg_coord", "pidx", "val")))
+                    for k in ("perm", "bf", "sf", "seg_base", "seg_coord", "pidx", "val", "pk", "blk_start",
+                              "blk_end")))
     _check(load_library().fcoo_export(f.h, ctypes.byref(v), ctypes.c_void_p(_stream_ptr(stream))), "fcoo_export")
     return d
 
@@ -463,13 +519,9 @@ def _tensor_view(ptr: int, numel: int) -> torch.Tensor:
 def fcoo_mttkrp_mc(f: Fcoo, factors, R: int, out: McBuffer, stream=None) -> torch.Tensor:
     """SpMTTKRP with the cross-rank combine fused into the epilogue; returns out.local[:I_n*R] as (I_n, R)."""
     L = load_library()
-    ptrs = []
-    for m, U in enumerate(factors):
-        if U is None:
-            ptrs.append(None)
-            continue
-        _require_cuda(U, torch.float32, f"factors[{m}]")
-        ptrs.append(U.data_ptr())
+    ptrs = _factor_ptrs(f, factors, R, f.info.mode)
+    if out.numel < f.info.dims[f.info.mode] * R:
+        raise ValueError(f"multicast buffer holds {out.numel} floats, output needs {f.info.dims[f.info.mode] * R}")
     arr = (ctypes.c_void_p * len(ptrs))(*ptrs)
     _check(L.fcoo_mttkrp_mc(f.h, arr, R, out.h, ctypes.c_void_p(_stream_ptr(stream))), "fcoo_mttkrp_mc")
     I = f.info.dims[f.info.mode]
@@ -483,8 +535,12 @@ def cp_als(coo: Coo, R: int, iters: int, factors, tol: float = 0.0, tile_nnz: in
     Returns (lambda CUDA fp32 (R,), fit_trace list)."""
     import numpy as np
     L = load_library()
+    if len(factors) != coo.order:
+        raise ValueError(f"expected {coo.order} factors, got {len(factors)}")
     for m, U in enumerate(factors):
         _require_cuda(U, torch.float32, f"factors[{m}]")
+        if tuple(U.shape) != (coo.dims[m], R):
+            raise ValueError(f"factors[{m}] has shape {tuple(U.shape)}, expected {(coo.dims[m], R)}")
     lam = torch.empty(R, dtype=torch.float32, device=factors[0].device)
     trace = np.zeros(iters, np.float64)
     done = ctypes.c_int(0)
