@@ -123,3 +123,37 @@ def workload(name: str, nnz: int | None = None):
     w = WORKLOADS[name]
     idx, val = coo(w.dims, nnz if nnz is not None else w.nnz, w.alpha, w.seed)
     return w, idx, val
+
+
+def planted_sparse(dims, R: int, s: int, seed: int, disjoint_mode: int = 0):
+    """Test-data synthesis (no method arithmetic): a rank-R tensor with sparse-support factors,
+    X = sum_r lam_r U_0(:,r) o U_1(:,r) o ... (SURVEY §8(c) c4 "exact recovery" family at
+    configuration-5 shape).  Column r of mode m is nonzero on s distinct rows, values in [0.5, 1.5);
+    in `disjoint_mode` the supports of different columns are disjoint (needs R*s <= dims[mode]), so
+    every stored cell belongs to exactly one rank-1 term and its value is that term's product,
+    evaluated in fp64 and rounded once to fp32.  nnz = R * s**order.
+    Returns (idx (order, nnz) uint32, val fp32, factors fp64 list, lam fp64)."""
+    rng = np.random.default_rng(seed)
+    order = len(dims)
+    assert R * s <= dims[disjoint_mode]
+    lam = 1.0 + rng.random(R)
+    facs = [np.zeros((int(I), R)) for I in dims]
+    sup = [[None] * R for _ in range(order)]
+    for m, I in enumerate(dims):
+        dis = rng.permutation(int(I))[: R * s] if m == disjoint_mode else None
+        for r in range(R):
+            rows = np.sort(dis[r * s:(r + 1) * s]) if m == disjoint_mode else np.sort(rng.choice(int(I), s, replace=False))
+            sup[m][r] = rows
+            facs[m][rows, r] = 0.5 + rng.random(s)
+    n_term = s ** order
+    idx = np.empty((order, R * n_term), np.uint32)
+    val = np.empty(R * n_term, np.float32)
+    for r in range(R):
+        grids = np.meshgrid(*[sup[m][r] for m in range(order)], indexing="ij")
+        prod = np.full(grids[0].shape, lam[r])
+        for m in range(order):
+            prod = prod * facs[m][grids[m], r]
+        for m in range(order):
+            idx[m, r * n_term:(r + 1) * n_term] = grids[m].ravel()
+        val[r * n_term:(r + 1) * n_term] = prod.ravel().astype(np.float32)
+    return idx, val, facs, lam

@@ -294,6 +294,9 @@ typedef struct {
   uint64_t seed;    /* != 0: the library seeds the factors itself (below); 0: caller's init */
   int deterministic; /* != 0: build every mode with FCOO_BUILD_DETERMINISTIC, so repeated runs
                         give bitwise-identical factors, lambda and fit trace */
+  int layout;        /* 0 = automatic: every mode's handle uses the blocked F-COO (FCOO_BUILD_BLOCKED)
+                        when the build allows it (not deterministic, order <= 5, packed word fits),
+                        else the plain F-COO; 1 = always the plain F-COO */
 } fcoo_cp_opts;
 
 /*

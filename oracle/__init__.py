@@ -56,6 +56,7 @@ def _load():
         L.orc_pinv_sym.argtypes = [ci, vp, vp]
         L.orc_normalize.argtypes = [i64, ci, vp, vp]
         L.orc_cp_als.argtypes = [ci, vp, i64, vp, vp, ci, ci, ctypes.c_double, vp, vp, vp, vp]
+        L.orc_cp_als_mt.argtypes = [ci, vp, i64, vp, vp, ci, ci, ctypes.c_double, vp, vp, vp, vp, ci]
         _lib = L
     return _lib
 
@@ -275,8 +276,9 @@ def normalize(A):
     return A, lam
 
 
-def cp_als(dims, idx, val, R: int, iters: int, init, tol: float = 0.0):
-    """Returns (factors fp64 list, lambda fp64[R], fit_trace fp64[iters_done])."""
+def cp_als(dims, idx, val, R: int, iters: int, init, tol: float = 0.0, nthreads: int = 1):
+    """Returns (factors fp64 list, lambda fp64[R], fit_trace fp64[iters_done]).  nthreads > 1 splits
+    each MTTKRP over host threads (private partials merged in thread order)."""
     L = _load()
     d, idx, val = _coo(dims, idx, val)
     ins = [np.ascontiguousarray(f, dtype=np.float32) for f in init]
@@ -285,8 +287,8 @@ def cp_als(dims, idx, val, R: int, iters: int, init, tol: float = 0.0):
     op = (ctypes.c_void_p * len(d))(*[_ptr(f) for f in outs])
     lam = np.zeros(R, np.float64)
     trace = np.zeros(iters, np.float64)
-    n = L.orc_cp_als(len(d), _ptr(d), val.shape[0], _ptr(idx), _ptr(val), R, iters, tol, ip, op, _ptr(lam),
-                     _ptr(trace))
+    n = L.orc_cp_als_mt(len(d), _ptr(d), val.shape[0], _ptr(idx), _ptr(val), R, iters, tol, ip, op, _ptr(lam),
+                        _ptr(trace), int(nthreads))
     if n < 0:
         raise OracleError(-n, "cp_als")
     return outs, lam, trace[:n].copy()

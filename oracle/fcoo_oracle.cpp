@@ -522,20 +522,42 @@ void orc_normalize(int64_t I, int R, double* A, double* lambda) {
   }
 }
 
-/* fp64 MTTKRP with fp64 factors (used inside the CP oracle). */
+/* fp64 MTTKRP with fp64 factors (used inside the CP oracle), Eq.(6) as in orc_mttkrp.
+ * nthreads > 1: each thread sums a contiguous range of q into a private fp64 I_n x R array and the
+ * partials are added in thread order (same sum, another association; pinned by the threads-agree
+ * test).  Timing/scale only: the arithmetic per term is unchanged. */
 static void mttkrp_f64(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, const float* val, int mode,
-                       double* const* U, int R, double* M) {
+                       double* const* U, int R, double* M, int nthreads) {
   int64_t In = dims[mode];
   memset(M, 0, sizeof(double) * (size_t)(In * R));
-  for (int64_t q = 0; q < nnz; ++q) {
-    int64_t i = idx[(int64_t)mode * nnz + q];
-    for (int r = 0; r < R; ++r) {
-      double t = (double)val[q];
-      for (int m = 0; m < order; ++m)
-        if (m != mode) t *= U[m][(int64_t)idx[(int64_t)m * nnz + q] * R + r];
-      M[i * R + r] += t;
+  auto range = [&](int64_t q0, int64_t q1, double* out) {
+    for (int64_t q = q0; q < q1; ++q) {
+      int64_t i = idx[(int64_t)mode * nnz + q];
+      for (int r = 0; r < R; ++r) {
+        double t = (double)val[q];
+        for (int m = 0; m < order; ++m)
+          if (m != mode) t *= U[m][(int64_t)idx[(int64_t)m * nnz + q] * R + r];
+        out[i * R + r] += t;
+      }
     }
+  };
+  if (nthreads <= 1) {
+    range(0, nnz, M);
+    return;
   }
+  std::vector<std::vector<double>> part((size_t)nthreads);
+#pragma omp parallel num_threads(nthreads)
+  {
+#ifdef _OPENMP
+    const int t = omp_get_thread_num();
+#else
+    const int t = 0;
+#endif
+    part[t].assign((size_t)(In * R), 0.0);
+    range(nnz * t / nthreads, nnz * (t + 1) / nthreads, part[t].data());
+  }
+  for (int t = 0; t < nthreads; ++t)
+    for (int64_t e = 0; e < In * R; ++e) M[e] += part[t][e];
 }
 
 /* CP-ALS, Algorithm 1 generalised to order N (Q9, Q13):
@@ -549,15 +571,36 @@ static void mttkrp_f64(int order, const int64_t* dims, int64_t nnz, const uint32
  *   stop early if tol > 0 and |fit - fit_prev| < tol ("no improvement").
  * init: order arrays of fp32 I_m x R (given).  out: factors fp64 (caller arrays), lambda[R],
  * fit_trace[iters], returns iterations done (>= 1) or -ORC_ERR_*. */
-int orc_cp_als(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, const float* val, int R, int iters,
-               double tol, const float* const* init, double* const* factors, double* lambda, double* fit_trace) {
+int orc_cp_als_mt(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, const float* val, int R,
+                  int iters, double tol, const float* const* init, double* const* factors, double* lambda,
+                  double* fit_trace, int nthreads) {
   if (order < 2 || order > 8) return -ORC_ERR_ORDER;
   if (R < 1 || iters < 1) return -ORC_ERR_ARG;
   if (nnz == 0) return -ORC_ERR_EMPTY;
   for (int m = 0; m < order; ++m)
     for (int64_t e = 0; e < dims[m] * R; ++e) factors[m][e] = (double)init[m][e];
   std::vector<std::vector<double>> G(order, std::vector<double>((size_t)R * R));
-  for (int m = 0; m < order; ++m) orc_gram(dims[m], R, factors[m], G[m].data());
+  /* Gram U^T U (orc_gram); nthreads > 1: per-thread partials over row ranges, added in thread
+   * order (scale only, same sum) */
+  auto gram_mt = [&](int64_t I, const double* A, double* Gout) {
+    if (nthreads <= 1) { orc_gram(I, R, A, Gout); return; }
+    std::vector<std::vector<double>> part((size_t)nthreads, std::vector<double>((size_t)R * R, 0.0));
+#pragma omp parallel num_threads(nthreads)
+    {
+#ifdef _OPENMP
+      const int t = omp_get_thread_num();
+#else
+      const int t = 0;
+#endif
+      orc_gram(I * (t + 1) / nthreads - I * t / nthreads, R, A + (I * t / nthreads) * R, part[t].data());
+    }
+    for (int a = 0; a < R * R; ++a) {
+      double s2 = 0.0;
+      for (int t = 0; t < nthreads; ++t) s2 += part[t][a];
+      Gout[a] = s2;
+    }
+  };
+  for (int m = 0; m < order; ++m) gram_mt(dims[m], factors[m], G[m].data());
   double xnorm2 = 0.0;
   for (int64_t q = 0; q < nnz; ++q) xnorm2 += (double)val[q] * (double)val[q];
   int64_t Imax = 0;
@@ -567,12 +610,13 @@ int orc_cp_als(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx,
   int it = 0;
   for (; it < iters; ++it) {
     for (int n = 0; n < order; ++n) {
-      mttkrp_f64(order, dims, nnz, idx, val, n, factors, R, M.data());
+      mttkrp_f64(order, dims, nnz, idx, val, n, factors, R, M.data(), nthreads);
       for (int a = 0; a < R * R; ++a) V[a] = 1.0;
       for (int m = 0; m < order; ++m)
         if (m != n)
           for (int a = 0; a < R * R; ++a) V[a] *= G[m][a];
       if (orc_pinv_sym(R, V.data(), P.data()) < 0) return -ORC_ERR_ARG;
+#pragma omp parallel for num_threads(nthreads > 1 ? nthreads : 1)
       for (int64_t i = 0; i < dims[n]; ++i)
         for (int b = 0; b < R; ++b) {
           double s = 0.0;
@@ -580,7 +624,7 @@ int orc_cp_als(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx,
           factors[n][i * R + b] = s;
         }
       orc_normalize(dims[n], R, factors[n], lambda);
-      orc_gram(dims[n], R, factors[n], G[n].data());
+      gram_mt(dims[n], factors[n], G[n].data());
     }
     /* fit after the last mode; M holds MTTKRP of mode N-1 with the current other factors */
     int nl = order - 1;
@@ -604,6 +648,11 @@ int orc_cp_als(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx,
     fit_prev = fit;
   }
   return it;
+}
+
+int orc_cp_als(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, const float* val, int R, int iters,
+               double tol, const float* const* init, double* const* factors, double* lambda, double* fit_trace) {
+  return orc_cp_als_mt(order, dims, nnz, idx, val, R, iters, tol, init, factors, lambda, fit_trace, 1);
 }
 
 } /* extern "C" */

@@ -315,12 +315,18 @@ cudaError_t launch_blocked_one(const BlockedParams& P, int nitems, cudaStream_t 
   constexpr bool FULL = VEC == 4;  // float4 shapes are chosen only when R == 4 * G
   void (*kern)(const BlockedParams) = k_mttkrp_blocked<NP, G, VEC, CPL, ACC, FULL, SMEM, TB, MINB>;
   const size_t smem = (SMEM ? (size_t)P.BR * P.R * 4 : 0) + sizeof(uint32_t) * (size_t)(TB / G) * BStage<NW, G>::STRIDE;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  // carveout: shared memory for the CTAs that fit by registers/threads, the rest stays L1
-  const int ctas = TB == 256 ? 2 : 1;
-  int pct = (int)((ctas * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)) + 1;
-  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
+  // attributes are set when the dynamic shared memory grows (not per call: cheap host path, and
+  // nothing but launches happens while cp_als captures an iteration into a CUDA graph)
+  static size_t configured = 0;
+  if (smem > configured) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    // carveout: shared memory for the CTAs that fit by registers/threads, the rest stays L1
+    const int ctas = TB == 256 ? 2 : 1;
+    int pct = (int)((ctas * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)) + 1;
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
+    configured = smem;
+  }
   if (nitems <= 0) return cudaSuccess;
   kern<<<(unsigned)nitems, TB, smem, s>>>(P);
   count_launch();

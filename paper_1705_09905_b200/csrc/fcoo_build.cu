@@ -255,6 +255,9 @@ void free_handle_arrays(fcoo_s* f) {
   if (f->seg_coord) f->alloc.put(f->seg_coord, f->bytes_seg_coord, s);
   if (f->perm) f->alloc.put(f->perm, f->bytes_perm, s);
   if (f->blk_start) f->alloc.put(f->blk_start, f->bytes_blk, s);
+  if (f->dpart) f->alloc.put(f->dpart, f->bytes_dpart, s);
+  f->dpart = nullptr;
+  f->bytes_dpart = 0;
   for (int k = 0; k < 10; ++k)
     if (f->items[k]) f->alloc.put(f->items[k], sizeof(int2) * f->h_items[k].size(), s);
   for (int k = 0; k < 10; ++k) f->items[k] = nullptr;

@@ -514,11 +514,19 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
   auto cleanup = [&]() { for (auto& h : H) { fcoo_destroy(h); h = nullptr; } };
   struct Guard { decltype(cleanup)& c; ~Guard() { c(); } } guard{cleanup};  // early returns too
   fcoo_build_opts bo{FCOO_OP_MTTKRP, o->tile_nnz > 0 ? o->tile_nnz : 0,
-                     o->deterministic ? FCOO_BUILD_DETERMINISTIC : 0u};
+                     o->deterministic ? FCOO_BUILD_DETERMINISTIC : 0u, 0};
+  fcoo_build_opts bb = bo;
+  bb.flags |= FCOO_BUILD_BLOCKED;
+  const bool try_blocked = !o->deterministic && o->layout == 0 && N <= 5;
   for (int n = 0; n < N; ++n) {
-    fcoo_status st = fcoo_build(X, n, &bo, alloc, (void*)s, &H[n]);
+    fcoo_status st = try_blocked ? fcoo_build(X, n, &bb, alloc, (void*)s, &H[n]) : FCOO_ERR_ARG;
+    if (st == FCOO_ERR_ARG) st = fcoo_build(X, n, &bo, alloc, (void*)s, &H[n]);  // layout not applicable
     if (st) { cleanup(); return st; }
     if (o->comm && o->nranks > 1) fcoo_set_shard(H[n], o->rank, o->nranks, o->comm);
+    if (o->deterministic) {  // reserve the boundary partials now: nothing allocates during capture
+      st = ensure_dpart(H[n], sizeof(double) * (size_t)H[n]->ntiles * 2 * (size_t)R, s);
+      if (st) { cleanup(); return st; }
+    }
   }
   int64_t Imax = 0;
   for (int m = 0; m < N; ++m) Imax = std::max(Imax, X->dims[m]);
@@ -738,10 +746,10 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
       fcoo::g_launches.fetch_sub(captured);  // recorded, not executed
       cudaGraph_t graph = nullptr;
       cudaError_t ce = cudaStreamEndCapture(s, &graph);
-      if (cst) {
+      if (cst) {  // something refused to be captured: run this and every later iteration eagerly
         if (graph) cudaGraphDestroy(graph);
-        st = cst;
-        break;
+        graph = nullptr;
+        ce = cudaErrorStreamCaptureInvalidated;
       }
       if (ce == cudaSuccess && graph) {
         size_t nn = 0;
@@ -782,6 +790,12 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
     if (ce == cudaSuccess) ce = cudaStreamSynchronize(s);
     if (ce != cudaSuccess) st = fail(FCOO_ERR_CUDA, "fit readback: %s", cudaGetErrorString(ce));
   }
+  // the handles are freed stream-ordered on the caller's stream: every kernel enqueued on the
+  // private and side streams must be ordered before that (also on the error paths)
+  cudaEventRecord(side.done, side.st);
+  cudaStreamWaitEvent(s, side.done, 0);
+  cudaEventRecord(join.out, s);
+  cudaStreamWaitEvent(user, join.out, 0);
   cleanup();
   return st;
 }

@@ -30,10 +30,12 @@ __global__ void k_zero_boundary_rows(const uint32_t* __restrict__ sf, const uint
 template <class ACC>
 __global__ void k_combine_boundaries(const uint32_t* __restrict__ sf, const uint32_t* __restrict__ seg_base,
                                      const uint32_t* __restrict__ seg_coord, int64_t ntiles, int64_t tile_begin,
-                                     int64_t tile_end, int R, const ACC* __restrict__ dpart, ACC* __restrict__ out) {
+                                     int64_t tile_end, int R, const ACC* __restrict__ dpart, ACC* __restrict__ out,
+                                     const int* gate, int gate_on) {
   const int64_t t = tile_begin + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / 32;
   const int lane = threadIdx.x & 31;
   if (t >= tile_end) return;
+  if (gate && ((__ldg(gate) != 0) != (gate_on != 0))) return;  // the gated-off MTTKRP wrote no partials
   auto sfbit = [&](int64_t u) { return (sf[u >> 5] >> (u & 31)) & 1u; };
   auto right_open = [&](int64_t u) { return u + 1 < ntiles && !sfbit(u + 1); };
   const uint32_t h0 = seg_base[t], h1 = seg_base[t + 1];  // heads before tile t / before t + 1
@@ -65,12 +67,13 @@ __global__ void k_combine_boundaries(const uint32_t* __restrict__ sf, const uint
 namespace {
 
 template <class ACC>
-fcoo_status combine_boundaries(fcoo_s* f, int R, const ACC* dpart, ACC* out, cudaStream_t s) {
+fcoo_status combine_boundaries(fcoo_s* f, int R, const ACC* dpart, ACC* out, cudaStream_t s, const int* gate = nullptr,
+                               int gate_on = 0) {
   const int64_t nt = f->tile_end - f->tile_begin;
   if (nt <= 0) return FCOO_OK;
   k_combine_boundaries<ACC><<<(unsigned)((nt * 32 + 255) / 256), 256, 0, s>>>(
       f->sf, f->seg_base, (f->op == FCOO_OP_MTTKRP && !f->dense_rows) ? f->seg_coord : nullptr, f->ntiles,
-      f->tile_begin, f->tile_end, R, dpart, out);
+      f->tile_begin, f->tile_end, R, dpart, out, gate, gate_on);
   FCOO_LAUNCH_CHECK();
   return FCOO_OK;
 }
@@ -190,12 +193,23 @@ fcoo_status mttkrp_t(fcoo_s* f, const float* const* factors, int R, ACC* out, cu
   } else if (!vec_ok || R < 16 || engine_env() != 2 || f->n_prod < 2) {
     return fail(FCOO_ERR_ARG, "fused combine needs the staged float4 engine (order >= 3, R %% 4 == 0, 16 <= R <= 128, aligned)");
   }
-  Buf dpart(&f->alloc, f->deterministic ? sizeof(ACC) * (size_t)f->ntiles * 2 * (size_t)R : 0, s);
-  if (!dpart.ok()) return fail(FCOO_ERR_OOM, "deterministic partials");
-  P.dpart = dpart.p;
+  if (f->deterministic) {
+    fcoo_status st = ensure_dpart(f, sizeof(ACC) * (size_t)f->ntiles * 2 * (size_t)R, s);
+    if (st) return st;
+  }
+  P.dpart = f->deterministic ? f->dpart : nullptr;
   cudaError_t e = launch_engine<ACC>(P, f->n_prod, vec_ok, s);
   if (e != cudaSuccess) return fail(FCOO_ERR_CUDA, "mttkrp launch: %s", cudaGetErrorString(e));
-  if (f->deterministic) return combine_boundaries<ACC>(f, R, dpart.as<ACC>(), out, s);
+  if (f->deterministic) return combine_boundaries<ACC>(f, R, reinterpret_cast<const ACC*>(f->dpart), out, s, gate, gate_on);
+  return FCOO_OK;
+}
+
+fcoo_status ensure_dpart(fcoo_s* f, size_t bytes, cudaStream_t s) {
+  if (f->bytes_dpart >= bytes) return FCOO_OK;
+  if (f->dpart) f->alloc.put(f->dpart, f->bytes_dpart, s);
+  f->dpart = f->alloc.get(bytes, s);
+  f->bytes_dpart = f->dpart ? bytes : 0;
+  if (!f->dpart) return fail(FCOO_ERR_OOM, "deterministic partials (%zu bytes)", bytes);
   return FCOO_OK;
 }
 
@@ -250,13 +264,15 @@ fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s
   P.T = (int)f->T; P.R = R; P.out = out;
   fcoo_status st = prepare_output<float>(f, R, out, f->nsegs, true, s);
   if (st) return st;
-  Buf dpart(&f->alloc, f->deterministic ? sizeof(float) * (size_t)f->ntiles * 2 * (size_t)R : 0, s);
-  if (!dpart.ok()) return fail(FCOO_ERR_OOM, "deterministic partials");
-  P.dpart = dpart.p;
+  if (f->deterministic) {
+    st = ensure_dpart(f, sizeof(float) * (size_t)f->ntiles * 2 * (size_t)R, s);
+    if (st) return st;
+  }
+  P.dpart = f->deterministic ? f->dpart : nullptr;
   cudaError_t e = launch_engine<float>(P, 1, vec_ok, s);
   if (e != cudaSuccess) return fail(FCOO_ERR_CUDA, "ttm launch: %s", cudaGetErrorString(e));
   if (f->deterministic) {
-    st = combine_boundaries<float>(f, R, dpart.as<float>(), out, s);
+    st = combine_boundaries<float>(f, R, reinterpret_cast<const float*>(f->dpart), out, s);
     if (st) return st;
   }
   if (f->comm) return comm_allreduce(f->comm, out, (size_t)f->nsegs * R, s);

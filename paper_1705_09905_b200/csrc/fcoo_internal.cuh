@@ -75,6 +75,11 @@ struct fcoo_s {
   // item = (block b, first tile t0), t0 = first tile of b + j*gpc; device int2 + host copy
   int2* items[10] = {nullptr};
   std::vector<int2> h_items[10];
+  // deterministic handles: the per-tile boundary partials (2 x R x sizeof(ACC) per tile), kept
+  // by the handle and grown on demand (fcoo::ensure_dpart) so no call allocates inside a CUDA
+  // graph capture (cp_als reserves the largest size it needs before capturing)
+  void* dpart = nullptr;
+  size_t bytes_dpart = 0;
   // shard
   int shard = 0, nshards = 1;
   int64_t tile_begin = 0, tile_end = 0;
@@ -99,6 +104,8 @@ fcoo_status comm_barrier(fcoo_comm_t comm, cudaStream_t s);
 void mc_views(fcoo_mc_t m, float** uc, float** mc, size_t* bytes, fcoo_comm_t* comm);
 fcoo_status run_mttkrp_mc(fcoo_s* f, const float* const* factors, int R, fcoo_mc_t out, cudaStream_t s);
 fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s);
+// deterministic handles: make f->dpart hold at least `bytes` (stream-ordered on s)
+fcoo_status ensure_dpart(fcoo_s* f, size_t bytes, cudaStream_t s);
 fcoo_status run_ttmc(fcoo_s* f, const float* const* factors, const int* ranks, float* out, cudaStream_t s);
 }  // namespace fcoo
 

@@ -113,3 +113,19 @@ def test_rank_above_extent():
     idx, val = gen.coo(dims, 120, None, 701)
     _, _, trace = oracle.cp_als(dims, idx, val, 5, 10, _init(dims, 5, 702))
     assert np.all(np.isfinite(trace)) and np.all(np.diff(trace) >= -1e-7)
+
+
+def test_threads_agree():
+    """The multi-threaded CP oracle (private per-thread MTTKRP partials merged in thread order, used
+    at configuration-5 scale) computes the same iteration as the single-threaded one up to rounding
+    order: fit traces within 1e-12, factors and lambda within 1e-9 relative."""
+    dims = (60, 50, 40, 30)
+    idx, val = gen.coo(dims, 20000, (0.5, 0.5, 0.5, 0.5), 61)
+    R = 8
+    init = gen.factors(dims, R, 62)
+    f1, l1, t1 = oracle.cp_als(dims, idx, val, R, 4, init, nthreads=1)
+    f4, l4, t4 = oracle.cp_als(dims, idx, val, R, 4, init, nthreads=4)
+    assert np.allclose(t1, t4, rtol=0, atol=1e-12)
+    assert np.allclose(l1, l4, rtol=1e-9, atol=0)
+    for a, b in zip(f1, f4):
+        assert np.allclose(a, b, rtol=1e-9, atol=1e-12)
