@@ -264,6 +264,11 @@ fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s
   P.T = (int)f->T; P.R = R; P.out = out;
   fcoo_status st = prepare_output<float>(f, R, out, f->nsegs, true, s);
   if (st) return st;
+  if (run_ttm_lean(f, U, R, out, s, &st)) {  // fcoo_ttm.cu: the specialised SpTTM kernel
+    if (st) return st;
+    if (f->comm) return comm_allreduce(f->comm, out, (size_t)f->nsegs * R, s);
+    return FCOO_OK;
+  }
   if (f->deterministic) {
     st = ensure_dpart(f, sizeof(float) * (size_t)f->ntiles * 2 * (size_t)R, s);
     if (st) return st;

@@ -104,6 +104,8 @@ fcoo_status comm_barrier(fcoo_comm_t comm, cudaStream_t s);
 void mc_views(fcoo_mc_t m, float** uc, float** mc, size_t* bytes, fcoo_comm_t* comm);
 fcoo_status run_mttkrp_mc(fcoo_s* f, const float* const* factors, int R, fcoo_mc_t out, cudaStream_t s);
 fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s);
+// SpTTM through the specialised kernel (fcoo_ttm.cu) when it applies; false = use the engine
+bool run_ttm_lean(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s, fcoo_status* st);
 // deterministic handles: make f->dpart hold at least `bytes` (stream-ordered on s)
 fcoo_status ensure_dpart(fcoo_s* f, size_t bytes, cudaStream_t s);
 fcoo_status run_ttmc(fcoo_s* f, const float* const* factors, const int* ranks, float* out, cudaStream_t s);

@@ -71,9 +71,32 @@ def test_order4_and_shards(F):
         _check(F, dims, idx, val, mode, 16, T=32, shards=3)
 
 
-def test_brainq_shaped_full_size(F):
-    """BASELINE configs[3]: brainq-shaped (60 x 70K x 9, 11M nnz), SpTTM every mode, R=16."""
+@pytest.mark.parametrize("T", [0, 2048])
+def test_brainq_shaped_full_size(F, T):
+    """BASELINE configs[3]: brainq-shaped (60 x 70K x 9, 11M nnz), SpTTM every mode, R=16, at the
+    automatic tile (T = 0: the one the timed path uses) and at T = 2048."""
     w = gen.WORKLOADS["brainq"]
     idx, val = gen.coo(w.dims, w.nnz, w.alpha, w.seed)
     for mode in range(3):
-        _check(F, w.dims, idx, val, mode, 16, T=2048)
+        _check(F, w.dims, idx, val, mode, 16, T=T)
+
+
+@pytest.mark.parametrize("R", [8, 16, 32, 64, 128])
+def test_lean_kernel_shapes(F, R):
+    """The specialised SpTTM kernel (fcoo_ttm.cu) for every float4 shape R = 4G, with the factor in
+    shared memory (mode 0/2: 60 and 9 rows) and gathered from global memory (mode 1); T = 32 so
+    fibres cross many tiles, plus tile-aligned shards."""
+    dims = (60, 3000, 9)
+    idx, val = gen.coo(dims, 50000, (0.3, 0.0, 0.6), 79)
+    for mode in range(3):
+        _check(F, dims, idx, val, mode, R, T=32)
+        _check(F, dims, idx, val, mode, R, T=64, shards=3)
+
+
+def test_long_and_singleton_fibres(F):
+    """One fibre spanning every tile (mode 1 of a 1 x N x 1 tensor) and all-singleton fibres."""
+    n = 30000
+    v = gen.uniform((n,), 5, 0) + 0.5
+    one = np.stack([np.zeros(n, np.uint32), np.arange(n, dtype=np.uint32), np.zeros(n, np.uint32)])
+    _check(F, (1, n, 1), one, v, 1, 16, T=32, signed=False)
+    _check(F, (1, n, 1), one, v, 0, 16, T=64)
