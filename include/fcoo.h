@@ -215,6 +215,16 @@ typedef struct {
 /* fcoo_export — copy the handle's arrays to host buffers; synchronises `stream`. */
 fcoo_status fcoo_export(fcoo_t f, fcoo_host_view* view, void* stream);
 
+/* fcoo_debug_flip_bit — TEST SUPPORT: flip bit `bit` of the handle's device
+ * bf array (which = 0; bit < stream length) or sf array (which = 1; bit < ntiles), synchronously, so
+ * a test can show that the parity checks detect a corrupted flag.  The handle's results are wrong
+ * afterwards (flip the same bit again to restore it).  Only flips that keep every kernel
+ * memory-safe are allowed: clearing a bf head (a segment ordinal can only lag) and restoring a head
+ * cleared this way, and flipping an sf bit of an MTTKRP handle; setting any other bf bit or touching
+ * sf of an SpTTM handle could index past the segment table and is rejected (ARG).  Errors: ARG (NULL, bit out of range, which not 0/1, a
+ * rejected flip), CUDA. */
+fcoo_status fcoo_debug_flip_bit(fcoo_t f, int which, int64_t bit);
+
 /* fcoo_destroy — free the handle (stream-ordered frees on the build stream). NULL is OK. */
 fcoo_status fcoo_destroy(fcoo_t f);
 

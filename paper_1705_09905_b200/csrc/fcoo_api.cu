@@ -228,6 +228,29 @@ fcoo_status fcoo_export(fcoo_t f, fcoo_host_view* v, void* stream) {
   return FCOO_OK;
 }
 
+fcoo_status fcoo_debug_flip_bit(fcoo_t f, int which, int64_t bit) {
+  if (!f) return fcoo::fail(FCOO_ERR_ARG, "NULL handle");
+  const int64_t n = which == 0 ? f->nnz_pad : which == 1 ? f->ntiles : -1;
+  if (n < 0) return fcoo::fail(FCOO_ERR_ARG, "which must be 0 (bf) or 1 (sf)");
+  if (bit < 0 || bit >= n) return fcoo::fail(FCOO_ERR_ARG, "bit %lld outside [0, %lld)", (long long)bit, (long long)n);
+  uint32_t* word = (which == 0 ? f->bf : f->sf) + (bit >> 5);
+  uint32_t w = 0;
+  FCOO_CUDA_TRY(cudaMemcpy(&w, word, 4, cudaMemcpyDeviceToHost));
+  if (which == 0 && !((w >> (bit & 31)) & 1u)) {  // setting: only to restore a head this call cleared
+    auto it = std::find(f->debug_cleared.begin(), f->debug_cleared.end(), bit);
+    if (it == f->debug_cleared.end())
+      return fcoo::fail(FCOO_ERR_ARG, "setting a bf bit is not memory-safe (only cleared heads can be restored)");
+    f->debug_cleared.erase(it);
+  } else if (which == 0) {
+    f->debug_cleared.push_back(bit);
+  }
+  if (which == 1 && f->op != FCOO_OP_MTTKRP)
+    return fcoo::fail(FCOO_ERR_ARG, "sf flips are supported on MTTKRP handles only");
+  w ^= 1u << (bit & 31);
+  FCOO_CUDA_TRY(cudaMemcpy(word, &w, 4, cudaMemcpyHostToDevice));
+  return FCOO_OK;
+}
+
 fcoo_status fcoo_destroy(fcoo_t f) {
   fcoo::destroy_impl(f);
   return FCOO_OK;

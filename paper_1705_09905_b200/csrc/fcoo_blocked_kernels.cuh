@@ -180,9 +180,9 @@ __global__ void __launch_bounds__(TB, MINB) k_mttkrp_blocked(const BlockedParams
   ACC* const outp = reinterpret_cast<ACC*>(P.out);
   float* const mcp = P.out_mc;
 
-  AT acc[CPL];
+  AT acc[CPL], hi[CPL];  // hi: the chain-capped part of the running segment (chain_fold)
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
+  for (int c = 0; c < CPL; ++c) acc[c] = hi[c] = A::zero();
   auto flush = [&]() {
 #pragma unroll
     for (int c = 0; c < CPL; ++c)
@@ -266,6 +266,8 @@ __global__ void __launch_bounds__(TB, MINB) k_mttkrp_blocked(const BlockedParams
       } else {
         const bool first = (ci == 0 && bi == 0);
 #pragma unroll
+        for (int c = 0; c < CPL; ++c) chain_absorb(acc[c], hi[c]);
+#pragma unroll
         for (int e = 0; e < B; ++e) {
           if ((heads >> e) & 1u) {
             if (e != 0 || !first) flush();
@@ -279,9 +281,15 @@ __global__ void __launch_bounds__(TB, MINB) k_mttkrp_blocked(const BlockedParams
         }
       }
     }
+    if (ci % kChainChunks == kChainChunks - 1) {
+#pragma unroll
+      for (int c = 0; c < CPL; ++c) chain_fold(hi[c], acc[c]);
+    }
     __syncwarp(gmask);  // every lane is done with this stage before it is refilled
   }
   if (!live) return;
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) chain_absorb(acc[c], hi[c]);
   // ragged end of a block's last tile: one nonzero at a time
   for (int64_t p = p0 + (int64_t)nchunk * CH; p < pend; ++p) {
     if ((P.bf[p >> 5] >> (p & 31)) & 1u) {

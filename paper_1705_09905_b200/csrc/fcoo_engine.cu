@@ -93,11 +93,6 @@ cudaError_t launch_engine(const EngineParams& P, int NP, bool vec_ok, cudaStream
 
 bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
 
-// FCOO_ENGINE as launch_one reads it (2 = staged, the default)
-int engine_env() {
-  const char* e = getenv("FCOO_ENGINE");
-  return e ? atoi(e) : 2;
-}
 
 template <class ACC>
 fcoo_status prepare_output(fcoo_s* f, int R, ACC* out, int64_t rows, bool all_rows_are_segments, cudaStream_t s) {
@@ -190,7 +185,7 @@ fcoo_status mttkrp_t(fcoo_s* f, const float* const* factors, int R, ACC* out, cu
   if (!out_mc) {
     fcoo_status st = prepare_output<ACC>(f, R, out, f->dims[f->mode], f->dense_rows != 0, s);
     if (st) return st;
-  } else if (!vec_ok || R < 16 || engine_env() != 2 || f->n_prod < 2) {
+  } else if (!vec_ok || R < 16 || f->n_prod < 2) {  // the staged float4 kernel (G = R/4 >= 4 lanes)
     return fail(FCOO_ERR_ARG, "fused combine needs the staged float4 engine (order >= 3, R %% 4 == 0, 16 <= R <= 128, aligned)");
   }
   if (f->deterministic) {

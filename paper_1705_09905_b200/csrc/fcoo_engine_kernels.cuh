@@ -62,12 +62,7 @@ __device__ __forceinline__ void ld_batch(const void* p, uint32_t (&w)[B]) {
 template <int NP, int VEC, int CPL>
 constexpr int batch_size() {
   constexpr int regs = NP * VEC * CPL;
-#ifdef FCOO_BATCH_MAX  // experiment builds: cap the batch (memory-level-parallelism probe)
-  constexpr int b = regs * 8 <= 64 ? 8 : regs * 4 <= 64 ? 4 : regs * 2 <= 64 ? 2 : 1;
-  return b < FCOO_BATCH_MAX ? b : FCOO_BATCH_MAX;
-#else
   return regs * 8 <= 64 ? 8 : regs * 4 <= 64 ? 4 : regs * 2 <= 64 ? 2 : 1;
-#endif
 }
 
 __device__ __forceinline__ void red_add_v4(float* p, float4 v) {
@@ -125,6 +120,27 @@ __device__ __forceinline__ void store2_if(bool s0, float* p0, bool s1, float* p1
       : "memory");
 }
 
+// Accumulation-chain cap (DESIGN.md §2 Q16): a lane-group's fp32 partial of a segment is folded
+// into a second register set every kChainChunks x 32 = 256 nonzeros (chain_fold), and the two are
+// re-joined before any flush (chain_absorb), so no sequential fp32 chain inside a tile is longer
+// than 256 + T/256 + 8 additions: per-element error <= (264 + T/256 + k) u * sum|contributions|
+// for a segment split over k tiles (u = 2^-24).  fp64 accumulators (CP fit mode) need no cap.
+constexpr int kChainChunks = 8;
+__device__ __forceinline__ void chain_fold(float4& hi, float4& acc) {
+  hi = make_float4(hi.x + acc.x, hi.y + acc.y, hi.z + acc.z, hi.w + acc.w);
+  acc = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ void chain_absorb(float4& acc, float4& hi) {
+  acc = make_float4(acc.x + hi.x, acc.y + hi.y, acc.z + hi.z, acc.w + hi.w);
+  hi = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+__device__ __forceinline__ void chain_fold(float& hi, float& acc) { hi += acc; acc = 0.f; }
+__device__ __forceinline__ void chain_absorb(float& acc, float& hi) { acc += hi; hi = 0.f; }
+template <class T>
+__device__ __forceinline__ void chain_fold(T&, T&) {}
+template <class T>
+__device__ __forceinline__ void chain_absorb(T&, T&) {}
+
 // Per-lane column slot: VEC consecutive fp32 factor entries (float4 on the vector path) and an
 // accumulator of type ACC (fp32 for the product path; fp64 for the CP-ALS fit mode, where the
 // identity-based fit needs the inner product <X, Xhat> to ~1e-12).
@@ -135,65 +151,22 @@ struct Ld<4> {
   using T = float4;
   static __device__ __forceinline__ T zero() { return make_float4(0.f, 0.f, 0.f, 0.f); }
   static __device__ __forceinline__ T load(const float* p) { return __ldg(reinterpret_cast<const float4*>(p)); }
-  // Gather with an L1 eviction policy: 0 default, 1 no_allocate, 2 evict_first, 3 evict_last.
-  template <int POL>
-  static __device__ __forceinline__ T load_pol(const float* p) {
-    if constexpr (POL == 0) {
-      return load(p);
-    } else {
-      T r;
-      if constexpr (POL == 1)
-        asm("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
-      else if constexpr (POL == 2)
-        asm("ld.global.nc.L1::evict_first.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
-      else
-        asm("ld.global.nc.L1::evict_last.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
-      return r;
-    }
-  }
-  // Predicated gather into fresh registers (opaque to the compiler, so it cannot fold the
-  // "keep the previous row" select into a chain of moves that waits on earlier loads).
-  static __device__ __forceinline__ T load_if(bool pred, const float* p) {
-    T r;
-    asm volatile(
-        "{ .reg .pred q; setp.ne.b32 q, %4, 0;\n"
-        "  mov.b32 %0, 0; mov.b32 %1, 0; mov.b32 %2, 0; mov.b32 %3, 0;\n"
-        "  @q ld.global.nc.v4.f32 {%0,%1,%2,%3}, [%5]; }"
-        : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
-        : "r"((int)pred), "l"(p));
-    return r;
-  }
 };
 template <>
 struct Ld<1> {
   using T = float;
   static __device__ __forceinline__ T zero() { return 0.f; }
   static __device__ __forceinline__ T load(const float* p) { return __ldg(p); }
-  template <int POL>
-  static __device__ __forceinline__ T load_pol(const float* p) { return load(p); }
-  static __device__ __forceinline__ T load_if(bool pred, const float* p) {
-    T r;
-    asm volatile(
-        "{ .reg .pred q; setp.ne.b32 q, %1, 0;\n"
-        "  mov.b32 %0, 0;\n"
-        "  @q ld.global.nc.f32 %0, [%2]; }"
-        : "=f"(r)
-        : "r"((int)pred), "l"(p));
-    return r;
-  }
 };
 
 // fp64 accumulator (CP fit mode).  Products are formed in fp64 (exact for two fp32 factors)
 // because the fit identity needs <X, Xhat> to ~1e-10 relative near fit = 1: an fp32 product
-// rounding (2^-24 per term) left a ~1e-4 jitter in the fit of small converged problems.  The
-// `part` slot (settle()) is an fp32 staging partial kept for experiments; add() does not use it.
+// rounding (2^-24 per term) left a ~1e-4 jitter in the fit of small converged problems.
 struct d4 {
   double x, y, z, w;
-  float4 part;
 };
 struct d1 {
   double x;
-  float part;
 };
 
 template <int VEC, class ACC>
@@ -219,7 +192,6 @@ struct Acc<4, float> {
   static __device__ __forceinline__ void fold(T& acc, const T& t, float4 r0) {  // acc += t * r0
     acc = make_float4(fmaf(t.x, r0.x, acc.x), fmaf(t.y, r0.y, acc.y), fmaf(t.z, r0.z, acc.z), fmaf(t.w, r0.w, acc.w));
   }
-  static __device__ __forceinline__ void settle(T&) {}
   static __device__ __forceinline__ void store(float* p, T v) { *reinterpret_cast<float4*>(p) = v; }
   static __device__ __forceinline__ void red(float* p, T v) { red_add_v4(p, v); }
 };
@@ -242,14 +214,13 @@ struct Acc<1, float> {
     t = fmaf(v, h, t);
   }
   static __device__ __forceinline__ void fold(T& acc, const T& t, float r0) { acc = fmaf(t, r0, acc); }
-  static __device__ __forceinline__ void settle(T&) {}
   static __device__ __forceinline__ void store(float* p, T v) { *p = v; }
   static __device__ __forceinline__ void red(float* p, T v) { atomicAdd(p, v); }
 };
 template <>
 struct Acc<4, double> {
   using T = d4;
-  static __device__ __forceinline__ T zero() { return d4{0.0, 0.0, 0.0, 0.0, make_float4(0.f, 0.f, 0.f, 0.f)}; }
+  static __device__ __forceinline__ T zero() { return d4{0.0, 0.0, 0.0, 0.0}; }
   template <int NP>
   static __device__ __forceinline__ void add(T& acc, float v, const float4 (&r)[NP]) {
     // products in fp64: r0*r1 of two fp32 values is exact, v*(r0*r1) rounds once at 2^-53
@@ -258,10 +229,6 @@ struct Acc<4, double> {
     for (int a = 1; a < NP; ++a) { hx *= (double)r[a].x; hy *= (double)r[a].y; hz *= (double)r[a].z; hw *= (double)r[a].w; }
     const double dv = v;
     acc.x = fma(dv, hx, acc.x); acc.y = fma(dv, hy, acc.y); acc.z = fma(dv, hz, acc.z); acc.w = fma(dv, hw, acc.w);
-  }
-  static __device__ __forceinline__ void settle(T& acc) {
-    acc.x += (double)acc.part.x; acc.y += (double)acc.part.y; acc.z += (double)acc.part.z; acc.w += (double)acc.part.w;
-    acc.part = make_float4(0.f, 0.f, 0.f, 0.f);
   }
   template <int NP>
   static __device__ __forceinline__ void add_inner(T& t, float v, const float4 (&r)[NP]) {
@@ -276,29 +243,23 @@ struct Acc<4, double> {
     acc.z = fma(t.z, (double)r0.z, acc.z); acc.w = fma(t.w, (double)r0.w, acc.w);
   }
   static __device__ __forceinline__ void store(double* p, T v) {
-    settle(v);
     reinterpret_cast<double2*>(p)[0] = make_double2(v.x, v.y);
     reinterpret_cast<double2*>(p)[1] = make_double2(v.z, v.w);
   }
   static __device__ __forceinline__ void red(double* p, T v) {
-    settle(v);
     atomicAdd(p, v.x); atomicAdd(p + 1, v.y); atomicAdd(p + 2, v.z); atomicAdd(p + 3, v.w);
   }
 };
 template <>
 struct Acc<1, double> {
   using T = d1;
-  static __device__ __forceinline__ T zero() { return d1{0.0, 0.f}; }
+  static __device__ __forceinline__ T zero() { return d1{0.0}; }
   template <int NP>
   static __device__ __forceinline__ void add(T& acc, float v, const float (&r)[NP]) {
     double h = r[0];
 #pragma unroll
     for (int a = 1; a < NP; ++a) h *= (double)r[a];
     acc.x = fma((double)v, h, acc.x);
-  }
-  static __device__ __forceinline__ void settle(T& acc) {
-    acc.x += (double)acc.part;
-    acc.part = 0.f;
   }
   template <int NP>
   static __device__ __forceinline__ void add_inner(T& t, float v, const float (&r)[NP]) {
@@ -309,11 +270,9 @@ struct Acc<1, double> {
   }
   static __device__ __forceinline__ void fold(T& acc, const T& t, float r0) { acc.x = fma(t.x, (double)r0, acc.x); }
   static __device__ __forceinline__ void store(double* p, T v) {
-    settle(v);
     *p = v.x;
   }
   static __device__ __forceinline__ void red(double* p, T v) {
-    settle(v);
     atomicAdd(p, v.x);
   }
 };
@@ -366,9 +325,9 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
   if (left_open) row = P.seg_coord ? (int64_t)P.seg_coord[s] : s;
   bool own = false;  // did the current segment start inside this tile?
 
-  AT acc[CPL];
+  AT acc[CPL], hi[CPL];  // hi: the chain-capped part of the running segment (chain_fold)
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
+  for (int c = 0; c < CPL; ++c) acc[c] = hi[c] = A::zero();
   auto flush = [&](bool store) {
     ACC* o = reinterpret_cast<ACC*>(P.out) + row * (int64_t)R;
     // deterministic handles: a shared segment goes to the tile's partial slot (0: left-open first
@@ -415,15 +374,21 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
         for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), r[e][c]);
     } else {
 #pragma unroll
+      for (int c = 0; c < CPL; ++c) chain_absorb(acc[c], hi[c]);
+#pragma unroll
       for (int e = 0; e < B; ++e) {
         if ((heads >> e) & 1u) open_segment(pb + e);
 #pragma unroll
         for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), r[e][c]);
       }
     }
+    if (((pb - p0 + B) & (kChainChunks * 32 - 1)) == 0) {
 #pragma unroll
-    for (int c = 0; c < CPL; ++c) A::settle(acc[c]);
+      for (int c = 0; c < CPL; ++c) chain_fold(hi[c], acc[c]);
+    }
   }
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) chain_absorb(acc[c], hi[c]);
   // ragged tail of the tensor's last tile: one nonzero at a time
   for (int64_t p = pfull; p < p1; ++p) {
     if ((p & 31) == 0 || p == pfull) bfw = ld_stream4(P.bf + (p >> 5));
@@ -440,171 +405,6 @@ __global__ void __launch_bounds__(256) k_segreduce(const EngineParams P) {
 #pragma unroll
     for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], v, r1[c]);
   }
-  const bool right_open = (t + 1 < P.ntiles) && !((P.sf[(t + 1) >> 5] >> ((t + 1) & 31)) & 1u);
-  flush(own && !right_open);
-}
-
-// Factored variant (NP >= 2): CSF-style reuse of the outer (first, sorted) product mode.  Within a
-// segment the nonzeros are ordered by the product modes (reading Q5), so consecutive nonzeros
-// often share the outer index j.  For such a run, acc += U_0(j,:) * sum_run v * prod_{a>=1} U_a:
-// the run accumulator t collects the inner products and is folded into acc (one FFMA per column)
-// when the outer index changes or a segment head arrives; the outer row is gathered once per run
-// instead of once per nonzero.  This is the "data reuse" the paper lists among its GPU
-// optimisations applied to the F-COO stream; same sum, regrouped (error bound
-// unchanged: |fl(sum) - sum| <= gamma_n * sum |contributions|).
-template <int NP, int G, int VEC, int CPL, class ACC, bool FULL>
-__global__ void __launch_bounds__(256) k_segreduce_fact(const EngineParams P) {
-  static_assert(NP >= 2, "factored variant needs an outer and an inner product mode");
-  using V = Ld<VEC>;
-  using VT = typename V::T;
-  using A = Acc<VEC, ACC>;
-  using AT = typename A::T;
-  constexpr int B = batch_size<NP, VEC, CPL>();
-  const int gl = threadIdx.x % G;
-  const int64_t t = P.tile_begin + ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / G;
-  if (t >= P.tile_end || gated_off(P)) return;
-
-  const int R = P.R;
-  const uint32_t rowb = (uint32_t)R * 4u;
-  int col[CPL];
-  bool cok[CPL];
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    col[c] = (gl + G * c) * VEC;
-    cok[c] = FULL || col[c] < R;
-  }
-  const char* ub[NP][CPL];
-#pragma unroll
-  for (int a = 0; a < NP; ++a)
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) ub[a][c] = reinterpret_cast<const char*>(P.U[a] + (cok[c] ? col[c] : 0));
-
-  const int64_t p0 = t * (int64_t)P.T;
-  const int64_t p1 = min(p0 + (int64_t)P.T, P.nnz);
-  const int64_t pfull = p0 + ((p1 - p0) / B) * B;
-
-  const bool left_open = !((P.sf[t >> 5] >> (t & 31)) & 1u);
-  int64_t s = (int64_t)P.seg_base[t] - 1;
-  int64_t row = 0;
-  if (left_open) row = P.seg_coord ? (int64_t)P.seg_coord[s] : s;
-  bool own = false;
-
-  AT acc[CPL], run[CPL];
-  VT bcur[CPL];
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) {
-    acc[c] = A::zero();
-    run[c] = A::zero();
-    bcur[c] = V::zero();
-  }
-  uint32_t prev0 = 0xffffffffu;
-
-  auto flush = [&](bool store) {
-    ACC* o = reinterpret_cast<ACC*>(P.out) + row * (int64_t)R;
-    // deterministic handles: a shared segment goes to the tile's partial slot (0: left-open first
-    // segment, 1: own right-open last segment), combined later in tile order
-    ACC* dp = P.dpart ? reinterpret_cast<ACC*>(P.dpart) + ((size_t)t * 2 + (own ? 1 : 0)) * (uint32_t)R : nullptr;
-#pragma unroll
-    for (int c = 0; c < CPL; ++c)
-      if (cok[c]) {
-        if (store) A::store(o + col[c], acc[c]);
-        else if (dp) A::store(dp + col[c], acc[c]);
-        else A::red(o + col[c], acc[c]);
-      }
-  };
-  auto open_segment = [&](int64_t p) {
-    if (p != p0) flush(own);
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
-    own = true;
-    ++s;
-    row = P.seg_coord ? (int64_t)P.seg_coord[s] : s;
-  };
-
-  uint32_t bfw = 0;
-  for (int64_t pb = p0; pb < pfull; pb += B) {
-    if (((pb - p0) & 31) == 0) bfw = ld_stream4(P.bf + (pb >> 5));
-    uint32_t ix[NP][B];
-    uint32_t vb[B];
-#pragma unroll
-    for (int a = 0; a < NP; ++a) ld_batch<B>(P.pidx[a] + pb, ix[a]);
-    ld_batch<B>(P.val + pb, vb);
-    const uint32_t heads = (bfw >> ((pb - p0) & 31)) & ((1u << B) - 1u);
-    bool nr[B];  // a new run starts at e: outer index changes or a segment head
-#pragma unroll
-    for (int e = 0; e < B; ++e) nr[e] = (ix[0][e] != (e ? ix[0][e - 1] : prev0)) || ((heads >> e) & 1u);
-    prev0 = ix[0][B - 1];
-    VT r[B][CPL][NP];
-#pragma unroll
-    for (int e = 0; e < B; ++e)
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        r[e][c][0] = V::load_if(nr[e] && cok[c], reinterpret_cast<const float*>(ub[0][c] + (size_t)ix[0][e] * rowb));
-#pragma unroll
-        for (int a = 1; a < NP; ++a)
-          r[e][c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(ub[a][c] + (size_t)ix[a][e] * rowb)) : V::zero();
-      }
-    if (heads == 0) {  // common case: no segment boundary in the batch, straight-line code
-#pragma unroll
-      for (int e = 0; e < B; ++e) {
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) {
-          if (nr[e]) {
-            A::fold(acc[c], run[c], bcur[c]);
-            run[c] = A::zero();
-            bcur[c] = r[e][c][0];
-          }
-          A::template add_inner<NP>(run[c], __uint_as_float(vb[e]), r[e][c]);
-        }
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < B; ++e) {
-        if (nr[e]) {
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) {
-            A::fold(acc[c], run[c], bcur[c]);
-            run[c] = A::zero();
-          }
-        }
-        if ((heads >> e) & 1u) open_segment(pb + e);
-        if (nr[e]) {
-#pragma unroll
-          for (int c = 0; c < CPL; ++c) bcur[c] = r[e][c][0];
-        }
-#pragma unroll
-        for (int c = 0; c < CPL; ++c) A::template add_inner<NP>(run[c], __uint_as_float(vb[e]), r[e][c]);
-      }
-    }
-  }
-  for (int64_t p = pfull; p < p1; ++p) {  // ragged tail of the last tile
-    if ((p & 31) == 0 || p == pfull) bfw = ld_stream4(P.bf + (p >> 5));
-    const bool head = (bfw >> (p & 31)) & 1u;
-    const float v = __uint_as_float(ld_stream4(P.val + p));
-    uint32_t i0 = ld_stream4(P.pidx[0] + p);
-    VT r1[CPL][NP];
-#pragma unroll
-    for (int a = 0; a < NP; ++a) {
-      uint32_t i = a ? ld_stream4(P.pidx[a] + p) : i0;
-#pragma unroll
-      for (int c = 0; c < CPL; ++c)
-        r1[c][a] = cok[c] ? V::load(reinterpret_cast<const float*>(ub[a][c] + (size_t)i * rowb)) : V::zero();
-    }
-    if (head || i0 != prev0) {
-#pragma unroll
-      for (int c = 0; c < CPL; ++c) {
-        A::fold(acc[c], run[c], bcur[c]);
-        run[c] = A::zero();
-        bcur[c] = r1[c][0];
-      }
-    }
-    prev0 = i0;
-    if (head) open_segment(p);
-#pragma unroll
-    for (int c = 0; c < CPL; ++c) A::template add_inner<NP>(run[c], v, r1[c]);
-  }
-#pragma unroll
-  for (int c = 0; c < CPL; ++c) A::fold(acc[c], run[c], bcur[c]);
   const bool right_open = (t + 1 < P.ntiles) && !((P.sf[(t + 1) >> 5] >> ((t + 1) & 31)) & 1u);
   flush(own && !right_open);
 }
@@ -656,14 +456,6 @@ struct Stage {
 // exposed.  This is the "shared-memory staging of the nonzero stream" of the north star; the
 // factor rows still go through L1 (most of the unified carveout stays L1).
 template <int NP, int G, int VEC, int CPL, class ACC, bool FULL, bool DET>
-// L1 policy of the factor-row gathers in the staged kernel (see Ld<4>::load_pol): the last
-// product position is the per-nonzero random gather, the others are sorted within a segment.
-#ifndef FCOO_L1POL_INNER
-#define FCOO_L1POL_INNER 0
-#endif
-#ifndef FCOO_L1POL_OUTER
-#define FCOO_L1POL_OUTER 0
-#endif
 __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) {
   using V = Ld<VEC>;
   using VT = typename V::T;
@@ -708,9 +500,9 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
   bool own = false;
   ACC* const outp = reinterpret_cast<ACC*>(P.out);
 
-  AT acc[CPL];
+  AT acc[CPL], hi[CPL];  // hi: the chain-capped part of the running segment (chain_fold)
 #pragma unroll
-  for (int c = 0; c < CPL; ++c) acc[c] = A::zero();
+  for (int c = 0; c < CPL; ++c) acc[c] = hi[c] = A::zero();
   float* const mcp = NP >= 2 ? P.out_mc : nullptr;  // fused combine (float4 fp32, order >= 3; host checks)
   // deterministic handles, branch-free path: the only shared flush there is the left-open segment,
   // to slot 0 of this tile (address formed at the flush from the kernel parameter)
@@ -784,9 +576,7 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
 #pragma unroll
           for (int c = 0; c < CPL; ++c) {
             const float* gp = reinterpret_cast<const float*>(ub[a][c] + (size_t)ix[a][e] * rowb);
-            r[e][c][a] = !cok[c] ? V::zero()
-                         : (a == NP - 1) ? V::template load_pol<FCOO_L1POL_INNER>(gp)
-                                         : V::template load_pol<FCOO_L1POL_OUTER>(gp);
+            r[e][c][a] = !cok[c] ? V::zero() : V::load(gp);
           }
       if (heads == 0) {
 #pragma unroll
@@ -794,6 +584,8 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
 #pragma unroll
           for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), r[e][c]);
       } else if constexpr (std::is_same<ACC, float>::value) {
+#pragma unroll
+        for (int c = 0; c < CPL; ++c) chain_absorb(acc[c], hi[c]);
         // branch-free segment handling (short segments, e.g. SpTTM fibres): at a head the running
         // segment is flushed by a predicated store (owned) or red.add (shared with the left tile),
         // the accumulator is reset by select and the segment ordinal advances by the head bit
@@ -842,11 +634,15 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
           for (int c = 0; c < CPL; ++c) A::template add<NP>(acc[c], __uint_as_float(vb[e]), r[e][c]);
         }
       }
+    }
+    if (ci % kChainChunks == kChainChunks - 1) {
 #pragma unroll
-      for (int c = 0; c < CPL; ++c) A::settle(acc[c]);
+      for (int c = 0; c < CPL; ++c) chain_fold(hi[c], acc[c]);
     }
     __syncwarp(gmask);  // every lane is done with this stage before it is refilled
   }
+#pragma unroll
+  for (int c = 0; c < CPL; ++c) chain_absorb(acc[c], hi[c]);
   uint32_t bfw = 0;
   for (int64_t p = p0 + (int64_t)nchunk * CH; p < p1; ++p) {  // ragged tail of the last tile
     if ((p & 31) == 0 || p == p0 + (int64_t)nchunk * CH) bfw = ld_stream4(P.bf + (p >> 5));
@@ -863,7 +659,6 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
 #pragma unroll
     for (int c = 0; c < CPL; ++c) {
       A::template add<NP>(acc[c], v, r1[c]);
-      A::settle(acc[c]);
     }
   }
   const bool right_open = (t + 1 < P.ntiles) && !((P.sf[(t + 1) >> 5] >> ((t + 1) & 31)) & 1u);
@@ -871,40 +666,23 @@ __global__ void __launch_bounds__(256) k_segreduce_staged(const EngineParams P) 
   if (mcp) __threadfence_system();  // multicast writes visible system-wide before the kernel ends
 }
 
-// Engine variant (FCOO_ENGINE env var, read once): 0 = plain, 1 = factored outer mode,
-// 2 = shared-memory-staged stream (default; used when a lane-group has >= 4 lanes).
-inline int engine_variant() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("FCOO_ENGINE");
-    v = e ? atoi(e) : 2;
-  }
-  return v;
-}
-
 // CTAs per SM the staged kernel's shared-memory carveout is sized for: the register-limited count
 // (64K registers / (regs x 256 threads), at most 4), so shared memory never lowers occupancy and
 // the rest of the unified 228 KB stays L1 for the factor rows.  Measured: SpTTM (NP=1, 70 regs)
-// 2 -> 3 CTAs is 10-15% faster on brainq; MTTKRP (>= 94 regs) stays at 2.  Env FCOO_STAGED_CTAS
-// overrides (A/B).
+// 2 -> 3 CTAs is 10-15% faster on brainq; MTTKRP (>= 94 regs) stays at 2.
 inline int staged_ctas_per_sm(const void* kern) {
-  const char* e = getenv("FCOO_STAGED_CTAS");
-  int v = e ? atoi(e) : 0;
-  if (v <= 0) {
-    cudaFuncAttributes fa;
-    v = 2;
-    if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && fa.numRegs > 0) v = 65536 / (fa.numRegs * 256);
-    if (v > 4) v = 4;
-  }
-  return v < 1 ? 1 : v > 8 ? 8 : v;
+  cudaFuncAttributes fa;
+  int v = 2;
+  if (cudaFuncGetAttributes(&fa, kern) == cudaSuccess && fa.numRegs > 0) v = 65536 / (fa.numRegs * 256);
+  return v < 1 ? 1 : v > 4 ? 4 : v;
 }
 
+// The staged kernel (stream through shared memory) when a lane-group has >= 4 lanes, else the
+// plain one (tiny ranks: per-lane staging would not pay).
 template <int NP, int G, int VEC, int CPL, class ACC>
 cudaError_t launch_one(const EngineParams& P, cudaStream_t s) {
   const bool full = (P.R == G * VEC * CPL);
-  const int variant = engine_variant();
-  const bool fact = NP >= 2 && variant == 1 && !P.dpart;
-  const bool staged = variant == 2 && G >= 4;
+  const bool staged = G >= 4;
   const int TB = 256;
   void (*kern)(const EngineParams);
   size_t smem = 0;
@@ -914,16 +692,12 @@ cudaError_t launch_one(const EngineParams& P, cudaStream_t s) {
     else
       kern = full ? k_segreduce_staged<NP, G, VEC, CPL, ACC, true, false> : k_segreduce_staged<NP, G, VEC, CPL, ACC, false, false>;
     smem = sizeof(uint32_t) * (size_t)(TB / G) * Stage<NP>::STRIDE;
-  } else if constexpr (NP >= 2) {
-    if (fact) kern = full ? k_segreduce_fact<NP, G, VEC, CPL, ACC, true> : k_segreduce_fact<NP, G, VEC, CPL, ACC, false>;
-    else kern = full ? k_segreduce<NP, G, VEC, CPL, ACC, true> : k_segreduce<NP, G, VEC, CPL, ACC, false>;
   } else {
     kern = full ? k_segreduce<NP, G, VEC, CPL, ACC, true> : k_segreduce<NP, G, VEC, CPL, ACC, false>;
   }
-  static bool configured[2][3][2] = {};  // [full][variant][deterministic]: one entry per kernel
-  const int ci = staged ? 2 : fact ? 1 : 0;
+  static bool configured[2][2][2] = {};  // [full][staged][deterministic]: one entry per kernel
   const int di = (staged && P.dpart) ? 1 : 0;
-  if (!configured[full][ci][di]) {
+  if (!configured[full][staged][di]) {
     if (staged) {  // small staging buffers: ask for just enough carveout, keep the rest as L1
       cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       const int ctas = staged_ctas_per_sm(reinterpret_cast<const void*>(kern));
@@ -932,7 +706,7 @@ cudaError_t launch_one(const EngineParams& P, cudaStream_t s) {
     } else {  // no shared memory: give the whole unified carveout to L1 (factor rows)
       cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 0);
     }
-    configured[full][ci][di] = true;
+    configured[full][staged][di] = true;
   }
   int64_t groups = P.tile_end - P.tile_begin;
   int64_t threads = groups * G;

@@ -80,6 +80,7 @@ struct fcoo_s {
   // graph capture (cp_als reserves the largest size it needs before capturing)
   void* dpart = nullptr;
   size_t bytes_dpart = 0;
+  std::vector<int64_t> debug_cleared;  // bf heads cleared by fcoo_debug_flip_bit (restorable)
   // shard
   int shard = 0, nshards = 1;
   int64_t tile_begin = 0, tile_end = 0;

@@ -127,6 +127,7 @@ __global__ void __launch_bounds__(256) k_ttm_lean(const TtmParams P) {
     uint32_t s = live ? P.seg_base[t] - (left_open ? 1u : 0u) : 0u;
     bool lo = left_open;  // the running segment is the one shared with the previous tile
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 hi = acc;  // the chain-capped part of the running segment (chain_fold, every 256 nnz)
     // warp-cooperative copy of chunk ci of every group of the warp: each 8-lane quarter writes one
     // contiguous 128-B segment (one array of one group), so the shared-memory writes are
     // conflict-free (a 4-lane group writing 64 B per instruction collided 4-way)
@@ -175,6 +176,7 @@ __global__ void __launch_bounds__(256) k_ttm_lean(const TtmParams P) {
 #pragma unroll
           for (int e = 0; e < B; ++e) fma4(acc, __uint_as_float(vb[e]), w[e]);
         } else if (!__any_sync(0xffffffffu, lo && heads != 0)) {  // every closed segment is owned
+          chain_absorb(acc, hi);
 #pragma unroll
           for (int e = 0; e < B; ++e) {
             const bool hd = (heads >> e) & 1u;
@@ -183,6 +185,7 @@ __global__ void __launch_bounds__(256) k_ttm_lean(const TtmParams P) {
             scale_fma(acc, hd ? 0.f : 1.f, __uint_as_float(vb[e]), w[e]);
           }
         } else {  // some group closes its left-open segment (once per tile): red.add for that one
+          chain_absorb(acc, hi);
 #pragma unroll
           for (int e = 0; e < B; ++e) {
             const bool hd = (heads >> e) & 1u;
@@ -193,9 +196,11 @@ __global__ void __launch_bounds__(256) k_ttm_lean(const TtmParams P) {
           }
         }
       }
+      if (ci % kChainChunks == kChainChunks - 1) chain_fold(hi, acc);
       __syncwarp();  // every lane is done with this stage before it is refilled
     }
     if (!live) continue;
+    chain_absorb(acc, hi);
     // ragged tail of the tensor's last tile
     for (int64_t p = p0 + (int64_t)nchunk * CH; p < p1; ++p) {
       const bool hd = p != p0 && ((P.bf[p >> 5] >> (p & 31)) & 1u);

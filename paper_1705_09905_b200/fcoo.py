@@ -79,7 +79,7 @@ SYMBOLS = ["fcoo_build", "fcoo_build_sharded", "fcoo_mttkrp", "fcoo_ttm", "fcoo_
            "fcoo_comm_unique_id", "fcoo_comm_init", "fcoo_comm_destroy", "fcoo_allreduce_sum", "fcoo_set_shard",
            "fcoo_mc_alloc", "fcoo_mc_ptr", "fcoo_mc_free", "fcoo_mttkrp_mc",
            "fcoo_shard_range", "cp_als", "fcoo_tns_read", "fcoo_tns_info", "fcoo_tns_copy", "fcoo_tns_destroy",
-           "fcoo_tns_write", "fcoo_status_str", "fcoo_last_error", "fcoo_launch_count"]
+           "fcoo_tns_write", "fcoo_debug_flip_bit", "fcoo_status_str", "fcoo_last_error", "fcoo_launch_count"]
 
 _lib = None
 
@@ -103,6 +103,7 @@ def load_library():
     L.fcoo_info.argtypes = [vp, ctypes.POINTER(_Info)]
     L.fcoo_export.argtypes = [vp, ctypes.POINTER(_HostView), vp]
     L.fcoo_destroy.argtypes = [vp]
+    L.fcoo_debug_flip_bit.argtypes = [vp, ci, i64]
     L.fcoo_comm_unique_id.argtypes = [vp]
     L.fcoo_comm_init.argtypes = [ci, ci, vp, ctypes.POINTER(vp)]
     L.fcoo_comm_destroy.argtypes = [vp]
@@ -404,6 +405,11 @@ def fcoo_ttmc(f: Fcoo, factors, out: torch.Tensor, stream=None) -> torch.Tensor:
     _check(L.fcoo_ttmc(f.h, arr, rk, ctypes.c_void_p(out.data_ptr()), ctypes.c_void_p(_stream_ptr(stream))),
            "fcoo_ttmc")
     return out
+
+
+def fcoo_debug_flip_bit(f: Fcoo, which: str, bit: int):
+    """TEST SUPPORT: flip one bit of the handle's device bf ("bf") or sf ("sf") array."""
+    _check(load_library().fcoo_debug_flip_bit(f.h, {"bf": 0, "sf": 1}[which], int(bit)), "fcoo_debug_flip_bit")
 
 
 def fcoo_export(f: Fcoo, perm: bool = False, stream=None) -> dict:

@@ -1,6 +1,6 @@
 """Quick per-(R, mode) timing sweep of fcoo_mttkrp on a workload (engine A/B experiments).
 
-FCOO_ENGINE=0|1 python tools/sweep.py [--workload nell2] [--R 16,32,64] [--tile 256]
+python tools/sweep.py [--workload nell2] [--R 16,32,64] [--tile 256] [--layout blocked|fcoo]
 Prints one JSON line per (R, mode): ms (CUDA events, 10 reps after 2 warm-up), G nnz/s, %HBM.
 """
 import argparse
@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--reps", type=int, default=10)
     ap.add_argument("--op", default="mttkrp")
     ap.add_argument("--desc", action="store_true", help="FCOO_BUILD_PRODUCT_DESC")
+    ap.add_argument("--layout", default="fcoo", choices=["fcoo", "blocked"], help="MTTKRP handle layout")
     ap.add_argument("--flush", action="store_true",
                     help="SURVEY 8(d) protocol: write a 2 x L2 scratch buffer before every rep (cold factors and "
                          "stream), time each rep alone, report median and min")
@@ -37,10 +38,11 @@ def main():
     import time
     for n in range(N):
         bop = P.OP_TTM if a.op == "ttm" else P.OP_MTTKRP
-        P.fcoo_build(coo, n, op=bop, tile_nnz=a.tile, product_desc=a.desc).destroy()  # warm allocator / CUB
+        blk = a.layout == "blocked" and bop == P.OP_MTTKRP
+        P.fcoo_build(coo, n, op=bop, tile_nnz=a.tile, product_desc=a.desc, blocked=blk).destroy()  # warm allocator / CUB
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        h = P.fcoo_build(coo, n, op=bop, tile_nnz=a.tile, product_desc=a.desc)
+        h = P.fcoo_build(coo, n, op=bop, tile_nnz=a.tile, product_desc=a.desc, blocked=blk)
         torch.cuda.synchronize()
         build_ms = (time.perf_counter() - t0) * 1e3
         for R in [int(x) for x in a.R.split(",")]:
@@ -93,7 +95,7 @@ def main():
             else:
                 b = compulsory_bytes(w.dims, nnz, n, R, h.info.tile_nnz)
             flops = {"ttm": 2 * R, "ttmc": 2 * width + 1}.get(a.op, N * R) * nnz
-            print(json.dumps({"engine": os.environ.get("FCOO_ENGINE", "default"), "workload": a.workload,
+            print(json.dumps({"layout": a.layout, "workload": a.workload,
                               "op": a.op, "desc": a.desc, "mode": n, "R": R, "tile": h.info.tile_nnz, "build_ms": round(build_ms, 2), "ms": round(ms, 4),
                               "gnnz_s": round(nnz / ms / 1e6, 2), "gflops": round(flops / ms / 1e6, 1),
                               "hbm_frac": round(b / (ms / 1e3) / 1e9 / peak, 4), **extra}),
