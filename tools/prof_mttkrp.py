@@ -1,7 +1,7 @@
 """Short, profiler-friendly run of the bench workload: build once, then `reps` fcoo_mttkrp calls per
 mode.  Used under ncu (launch lists / --set full).  Not a bench number.
 
-python tools/prof_mttkrp.py [--workload nell2] [--R 32] [--reps 3] [--modes 0,1,2] [--tile 256]
+python tools/prof_mttkrp.py [--workload nell2] [--R 32] [--reps 3] [--modes 0,1,2] [--tile 256] [--layout blocked|fcoo]
 """
 import argparse
 import os
@@ -19,6 +19,7 @@ def main():
     ap.add_argument("--modes", default=None)
     ap.add_argument("--tile", type=int, default=0)
     ap.add_argument("--op", default="mttkrp")
+    ap.add_argument("--layout", default="blocked", choices=["blocked", "fcoo"])
     a = ap.parse_args()
     import torch
 
@@ -40,7 +41,7 @@ def main():
             for _ in range(a.reps):
                 P.fcoo_ttmc(h, fs, out)
         else:
-            h = P.fcoo_build(coo, n, tile_nnz=a.tile)
+            h = P.fcoo_build(coo, n, tile_nnz=a.tile, blocked=(a.layout == "blocked"))
             out = torch.empty((w.dims[n], a.R), device="cuda")
             for _ in range(a.reps):
                 P.fcoo_mttkrp(h, fs, a.R, out)
