@@ -29,30 +29,33 @@ struct fcoo_mc_s {
 
 namespace fcoo {
 
-fcoo_status comm_allreduce(fcoo_comm_t c, float* buf, size_t count, cudaStream_t s) {
-  if (!c || !c->comm) return FCOO_OK;
-  ncclResult_t r = ncclAllReduce(buf, buf, count, ncclFloat, ncclSum, c->comm, s);
-  if (r != ncclSuccess) return fail(FCOO_ERR_NCCL, "ncclAllReduce: %s", ncclGetErrorString(r));
+// Status of an enqueued NCCL call: the immediate result, then the communicator's asynchronous
+// error state (ncclCommGetAsyncError, non-blocking: a peer failure or a network error surfaces
+// here on the next collective instead of as a hang) -> FCOO_ERR_NCCL.
+static fcoo_status nccl_status(fcoo_comm_t c, ncclResult_t r, const char* what) {
+  if (r != ncclSuccess && r != ncclInProgress) return fail(FCOO_ERR_NCCL, "%s: %s", what, ncclGetErrorString(r));
+  ncclResult_t ae = ncclSuccess;
+  if (ncclCommGetAsyncError(c->comm, &ae) != ncclSuccess || (ae != ncclSuccess && ae != ncclInProgress))
+    return fail(FCOO_ERR_NCCL, "%s: communicator error: %s", what, ncclGetErrorString(ae));
   count_launch();
   return FCOO_OK;
 }
 
+fcoo_status comm_allreduce(fcoo_comm_t c, float* buf, size_t count, cudaStream_t s) {
+  if (!c || !c->comm) return FCOO_OK;
+  return nccl_status(c, ncclAllReduce(buf, buf, count, ncclFloat, ncclSum, c->comm, s), "ncclAllReduce");
+}
+
 fcoo_status comm_allreduce_f64(fcoo_comm_t c, double* buf, size_t count, cudaStream_t s) {
   if (!c || !c->comm) return FCOO_OK;
-  ncclResult_t r = ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, s);
-  if (r != ncclSuccess) return fail(FCOO_ERR_NCCL, "ncclAllReduce(f64): %s", ncclGetErrorString(r));
-  count_launch();
-  return FCOO_OK;
+  return nccl_status(c, ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, s), "ncclAllReduce(f64)");
 }
 
 // Stream-ordered barrier over the comm: a one-element all-reduce completes on a rank only after
 // every rank has reached it (and, by stream order, finished the work enqueued before it).
 fcoo_status comm_barrier(fcoo_comm_t c, cudaStream_t s) {
   if (!c || !c->comm) return FCOO_OK;
-  ncclResult_t r = ncclAllReduce(c->scratch, c->scratch, 1, ncclInt, ncclSum, c->comm, s);
-  if (r != ncclSuccess) return fail(FCOO_ERR_NCCL, "barrier: %s", ncclGetErrorString(r));
-  count_launch();
-  return FCOO_OK;
+  return nccl_status(c, ncclAllReduce(c->scratch, c->scratch, 1, ncclInt, ncclSum, c->comm, s), "barrier");
 }
 
 void comm_rank_size(fcoo_comm_t c, int* rank, int* nranks) {
@@ -201,6 +204,26 @@ fcoo_status host_barrier(fcoo_comm_t c) {
   return FCOO_OK;
 }
 
+// Collective agreement: 1 on every rank iff `ok` is nonzero on every rank (min all-reduce on a
+// private stream, host-synchronous).  fcoo_mc_alloc calls it after every step that can fail on one
+// rank only, so all ranks bail out together instead of leaving the others blocked in a collective.
+bool agree_ok(fcoo_comm_t c, int ok) {
+  if (c->nranks == 1) return ok != 0;
+  int* d = nullptr;
+  cudaStream_t s = nullptr;
+  int res = 0;
+  if (cudaMalloc(&d, sizeof(int)) == cudaSuccess && cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) == cudaSuccess &&
+      cudaMemcpyAsync(d, &ok, sizeof(int), cudaMemcpyHostToDevice, s) == cudaSuccess &&
+      ncclAllReduce(d, d, 1, ncclInt, ncclMin, c->comm, s) == ncclSuccess &&
+      cudaMemcpyAsync(&res, d, sizeof(int), cudaMemcpyDeviceToHost, s) == cudaSuccess && cudaStreamSynchronize(s) == cudaSuccess) {
+  } else {
+    res = 0;
+  }
+  if (s) cudaStreamDestroy(s);
+  if (d) cudaFree(d);
+  return res != 0;
+}
+
 // rank `root`'s n bytes to every rank (ncclBroadcast through a device staging buffer)
 fcoo_status bcast_bytes(fcoo_comm_t c, void* host, size_t n, int root) {
   if (c->nranks == 1) return FCOO_OK;
@@ -236,7 +259,7 @@ fcoo_status fcoo_mc_alloc(fcoo_comm_t c, size_t bytes, fcoo_mc_t* out) {
   if (d.deviceGet(&dev, c->device) != CUDA_SUCCESS) return fail(FCOO_ERR_CUDA, "cuDeviceGet");
   int mcs = 0;
   d.deviceAttr(&mcs, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, dev);
-  if (!mcs) return fail(FCOO_ERR_ARG, "fcoo_mc_alloc: device does not support NVLS multicast");
+  if (!agree_ok(c, mcs)) return fail(FCOO_ERR_ARG, "fcoo_mc_alloc: a device of the comm does not support NVLS multicast");
   const bool shared = c->nranks > 1;
   CUmulticastObjectProp mp;
   memset(&mp, 0, sizeof(mp));
@@ -281,6 +304,15 @@ fcoo_status fcoo_mc_alloc(fcoo_comm_t c, size_t bytes, fcoo_mc_t* out) {
       ok0 = cr == CUDA_SUCCESS;
     }
   }
+  // from here on every failure point is agreed on by all ranks (agree_ok) before anyone bails,
+  // so a failure on one rank never leaves the others blocked in a later collective
+  fcoo_status err = FCOO_OK;
+  auto failed_somewhere = [&](fcoo_status local) {
+    if (local && !err) err = local;
+    if (agree_ok(c, local == FCOO_OK)) return false;
+    if (!err) err = fail(FCOO_ERR_CUDA, "fcoo_mc_alloc: a step failed on another rank");
+    return true;
+  };
   if (shared) {
     struct { CUmemFabricHandle h; int ok; } msg;
     msg.h = fh;
@@ -288,34 +320,41 @@ fcoo_status fcoo_mc_alloc(fcoo_comm_t c, size_t bytes, fcoo_mc_t* out) {
     fcoo_status st = bcast_bytes(c, &msg, sizeof(msg), 0);
     if (st) return bail(st);
     if (!msg.ok) return bail(fail(FCOO_ERR_CUDA, "cuMulticastCreate/export failed on rank 0 (CUresult %d)", (int)cr));
+    fcoo_status imp = FCOO_OK;
     if (c->rank != 0 && d.importHandle(&m->mcobj, &msg.h, CU_MEM_HANDLE_TYPE_FABRIC) != CUDA_SUCCESS)
-      return bail(fail(FCOO_ERR_CUDA, "cuMemImportFromShareableHandle (multicast)"));
+      imp = fail(FCOO_ERR_CUDA, "cuMemImportFromShareableHandle (multicast)");
+    if (failed_somewhere(imp)) return bail(err);
   } else if (!ok0) {
     return bail(fail(FCOO_ERR_CUDA, "cuMulticastCreate: CUresult %d", (int)cr));
   }
-  if ((cr = d.mcAddDevice(m->mcobj, dev)) != CUDA_SUCCESS)
-    return bail(fail(FCOO_ERR_CUDA, "cuMulticastAddDevice: CUresult %d", (int)cr));
+  fcoo_status add = FCOO_OK;
+  if ((cr = d.mcAddDevice(m->mcobj, dev)) != CUDA_SUCCESS) add = fail(FCOO_ERR_CUDA, "cuMulticastAddDevice: CUresult %d", (int)cr);
+  if (failed_somewhere(add)) return bail(err);
   // every device must be added before any rank binds memory
   fcoo_status st = host_barrier(c);
   if (st) return bail(st);
-  if (d.memCreate(&m->mem, m->size, &ap, 0) != CUDA_SUCCESS) return bail(fail(FCOO_ERR_OOM, "cuMemCreate"));
-  if ((cr = d.mcBindMem(m->mcobj, 0, m->mem, 0, m->size, 0)) != CUDA_SUCCESS)
-    return bail(fail(FCOO_ERR_CUDA, "cuMulticastBindMem: CUresult %d", (int)cr));
-  m->bound = true;
   CUmemAccessDesc acc;
   memset(&acc, 0, sizeof(acc));
   acc.location.type = CU_MEM_LOCATION_TYPE_DEVICE;
   acc.location.id = c->device;
   acc.flags = CU_MEM_ACCESS_FLAGS_PROT_READWRITE;
-  if (d.addrReserve(&m->uc, m->size, g, 0, 0) != CUDA_SUCCESS) return bail(fail(FCOO_ERR_OOM, "VA reserve (unicast)"));
-  if (d.memMap(m->uc, m->size, 0, m->mem, 0) != CUDA_SUCCESS) return bail(fail(FCOO_ERR_CUDA, "cuMemMap (unicast)"));
-  m->uc_mapped = true;
-  if (d.setAccess(m->uc, m->size, &acc, 1) != CUDA_SUCCESS) return bail(fail(FCOO_ERR_CUDA, "cuMemSetAccess (unicast)"));
-  if (d.addrReserve(&m->mc, m->size, g, 0, 0) != CUDA_SUCCESS) return bail(fail(FCOO_ERR_OOM, "VA reserve (multicast)"));
-  if (d.memMap(m->mc, m->size, 0, m->mcobj, 0) != CUDA_SUCCESS) return bail(fail(FCOO_ERR_CUDA, "cuMemMap (multicast)"));
-  m->mc_mapped = true;
-  if (d.setAccess(m->mc, m->size, &acc, 1) != CUDA_SUCCESS) return bail(fail(FCOO_ERR_CUDA, "cuMemSetAccess (multicast)"));
-  if (cudaMemset((void*)m->uc, 0, m->size) != cudaSuccess) return bail(fail(FCOO_ERR_CUDA, "zero multicast buffer"));
+  auto setup = [&]() -> fcoo_status {  // local steps; the first failure is reported
+    if (d.memCreate(&m->mem, m->size, &ap, 0) != CUDA_SUCCESS) return fail(FCOO_ERR_OOM, "cuMemCreate");
+    if ((cr = d.mcBindMem(m->mcobj, 0, m->mem, 0, m->size, 0)) != CUDA_SUCCESS)
+      return fail(FCOO_ERR_CUDA, "cuMulticastBindMem: CUresult %d", (int)cr);
+    m->bound = true;
+    if (d.addrReserve(&m->uc, m->size, g, 0, 0) != CUDA_SUCCESS) return fail(FCOO_ERR_OOM, "VA reserve (unicast)");
+    if (d.memMap(m->uc, m->size, 0, m->mem, 0) != CUDA_SUCCESS) return fail(FCOO_ERR_CUDA, "cuMemMap (unicast)");
+    m->uc_mapped = true;
+    if (d.setAccess(m->uc, m->size, &acc, 1) != CUDA_SUCCESS) return fail(FCOO_ERR_CUDA, "cuMemSetAccess (unicast)");
+    if (d.addrReserve(&m->mc, m->size, g, 0, 0) != CUDA_SUCCESS) return fail(FCOO_ERR_OOM, "VA reserve (multicast)");
+    if (d.memMap(m->mc, m->size, 0, m->mcobj, 0) != CUDA_SUCCESS) return fail(FCOO_ERR_CUDA, "cuMemMap (multicast)");
+    m->mc_mapped = true;
+    if (d.setAccess(m->mc, m->size, &acc, 1) != CUDA_SUCCESS) return fail(FCOO_ERR_CUDA, "cuMemSetAccess (multicast)");
+    if (cudaMemset((void*)m->uc, 0, m->size) != cudaSuccess) return fail(FCOO_ERR_CUDA, "zero multicast buffer");
+    return FCOO_OK;
+  };
+  if (failed_somewhere(setup())) return bail(err);
   st = host_barrier(c);  // every rank bound and mapped before anyone writes through mc
   if (st) return bail(st);
   *out = m;
