@@ -48,6 +48,8 @@ def _load():
         L.orc_build_ex.argtypes = [ci, vp, i64, vp, vp, ci, ci, i64, ci, vp, vp, vp, vp, vp, vp, vp, vp]
         L.orc_build_blocked.argtypes = [ci, vp, i64, vp, vp, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                         i64, vp, vp, vp]
+        L.orc_build_blocked_ex.argtypes = [ci, vp, i64, vp, vp, ci, ci, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                                           vp, i64, vp, vp, vp, vp, vp]
         L.orc_mode_spec_ex.argtypes = [ci, vp, ci, ci, ci, vp, vp, vp, vp]
         L.orc_mttkrp.argtypes = [ci, vp, i64, vp, vp, ci, vp, ci, vp, vp, ci]
         L.orc_ttm.argtypes = [ci, vp, i64, vp, vp, ci, vp, ci, vp, vp, vp, vp]
@@ -155,19 +157,21 @@ class FcooBlocked:
     T: int
     BR: int
     IB: int
+    seg_row: np.ndarray = None   # SpTTM: fibre (output row) of each blocked segment
+    nfib: int = 0
 
     def bf_bits(self) -> np.ndarray:
         return np.unpackbits(self.bf, bitorder="little")[: self.nstream]
 
 
-def build_fcoo_blocked(dims, idx, val, mode: int, T: int, BR: int) -> FcooBlocked:
+def build_fcoo_blocked(dims, idx, val, mode: int, T: int, BR: int, op: int = OP_MTTKRP) -> FcooBlocked:
     L = _load()
     d, idx, val = _coo(dims, idx, val)
     nnz = val.shape[0]
     order = len(d)
     if order < 2 or order > 8:
         raise OracleError(ERR_ORDER, "build_blocked")
-    im, pm = mode_spec(d, OP_MTTKRP, mode)
+    im, pm = mode_spec(d, op, mode)
     nblocks = max(1, (int(d[pm[0]]) + BR - 1) // BR)
     cap = nnz + nblocks * (T - 1)
     ntiles_cap = max(1, cap // T + 1)
@@ -181,10 +185,12 @@ def build_fcoo_blocked(dims, idx, val, mode: int, T: int, BR: int) -> FcooBlocke
     pk = np.zeros(cap, np.uint32)
     bs = np.zeros(nblocks + 1, np.int64)
     be = np.zeros(nblocks, np.int64)
-    nsg, nst, nbl = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
-    rc = L.orc_build_blocked(order, _ptr(d), nnz, _ptr(idx), _ptr(val), mode, T, BR, _ptr(perm), _ptr(bf), _ptr(sf),
-                             _ptr(seg_base), _ptr(seg_coord), _ptr(pidx), _ptr(pval), _ptr(pk), _ptr(bs), _ptr(be),
-                             cap, ctypes.byref(nsg), ctypes.byref(nst), ctypes.byref(nbl))
+    nsg, nst, nbl, nfb = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_int64(0)
+    seg_row = np.zeros(max(1, nnz), np.uint32)
+    rc = L.orc_build_blocked_ex(order, _ptr(d), nnz, _ptr(idx), _ptr(val), op, mode, T, BR, _ptr(perm), _ptr(bf),
+                                _ptr(sf), _ptr(seg_base), _ptr(seg_coord), _ptr(pidx), _ptr(pval), _ptr(pk), _ptr(bs),
+                                _ptr(be), cap, ctypes.byref(nsg), ctypes.byref(nst), ctypes.byref(nbl),
+                                _ptr(seg_row), ctypes.byref(nfb))
     if rc:
         raise OracleError(rc, "build_blocked")
     ns, ntiles = nst.value, nst.value // T
@@ -194,7 +200,8 @@ def build_fcoo_blocked(dims, idx, val, mode: int, T: int, BR: int) -> FcooBlocke
     return FcooBlocked(im, pm, perm[:ns].copy(), bf[: (ns + 7) // 8].copy(), sf[: (ntiles + 31) // 32].copy(),
                        seg_base[:ntiles].copy(), seg_coord[: nsg.value].copy(),
                        pidx[: len(pm) * ns].reshape(len(pm), ns).copy(), pval[:ns].copy(), pk[:ns].copy(), bs, be,
-                       nsg.value, ns, nbl.value, T, BR, IB if len(pm) >= 2 else 0)
+                       nsg.value, ns, nbl.value, T, BR, IB if len(pm) >= 2 else 0,
+                       seg_row[: nsg.value].copy() if op == OP_TTM else None, nfb.value)
 
 
 def mttkrp(dims, idx, val, mode: int, factors, R: int | None = None, with_D: bool = True, nthreads: int = 1):

@@ -172,7 +172,7 @@ int orc_build(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, 
 }
 
 /* ------------------------------------------------------------------------- */
-/* c1b. Blocked F-COO for SpMTTKRP (DESIGN.md §5 "blocked layout", reading Q22).
+/* c1b. Blocked F-COO for SpMTTKRP and SpTTM (DESIGN.md §5 "blocked layout", reading Q22).
  * The F-COO of Fig. 2 / P:L246-282 applied to the sub-tensors X_b = { nonzeros q :
  * floor(i_outer(q) / BR) == b }, b = 0, 1, ..., where "outer" is the FIRST product mode of Q5
  * (smallest extent), concatenated in b order, each padded with empty positions to a multiple of
@@ -187,16 +187,20 @@ int orc_build(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, 
  *   pidx[a][p] = product coord a (global index, Q5 order) of the nonzero at p;
  *   pk[p] = ((i_outer - b*BR) << IB) | i_last  with IB = ceil(log2(I_last)) (n_prod >= 2), where
  *     "last" is the last product mode of Q5; pk[p] = i_outer - b*BR when n_prod == 1.
- * Inputs as orc_build_ex (op = MTTKRP), plus BR >= 1.  Capacities: stream arrays hold
+ * SpTTM (op = TTM): the product mode is mode n, which is then also "outer" and "last" (one
+ * product mode: the packed word is the local index); seg_row[s] (capacity nnz) = the ordinal of
+ * blocked segment s's index tuple among all distinct tuples in lexicographic order (the fibre =
+ * output row of Eq.(3)), nfib_out = the number of fibres.
+ * Inputs as orc_build_ex, plus BR >= 1.  Capacities: stream arrays hold
  * nnz + nblocks*(T-1) positions (nblocks = ceil(I_outer / BR)), seg_coord nnz*n_idx.
  * Errors as orc_build_ex; ORC_ERR_ARG if the packed word does not fit in 32 bits. */
-int orc_build_blocked(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, const float* val, int mode,
-                      int64_t T, int64_t BR, uint32_t* perm, uint8_t* bf, uint32_t* sf, uint32_t* seg_base,
-                      uint32_t* seg_coord, uint32_t* pidx, float* pval, uint32_t* pk, int64_t* blk_start,
-                      int64_t* blk_end, int64_t cap, int64_t* nsegs_out, int64_t* nstream_out,
-                      int64_t* nblocks_out) {
+int orc_build_blocked_ex(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, const float* val, int op,
+                         int mode, int64_t T, int64_t BR, uint32_t* perm, uint8_t* bf, uint32_t* sf,
+                         uint32_t* seg_base, uint32_t* seg_coord, uint32_t* pidx, float* pval, uint32_t* pk,
+                         int64_t* blk_start, int64_t* blk_end, int64_t cap, int64_t* nsegs_out,
+                         int64_t* nstream_out, int64_t* nblocks_out, uint32_t* seg_row, int64_t* nfib_out) {
   int idx_modes[8], prod_modes[8], n_idx = 0, n_prod = 0;
-  int rc = orc_mode_spec_ex(order, dims, ORC_OP_MTTKRP, mode, 0, idx_modes, &n_idx, prod_modes, &n_prod);
+  int rc = orc_mode_spec_ex(order, dims, op, mode, 0, idx_modes, &n_idx, prod_modes, &n_prod);
   if (rc) return rc;
   if (T < 1 || BR < 1) return ORC_ERR_ARG;
   if (nnz <= 0) return ORC_ERR_EMPTY;
@@ -282,7 +286,32 @@ int orc_build_blocked(int order, const int64_t* dims, int64_t nnz, const uint32_
   *nsegs_out = nsegs;
   *nstream_out = ns;
   *nblocks_out = nblocks;
+  /* SpTTM on a blocked stream: the output rows are the fibres of the F-COO (distinct index tuples
+   * in lexicographic order); seg_row[s] = the fibre of blocked segment s */
+  if (op == ORC_OP_TTM && seg_row) {
+    std::map<std::vector<uint32_t>, int64_t> fib;
+    for (int64_t k = 0; k < nnz; ++k) {
+      std::vector<uint32_t> t(n_idx);
+      for (int a = 0; a < n_idx; ++a) t[a] = coord(ord[k], a);
+      fib.emplace(t, 0);
+    }
+    int64_t r = 0;
+    for (auto& kv : fib) kv.second = r++;
+    for (int64_t s2 = 0; s2 < nsegs; ++s2)
+      seg_row[s2] = (uint32_t)fib.at(std::vector<uint32_t>(seg_coord + s2 * n_idx, seg_coord + (s2 + 1) * n_idx));
+    *nfib_out = r;
+  }
   return ORC_OK;
+}
+
+int orc_build_blocked(int order, const int64_t* dims, int64_t nnz, const uint32_t* idx, const float* val, int mode,
+                      int64_t T, int64_t BR, uint32_t* perm, uint8_t* bf, uint32_t* sf, uint32_t* seg_base,
+                      uint32_t* seg_coord, uint32_t* pidx, float* pval, uint32_t* pk, int64_t* blk_start,
+                      int64_t* blk_end, int64_t cap, int64_t* nsegs_out, int64_t* nstream_out,
+                      int64_t* nblocks_out) {
+  return orc_build_blocked_ex(order, dims, nnz, idx, val, ORC_OP_MTTKRP, mode, T, BR, perm, bf, sf, seg_base,
+                              seg_coord, pidx, pval, pk, blk_start, blk_end, cap, nsegs_out, nstream_out, nblocks_out,
+                              nullptr, nullptr);
 }
 
 /* ------------------------------------------------------------------------- */

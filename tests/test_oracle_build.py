@@ -295,3 +295,36 @@ def test_blocked_errors():
     with pytest.raises(oracle.OracleError) as e:
         oracle.build_fcoo_blocked(big, idx, np.ones(2, np.float32), 0, 4, 8)
     assert e.value.code == oracle.ERR_ARG
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+def test_blocked_ttm_stream(mode):
+    """Blocked F-COO for SpTTM (op = TTM): the product mode n is blocked; each blocked segment maps
+    (seg_row) to the fibre with its index tuple in the plain F-COO's fibre table, and Eq.(3)
+    evaluated from the blocked stream (each segment added into its fibre's row) equals the dense
+    X x_n U definition (tests/dense_defs.py)."""
+    import dense_defs
+    dims = (7, 9, 5)
+    R = 3
+    idx, val = gen.coo(dims, 150, None, 37)
+    U = gen.uniform((dims[mode], R), 38, mode, signed=True).astype(np.float64)
+    f = oracle.build_fcoo_blocked(dims, idx, val, mode, 8, 2, op=oracle.OP_TTM)
+    g = oracle.build_fcoo(dims, idx, val, oracle.OP_TTM, mode, 8)
+    assert f.product_modes == [mode] and f.nfib == g.nsegs
+    assert np.array_equal(g.seg_coord[f.seg_row], f.seg_coord)
+    assert np.all(f.pk[f.perm != 0xFFFFFFFF] == idx[mode][f.perm[f.perm != 0xFFFFFFFF]] % 2)
+    Y = np.zeros((f.nfib, R))
+    bits = f.bf_bits()
+    s = -1
+    for p in range(f.nstream):
+        if f.perm[p] == 0xFFFFFFFF:
+            continue
+        if bits[p]:
+            s += 1
+        Y[f.seg_row[s]] += float(f.val[p]) * U[int(f.pidx[0, p])]
+    X = dense_defs.dense_from_coo(dims, idx, val)
+    ref = dense_defs.ttm_dense(X, U, mode)
+    got = np.zeros_like(ref)
+    for r, c in enumerate(g.seg_coord):  # ttm_dense: the other modes in order, then the R axis
+        got[tuple(int(x) for x in c)] = Y[r]
+    assert np.allclose(got, ref, rtol=1e-12, atol=1e-12)
