@@ -81,7 +81,7 @@ typedef struct {
  * Same sum, a fixed association: repeated calls give identical bits.  SpTTMc and the CP-ALS
  * fit-mode fp64 pass keep red.add. */
 #define FCOO_BUILD_DETERMINISTIC 4u
-/* Blocked F-COO (FCOO_OP_MTTKRP only, reading Q22): the stream is the concatenation,
+/* Blocked F-COO (reading Q22): the stream is the concatenation,
  * over b = 0, 1, ..., of the F-COO of the sub-tensor X_b = {nonzeros with floor(i_outer / BR) == b},
  * "outer" = the first product mode of reading Q5 (smallest extent), BR = block_rows; each block is
  * padded with empty positions to a multiple of T, so every tile belongs to one block.  Eq.(6) is
@@ -91,7 +91,9 @@ typedef struct {
  * Per nonzero the stream holds ONE packed word (i_outer - b*BR) << IB | i_last (IB =
  * ceil(log2 I_last), "last" = last product mode of Q5; order 2: the local outer index alone),
  * plus, for order >= 4, the global index of each middle product mode: 8 B/nnz + flags for a
- * 3-order tensor instead of Table II's 12.  Requires 2 <= order <= 5 and ceil(log2 BR) + IB <= 32
+ * 3-order tensor instead of Table II's 12.  FCOO_OP_TTM: the one product mode n is blocked (the
+ * word is i_n - b*BR); segments are (block, fibre) pairs, mapped to the fibre table (output rows)
+ * by a sort of the segments' tuples: a third host synchronisation (fibre count).  Requires 2 <= order <= 5 and ceil(log2 BR) + IB <= 32
  * (else FCOO_ERR_ARG); incompatible with DETERMINISTIC and PRODUCT_DESC (ARG); fcoo_ttmc rejects
  * blocked handles (SHAPE).  The build synchronises the host twice (block sizes, then errors). */
 #define FCOO_BUILD_BLOCKED 8u
@@ -148,9 +150,11 @@ fcoo_status fcoo_mttkrp(fcoo_t f, const float* const* factors, int R, float* out
  * fcoo_ttm — SpTTM on the handle's mode n (Eq.(3); Table I row 1):
  *   out(s, :) = sum_{nonzeros q of fibre s} v_q * U(i_n(q), :)
  * on the same segmented-reduction engine.  Output is semi-sparse: one dense R-row
- * per non-empty fibre s (segment ordinal, in lexicographic order of the index tuple); the
- * fibre coordinates are the seg_coord table (fcoo_export).
- *   U: device, I_n x R fp32 row-major.  out: device, nsegs x R fp32, overwritten.
+ * per non-empty fibre s (in lexicographic order of the index tuple); the fibre coordinates are
+ * the fib_coord table (fcoo_export; = seg_coord on a plain handle).  On a blocked handle
+ * (FCOO_BUILD_BLOCKED) the kernel keeps block b of U (BR rows) in shared memory and every
+ * (block, fibre) segment is added into its fibre's row with red.global.add.
+ *   U: device, I_n x R fp32 row-major.  out: device, nfib x R fp32 (fcoo_info), overwritten.
  * Errors: SHAPE (handle built for MTTKRP), RANK, ARG, CUDA, NCCL.  Asynchronous.
  */
 fcoo_status fcoo_ttm(fcoo_t f, const float* U, int R, float* out, void* stream);
@@ -186,6 +190,8 @@ typedef struct {
   int64_t nstream;         /* stream positions (blocked: nnz + padding = ntiles * tile_nnz; else nnz) */
   int pk_shift;            /* IB of the packed word (blocked handles) */
   int n_words;             /* packed words per nonzero (blocked handles: 1 + max(0, n_prod - 2)) */
+  int64_t nfib;            /* SpTTM handles: output rows = fibres (non-empty index tuples); = nsegs for a
+                              plain handle, <= nsegs for a blocked one (a fibre recurs once per block); 0 for MTTKRP */
 } fcoo_info_t;
 
 /* fcoo_info — host-side metadata; no device work. */
@@ -210,6 +216,8 @@ typedef struct {
   uint32_t* pk;
   int64_t* blk_start;
   int64_t* blk_end;
+  uint32_t* seg_row;   /* blocked SpTTM handles: u32[nsegs], the fibre (output row) of each segment */
+  uint32_t* fib_coord; /* SpTTM handles: u32[nfib*n_idx], the index tuple of each output row (plain: = seg_coord) */
 } fcoo_host_view;
 
 /* fcoo_export — copy the handle's arrays to host buffers; synchronises `stream`. */

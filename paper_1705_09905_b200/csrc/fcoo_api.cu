@@ -176,7 +176,8 @@ fcoo_status fcoo_info(fcoo_t f, fcoo_info_t* info) {
   info->pk_shift = f->pk_shift;
   info->n_words = f->n_words;
   if (f->blocked)  // packed words + values + bf over the padded stream, block tables
-    info->device_bytes += (int64_t)f->bytes_blk;
+    info->device_bytes += (int64_t)(f->bytes_blk + f->bytes_seg_row + f->bytes_fib);
+  info->nfib = f->op != FCOO_OP_TTM ? 0 : f->blocked ? f->nfib : f->nsegs;
   return FCOO_OK;
 }
 
@@ -198,6 +199,12 @@ fcoo_status fcoo_export(fcoo_t f, fcoo_host_view* v, void* stream) {
     if (v->pk) FCOO_CUDA_TRY(cudaMemcpyAsync(v->pk, f->pidx, 4 * ns * f->n_words, cudaMemcpyDeviceToHost, s));
     if (v->blk_start) memcpy(v->blk_start, f->h_blk_start.data(), sizeof(int64_t) * (f->nblocks + 1));
     if (v->blk_end) memcpy(v->blk_end, f->h_blk_end.data(), sizeof(int64_t) * f->nblocks);
+    if (f->op == FCOO_OP_TTM) {
+      if (v->seg_row && f->nsegs > 0)
+        FCOO_CUDA_TRY(cudaMemcpyAsync(v->seg_row, f->seg_row, 4 * f->nsegs, cudaMemcpyDeviceToHost, s));
+      if (v->fib_coord && f->nfib > 0)
+        FCOO_CUDA_TRY(cudaMemcpyAsync(v->fib_coord, f->fib_coord, 4 * f->nfib * f->n_idx, cudaMemcpyDeviceToHost, s));
+    }
     if (v->pidx) {
       fcoo::Buf tmp(&f->alloc, sizeof(uint32_t) * (size_t)(ns * f->n_prod), s);
       if (!tmp.ok()) return fcoo::fail(FCOO_ERR_OOM, "export scratch");
@@ -224,6 +231,8 @@ fcoo_status fcoo_export(fcoo_t f, fcoo_host_view* v, void* stream) {
     for (int a = 0; a < f->n_prod; ++a)
       FCOO_CUDA_TRY(cudaMemcpyAsync(v->pidx + a * nnz, f->pidx + a * f->nnz_pad, 4 * nnz, cudaMemcpyDeviceToHost, s));
   if (v->val) FCOO_CUDA_TRY(cudaMemcpyAsync(v->val, f->val, 4 * nnz, cudaMemcpyDeviceToHost, s));
+  if (f->op == FCOO_OP_TTM && v->fib_coord && f->nsegs > 0)  // plain SpTTM: the fibres are the segments
+    FCOO_CUDA_TRY(cudaMemcpyAsync(v->fib_coord, f->seg_coord, 4 * f->nsegs * f->n_idx, cudaMemcpyDeviceToHost, s));
   FCOO_CUDA_TRY(cudaStreamSynchronize(s));
   return FCOO_OK;
 }

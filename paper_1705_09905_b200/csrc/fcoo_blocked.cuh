@@ -3,6 +3,7 @@
 // fcoo_blocked_np<NP>_<acc>.cu (kernels: fcoo_blocked_kernels.cuh).
 #pragma once
 #include <cuda_runtime.h>
+#include <algorithm>
 #include <stddef.h>
 
 #include "fcoo_engine.cuh"
@@ -28,14 +29,17 @@ struct BlockedParams {
   int gate_on;
 };
 
-// Shared-memory staging of the stream: per lane-group, 2 stages of one 32-nonzero chunk:
-// NW packed-word rows + the values + the bf word (+3 pad words, 16-B aligned).  The per-group
-// stride is padded to G (mod 32) words so the 32/G groups of a warp read distinct banks.
-template <int NW, int G>
+// Shared-memory staging of the stream: per lane-group, NST stages of one 32-nonzero chunk each
+// (NST - 1 chunks in flight): NW packed-word rows + the values + the bf word (+3 pad words, 16-B
+// aligned).  The per-group stride is padded to G (mod 32) words so the 32/G groups of a warp read
+// distinct banks.  NST = 2 (SpTTM with 4 stages measured the same: not stream-latency bound).
+template <int NP>
+constexpr int blocked_nst() { return 2; }
+template <int NW, int G, int NST = 2>
 struct BStage {
   static constexpr int CH = 32;
   static constexpr int WORDS = (NW + 1) * CH + 4;
-  static constexpr int RAW = 2 * WORDS;
+  static constexpr int RAW = NST * WORDS;
   static constexpr int WANT = (G >= 4 ? G : 4) % 32;
   static constexpr int STRIDE = RAW + (((WANT - RAW % 32) % 32) + 32) % 32;
 };
@@ -44,11 +48,21 @@ struct BStage {
 struct BlockedShape {
   int G, VEC, CPL, TB;
   bool smem;
+  int ncp;  // copies of the block in shared memory (0: outer rows from global memory)
   size_t block_bytes;
 };
-// Staging bytes of a CTA of TB threads (lane-groups of G lanes, NW packed-word rows).
-inline size_t blocked_stage_bytes(int NW, int G, int TB) {
-  const int words = (NW + 1) * 32 + 4, raw = 2 * words, want = (G >= 4 ? G : 4) % 32;
+// Copies of the block that make the float4 row reads of a warp bank-conflict-free: rows of 4R
+// bytes < 128 B share a bank line 128 / 4R at a time (R = 16: 2 copies, R = 8: 4).
+constexpr int blocked_copies(int R) { return 4 * R < 128 ? 128 / (4 * R) : 1; }
+// Shared-memory bytes of the block with ncp copies (copy k starts k rows past a 128-B boundary).
+inline size_t blocked_block_bytes(int BR, int R, int ncp) {
+  if (ncp <= 0) return 0;
+  if (ncp == 1) return (size_t)BR * R * 4;
+  return (size_t)ncp * (((size_t)BR * R + 31) / 32 * 32 + R) * 4;
+}
+// Staging bytes of a CTA of TB threads (lane-groups of G lanes, NW packed-word rows, NST stages).
+inline size_t blocked_stage_bytes(int NW, int G, int TB, int NST) {
+  const int words = (NW + 1) * 32 + 4, raw = NST * words, want = (G >= 4 ? G : 4) % 32;
   const int stride = raw + (((want - raw % 32) % 32) + 32) % 32;
   return sizeof(uint32_t) * (size_t)(TB / G) * stride;
 }
@@ -71,14 +85,26 @@ inline BlockedShape blocked_shape(int NP, int R, int BR, bool vec_ok) {
   // ~110 KB each, else one 512-thread CTA up to ~220 KB, else the outer rows are gathered from
   // global memory like the others (always for scalar lanes: the TMA bulk copy moves whole 16-B
   // units of 16-B aligned rows)
-  const int NW = NP >= 2 ? NP - 1 : 1;
+  const int NW = NP >= 2 ? NP - 1 : 1, NST = 2;
   sh.smem = false;
+  sh.ncp = 0;
   sh.TB = 256;
   if (vec_ok) {
-    if (sh.block_bytes + blocked_stage_bytes(NW, sh.G, 256) <= 110 * 1024) {
+    // copies of a narrow-row block only where they keep the CTAs per SM (3 for one product mode,
+    // else 2): measured on brainq SpTTM, occupancy outweighs the bank conflicts they remove
+    const int C = blocked_copies(R), want = NP == 1 ? 3 : 2;
+    const size_t st256 = blocked_stage_bytes(NW, sh.G, 256, NST);
+    auto ctas = [&](size_t bytes) { return std::min<int>(want, (int)((228 * 1024) / (bytes + st256 + 1024))); };
+    if (C > 1 && ctas(blocked_block_bytes(BR, R, C)) >= ctas(sh.block_bytes) &&
+        blocked_block_bytes(BR, R, C) + st256 <= 110 * 1024) {
       sh.smem = true;
-    } else if (sh.block_bytes + blocked_stage_bytes(NW, sh.G, 512) <= 220 * 1024) {
+      sh.ncp = C;
+    } else if (sh.block_bytes + st256 <= 110 * 1024) {
       sh.smem = true;
+      sh.ncp = 1;
+    } else if (sh.block_bytes + blocked_stage_bytes(NW, sh.G, 512, NST) <= 220 * 1024) {
+      sh.smem = true;
+      sh.ncp = 1;
       sh.TB = 512;
     }
   }

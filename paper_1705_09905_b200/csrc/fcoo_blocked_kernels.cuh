@@ -112,14 +112,19 @@ __device__ __forceinline__ void acc_add(typename Acc<VEC, ACC>::T& acc, float v,
 // NP product modes (outer + NP-1 gathered), G lanes per group, VEC floats per column slot, CPL
 // column slots per lane; SMEM: outer rows from the shared-memory block (else LDG, for a block
 // too large for shared memory); TB threads per CTA.
-template <int NP, int G, int VEC, int CPL, class ACC, bool FULL, bool SMEM, int TB, int MINB>
+// NCP copies of the block (NCP > 1 only for rows narrower than 128 B: copy k starts k row-widths
+// past a 128-B boundary, and group g reads row r from copy (g - r) mod NCP, so the NCP groups that
+// share a 128-B bank line in one LDS.128 always hit disjoint banks; measured).
+template <int NP, int G, int VEC, int CPL, class ACC, bool FULL, int NCP, int TB, int MINB>
 __global__ void __launch_bounds__(TB, MINB) k_mttkrp_blocked(const BlockedParams P) {
+  constexpr bool SMEM = NCP > 0;
   using V = Ld<VEC>;
   using VT = typename V::T;
   using A = Acc<VEC, ACC>;
   using AT = typename A::T;
   constexpr int NW = NP >= 2 ? NP - 1 : 1;
-  using S = BStage<NW, G>;
+  constexpr int NST = blocked_nst<NP>();
+  using S = BStage<NW, G, NST>;
   constexpr int B = batch_size<NP, VEC, CPL>();
   constexpr int CH = S::CH;
   extern __shared__ uint4 smem_raw[];
@@ -129,17 +134,22 @@ __global__ void __launch_bounds__(TB, MINB) k_mttkrp_blocked(const BlockedParams
   const int b = item.x;
   const int R = P.R;
   float* blk = reinterpret_cast<float*>(smem_raw);
-  uint32_t* stage_base = reinterpret_cast<uint32_t*>(smem_raw) + (SMEM ? (size_t)P.BR * R : 0);  // R % 4 == 0
+  // floats from one copy of the block to the next (a multiple of 128 B plus one row)
+  const uint32_t cstride = NCP > 1 ? ((uint32_t)P.BR * R + 31u) / 32u * 32u + (uint32_t)R : 0u;
+  uint32_t* stage_base =
+      reinterpret_cast<uint32_t*>(smem_raw) + (SMEM ? (NCP > 1 ? NCP * cstride : (size_t)P.BR * R) : 0);  // R % 4 == 0
   if constexpr (SMEM) {
     if (threadIdx.x == 0) {
-      mbar_init(&mbar, 1);
+      mbar_init(&mbar, NCP);
       asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
     if (threadIdx.x == 0) {
       const int r0 = b * P.BR;
       const int nr = min(P.BR, P.Io - r0);
-      bulk_g2s(blk, P.U[0] + (size_t)r0 * R, (uint32_t)nr * (uint32_t)R * 4u, &mbar);
+#pragma unroll
+      for (int k = 0; k < NCP; ++k)
+        bulk_g2s(blk + k * cstride, P.U[0] + (size_t)r0 * R, (uint32_t)nr * (uint32_t)R * 4u, &mbar);
     }
   }
   const int g = threadIdx.x / G;
@@ -207,7 +217,9 @@ __global__ void __launch_bounds__(TB, MINB) k_mttkrp_blocked(const BlockedParams
         for (int a = 0; a < NP; ++a) r[c][a] = V::zero();
         continue;
       }
-      if constexpr (SMEM) r[c][0] = lds_row<VEC>(sb[c] + local * rowb);
+      if constexpr (NCP > 1)
+        r[c][0] = lds_row<VEC>(sb[c] + (((uint32_t)g - local) & (NCP - 1)) * (cstride * 4u) + local * rowb);
+      else if constexpr (SMEM) r[c][0] = lds_row<VEC>(sb[c] + local * rowb);
       else r[c][0] = V::load(reinterpret_cast<const float*>(ub[0][c] + (size_t)local * rowb));
       if constexpr (NP >= 2) {
 #pragma unroll
@@ -231,16 +243,19 @@ __global__ void __launch_bounds__(TB, MINB) k_mttkrp_blocked(const BlockedParams
     }
     if (gl == 0) cp_async4(dst + (NW + 1) * CH, P.bf + (pc >> 5));
   };
-  if (nchunk > 0) issue(p0, 0);
-  cp_async_commit();
+#pragma unroll
+  for (int j = 0; j + 1 < NST; ++j) {  // NST - 1 chunks in flight
+    if (j < nchunk) issue(p0 + (int64_t)j * CH, j);
+    cp_async_commit();
+  }
   if constexpr (SMEM) mbar_wait(&mbar, 0);  // every thread: the block rows are resident
 
   for (int ci = 0; ci < nchunk; ++ci) {
-    if (ci + 1 < nchunk) issue(p0 + (int64_t)(ci + 1) * CH, (ci + 1) & 1);
+    if (ci + NST - 1 < nchunk) issue(p0 + (int64_t)(ci + NST - 1) * CH, (ci + NST - 1) % NST);
     cp_async_commit();
-    cp_async_wait<1>();
+    cp_async_wait<NST - 1>();
     __syncwarp(gmask);
-    const uint32_t* stg = my + (ci & 1) * S::WORDS;
+    const uint32_t* stg = my + (ci % NST) * S::WORDS;
     const uint32_t bfw = stg[(NW + 1) * CH];
 #pragma unroll
     for (int bi = 0; bi < CH / B; ++bi) {
@@ -316,13 +331,16 @@ __global__ void __launch_bounds__(TB, MINB) k_mttkrp_blocked(const BlockedParams
 
 namespace fcoo {
 
-template <int NP, int G, int VEC, int CPL, class ACC, bool SMEM, int TB>
+template <int NP, int G, int VEC, int CPL, class ACC, int NCP, int TB>
 cudaError_t launch_blocked_one(const BlockedParams& P, int nitems, cudaStream_t s) {
+  constexpr bool SMEM = NCP > 0;
   constexpr int NW = NP >= 2 ? NP - 1 : 1;
-  constexpr int MINB = TB == 256 ? 2 : 1;
+  // one product mode (SpTTM, order-2 MTTKRP): 77 registers, so 3 CTAs of 256 threads fit per SM
+  constexpr int MINB = TB == 256 ? (NP == 1 ? 3 : 2) : 1;
   constexpr bool FULL = VEC == 4;  // float4 shapes are chosen only when R == 4 * G
-  void (*kern)(const BlockedParams) = k_mttkrp_blocked<NP, G, VEC, CPL, ACC, FULL, SMEM, TB, MINB>;
-  const size_t smem = (SMEM ? (size_t)P.BR * P.R * 4 : 0) + sizeof(uint32_t) * (size_t)(TB / G) * BStage<NW, G>::STRIDE;
+  void (*kern)(const BlockedParams) = k_mttkrp_blocked<NP, G, VEC, CPL, ACC, FULL, NCP, TB, MINB>;
+  const size_t smem = blocked_block_bytes(P.BR, P.R, NCP) +
+                      sizeof(uint32_t) * (size_t)(TB / G) * BStage<NW, G, blocked_nst<NP>()>::STRIDE;
   // attributes are set when the dynamic shared memory grows (not per call: cheap host path, and
   // nothing but launches happens while cp_als captures an iteration into a CUDA graph)
   static size_t configured = 0;
@@ -330,7 +348,7 @@ cudaError_t launch_blocked_one(const BlockedParams& P, int nitems, cudaStream_t 
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     // carveout: shared memory for the CTAs that fit by registers/threads, the rest stays L1
-    const int ctas = TB == 256 ? 2 : 1;
+    const int ctas = std::max(1, std::min(MINB, (int)((228 * 1024) / (smem + 1024))));
     int pct = (int)((ctas * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024)) + 1;
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, pct > 100 ? 100 : pct);
     configured = smem;
@@ -343,9 +361,12 @@ cudaError_t launch_blocked_one(const BlockedParams& P, int nitems, cudaStream_t 
 
 template <int NP, int G, class ACC>
 cudaError_t launch_blocked_g4(const BlockedParams& P, int nitems, const BlockedShape& sh, cudaStream_t s) {
-  if (!sh.smem) return launch_blocked_one<NP, G, 4, 1, ACC, false, 256>(P, nitems, s);
-  if (sh.TB == 512) return launch_blocked_one<NP, G, 4, 1, ACC, true, 512>(P, nitems, s);
-  return launch_blocked_one<NP, G, 4, 1, ACC, true, 256>(P, nitems, s);
+  constexpr int C = blocked_copies(4 * G);
+  if (!sh.smem) return launch_blocked_one<NP, G, 4, 1, ACC, 0, 256>(P, nitems, s);
+  if (sh.TB == 512) return launch_blocked_one<NP, G, 4, 1, ACC, 1, 512>(P, nitems, s);
+  if constexpr (C > 1)
+    if (sh.ncp == C) return launch_blocked_one<NP, G, 4, 1, ACC, C, 256>(P, nitems, s);
+  return launch_blocked_one<NP, G, 4, 1, ACC, 1, 256>(P, nitems, s);
 }
 
 template <int NP, class ACC>
@@ -361,10 +382,10 @@ cudaError_t launch_blocked_np(const BlockedParams& P, int nitems, bool vec_ok, c
     }
   }
   switch (sh.CPL) {
-    case 1: return launch_blocked_one<NP, 32, 1, 1, ACC, false, 256>(P, nitems, s);
-    case 2: return launch_blocked_one<NP, 32, 1, 2, ACC, false, 256>(P, nitems, s);
-    case 4: return launch_blocked_one<NP, 32, 1, 4, ACC, false, 256>(P, nitems, s);
-    default: return launch_blocked_one<NP, 32, 1, 8, ACC, false, 256>(P, nitems, s);
+    case 1: return launch_blocked_one<NP, 32, 1, 1, ACC, 0, 256>(P, nitems, s);
+    case 2: return launch_blocked_one<NP, 32, 1, 2, ACC, 0, 256>(P, nitems, s);
+    case 4: return launch_blocked_one<NP, 32, 1, 4, ACC, 0, 256>(P, nitems, s);
+    default: return launch_blocked_one<NP, 32, 1, 8, ACC, 0, 256>(P, nitems, s);
   }
 }
 

@@ -233,6 +233,42 @@ __global__ void k_seg_coord_blocked(const K* __restrict__ keys, const uint32_t* 
   for (int a = 0; a < L.n_idx; ++a) seg_coord[(int64_t)s * L.n_idx + a] = (uint32_t)((key >> L.shift[a]) & L.mask[a]);
 }
 
+// ---- blocked SpTTM (op TTM): the fibre (output row) of each blocked segment ----
+// A fibre's nonzeros are spread over the blocks of U rows, so the blocked stream holds one segment
+// per (block, fibre); the SpTTM output keeps one row per fibre (Eq.(3)) in lexicographic
+// order of the index tuple, as the plain F-COO does.  The segments' tuples are sorted (key = the
+// index part of the build key, payload = segment ordinal); a new tuple in sorted order starts a
+// fibre; seg_row[s] = fibre ordinal of segment s and fib_coord[r] = tuple of fibre r.
+template <class K>
+__global__ void k_fib_keys(const uint32_t* __restrict__ seg_coord, KeyLayout L, int64_t nsegs, K* __restrict__ keys,
+                           uint32_t* __restrict__ ids) {
+  const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nsegs) return;
+  K key = 0;
+  for (int a = 0; a < L.n_idx; ++a) key |= (K)seg_coord[s * L.n_idx + a] << (L.shift[a] - L.prod_bits);
+  keys[s] = key;
+  ids[s] = (uint32_t)s;
+}
+
+template <class K>
+__global__ void k_fib_heads(const K* __restrict__ keys, int64_t n, uint32_t* __restrict__ head) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p > n) return;
+  head[p] = p == n ? 0u : (p == 0 || keys[p] != keys[p - 1]) ? 1u : 0u;
+}
+
+// excl = exclusive scan of head: fibre ordinal of sorted position p = excl[p] + head[p] - 1
+__global__ void k_fib_scatter(const uint32_t* __restrict__ ids, const uint32_t* __restrict__ head,
+                              const uint32_t* __restrict__ excl, const uint32_t* __restrict__ seg_coord, int n_idx,
+                              int64_t n, uint32_t* __restrict__ seg_row, uint32_t* __restrict__ fib_coord) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const uint32_t r = excl[p] + head[p] - 1u, s = ids[p];
+  seg_row[s] = r;
+  if (head[p])
+    for (int a = 0; a < n_idx; ++a) fib_coord[(int64_t)r * n_idx + a] = seg_coord[(int64_t)s * n_idx + a];
+}
+
 int bits_for(int64_t n) {
   int b = 0;
   while (b < 63 && ((int64_t)1 << b) < n) ++b;
@@ -255,6 +291,8 @@ void free_handle_arrays(fcoo_s* f) {
   if (f->seg_coord) f->alloc.put(f->seg_coord, f->bytes_seg_coord, s);
   if (f->perm) f->alloc.put(f->perm, f->bytes_perm, s);
   if (f->blk_start) f->alloc.put(f->blk_start, f->bytes_blk, s);
+  if (f->seg_row) f->alloc.put(f->seg_row, f->bytes_seg_row, s);
+  if (f->fib_coord) f->alloc.put(f->fib_coord, f->bytes_fib, s);
   if (f->dpart) f->alloc.put(f->dpart, f->bytes_dpart, s);
   f->dpart = nullptr;
   f->bytes_dpart = 0;
@@ -264,6 +302,7 @@ void free_handle_arrays(fcoo_s* f) {
   f->blk_start = nullptr; f->blk_end = nullptr;
   f->pidx = nullptr; f->val = nullptr; f->bf = nullptr; f->sf = nullptr;
   f->seg_base = nullptr; f->seg_coord = nullptr; f->perm = nullptr;
+  f->seg_row = nullptr; f->fib_coord = nullptr;
 }
 
 }  // namespace
@@ -535,6 +574,65 @@ fcoo_status sort_and_flag_blocked(fcoo_s* f, const fcoo_coo* coo, const KeyLayou
   return FCOO_OK;
 }
 
+// Fibre table of a blocked SpTTM handle (k_fib_*): one more sort over the segments' index tuples
+// and a third host synchronisation (the fibre count sizes fib_coord).
+template <class K>
+fcoo_status fibre_table(fcoo_s* f, const KeyLayout& L, cudaStream_t s) {
+  const int64_t n = f->nsegs;
+  const int idx_bits = L.blk_shift - L.prod_bits;
+  const int TB = 256;
+  Buf k0(&f->alloc, sizeof(K) * n, s), k1(&f->alloc, sizeof(K) * n, s);
+  Buf i0(&f->alloc, sizeof(uint32_t) * n, s), i1(&f->alloc, sizeof(uint32_t) * n, s);
+  Buf head(&f->alloc, sizeof(uint32_t) * (n + 1), s), excl(&f->alloc, sizeof(uint32_t) * (n + 1), s);
+  if (!k0.ok() || !k1.ok() || !i0.ok() || !i1.ok() || !head.ok() || !excl.ok())
+    return fail(FCOO_ERR_OOM, "fibre table scratch allocation failed");
+  f->seg_row = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)n, s, &f->bytes_seg_row);
+  if (!f->seg_row) return fail(FCOO_ERR_OOM, "seg_row allocation");
+  cudaError_t ce;
+  k_fib_keys<K><<<(unsigned)((n + TB - 1) / TB), TB, 0, s>>>(f->seg_coord, L, n, k0.as<K>(), i0.as<uint32_t>());
+  count_launch();
+  if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_fib_keys: %s", cudaGetErrorString(ce));
+  cub::DoubleBuffer<K> dk(k0.as<K>(), k1.as<K>());
+  cub::DoubleBuffer<uint32_t> dv(i0.as<uint32_t>(), i1.as<uint32_t>());
+  size_t tmp_bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, dk, dv, n, 0, std::max(1, idx_bits), s);
+  {
+    Buf cubtmp(&f->alloc, tmp_bytes, s);
+    if (!cubtmp.ok()) return fail(FCOO_ERR_OOM, "radix sort scratch");
+    if ((ce = cub::DeviceRadixSort::SortPairs(cubtmp.p, tmp_bytes, dk, dv, n, 0, std::max(1, idx_bits), s)) !=
+        cudaSuccess)
+      return fail(FCOO_ERR_CUDA, "fibre sort: %s", cudaGetErrorString(ce));
+    count_launch(2 + (idx_bits + 7) / 8);
+  }
+  k_fib_heads<K><<<(unsigned)((n + 1 + TB - 1) / TB), TB, 0, s>>>(dk.Current(), n, head.as<uint32_t>());
+  count_launch();
+  if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_fib_heads: %s", cudaGetErrorString(ce));
+  size_t scan_bytes = 0;
+  cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, head.as<uint32_t>(), excl.as<uint32_t>(), n + 1, s);
+  {
+    Buf scantmp(&f->alloc, scan_bytes, s);
+    if (!scantmp.ok()) return fail(FCOO_ERR_OOM, "scan scratch");
+    if ((ce = cub::DeviceScan::ExclusiveSum(scantmp.p, scan_bytes, head.as<uint32_t>(), excl.as<uint32_t>(), n + 1,
+                                            s)) != cudaSuccess)
+      return fail(FCOO_ERR_CUDA, "scan: %s", cudaGetErrorString(ce));
+    count_launch(2);
+  }
+  uint32_t nfib = 0;
+  if ((ce = cudaMemcpyAsync(&nfib, excl.as<uint32_t>() + n, sizeof(uint32_t), cudaMemcpyDeviceToHost, s)) !=
+          cudaSuccess ||
+      (ce = cudaStreamSynchronize(s)) != cudaSuccess)
+    return fail(FCOO_ERR_CUDA, "build sync: %s", cudaGetErrorString(ce));
+  f->nfib = nfib;
+  f->fib_coord = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)std::max<int64_t>(1, (int64_t)nfib * f->n_idx), s,
+                                &f->bytes_fib);
+  if (!f->fib_coord) return fail(FCOO_ERR_OOM, "fib_coord allocation");
+  k_fib_scatter<<<(unsigned)((n + TB - 1) / TB), TB, 0, s>>>(dv.Current(), head.as<uint32_t>(), excl.as<uint32_t>(),
+                                                            f->seg_coord, f->n_idx, n, f->seg_row, f->fib_coord);
+  count_launch();
+  if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_fib_scatter: %s", cudaGetErrorString(ce));
+  return FCOO_OK;
+}
+
 fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opts, const fcoo_allocator* alloc,
                        cudaStream_t s, fcoo_t* out) {
   if (!coo || !out) return fail(FCOO_ERR_ARG, "NULL coo/out");
@@ -552,7 +650,6 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
   int BR = 0;
   if (blocked) {
     BR = (opts && opts->block_rows) ? opts->block_rows : 512;
-    if (op != FCOO_OP_MTTKRP) return fail(FCOO_ERR_ARG, "FCOO_BUILD_BLOCKED is for FCOO_OP_MTTKRP handles");
     if (coo->order > 5) return fail(FCOO_ERR_ARG, "FCOO_BUILD_BLOCKED supports order <= 5 (got %d)", coo->order);
     if (flags & (FCOO_BUILD_DETERMINISTIC | FCOO_BUILD_PRODUCT_DESC))
       return fail(FCOO_ERR_ARG, "FCOO_BUILD_BLOCKED excludes DETERMINISTIC and PRODUCT_DESC");
@@ -613,6 +710,10 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
     st = tb <= 64 ? sort_and_flag_blocked<uint64_t>(f, coo, L, ip, tb, flags, s)
                   : sort_and_flag_blocked<unsigned __int128>(f, coo, L, ip, tb, flags, s);
     if (st) return bail(st);
+    if (op == FCOO_OP_TTM) {
+      st = tb <= 64 ? fibre_table<uint64_t>(f, L, s) : fibre_table<unsigned __int128>(f, L, s);
+      if (st) return bail(st);
+    }
     *out = f;
     return FCOO_OK;
   }

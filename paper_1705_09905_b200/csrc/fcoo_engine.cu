@@ -248,7 +248,37 @@ fcoo_status run_mttkrp_f64(fcoo_s* f, const float* const* factors, int R, double
   return mttkrp_t<double>(f, factors, R, out, s, gate, gate_on);
 }
 
+// SpTTM on a blocked handle (FCOO_BUILD_BLOCKED, op TTM): the blocked kernel with one product
+// mode (the outer = last = mode n, U's block of BR rows in shared memory); segment s flushes into
+// its fibre's row seg_row[s] with red.add, so the nfib x R output is zeroed first.
+fcoo_status ttm_blocked(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s) {
+  BlockedParams P{};
+  const bool vec_ok = (R % 4 == 0) && R <= 128 && aligned16(out) && aligned16(U);
+  P.U[0] = U;
+  P.pk = f->pidx; P.val = f->val; P.bf = f->bf; P.sf = f->sf; P.seg_base = f->seg_base; P.seg_coord = f->seg_row;
+  P.blk_start = f->blk_start; P.blk_end = f->blk_end;
+  P.nstream = f->nnz_pad; P.ntiles = f->ntiles; P.tile_begin = f->tile_begin; P.tile_end = f->tile_end;
+  P.T = (int)f->T; P.R = R; P.BR = f->block_rows; P.Io = (int)f->dims[f->mode]; P.shift = 0;
+  P.out = out;
+  FCOO_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)f->nfib * R, s));
+  const BlockedShape sh = blocked_shape(1, R, f->block_rows, vec_ok);
+  int k = 0;
+  while ((1 << k) < sh.TB / sh.G) ++k;
+  const std::vector<int2>& items = f->h_items[k];
+  const int gpc = 1 << k;
+  int64_t i0 = 0, i1 = (int64_t)items.size();
+  while (i0 < i1 && (int64_t)items[i0].y + gpc <= f->tile_begin) ++i0;
+  while (i1 > i0 && (int64_t)items[i1 - 1].y >= f->tile_end) --i1;
+  P.items = f->items[k];
+  P.item0 = i0;
+  cudaError_t e = launch_blocked<float>(P, 1, (int)(i1 - i0), vec_ok, s);
+  if (e != cudaSuccess) return fail(FCOO_ERR_CUDA, "blocked ttm launch: %s", cudaGetErrorString(e));
+  if (f->comm) return comm_allreduce(f->comm, out, (size_t)f->nfib * R, s);
+  return FCOO_OK;
+}
+
 fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s) {
+  if (f->blocked) return ttm_blocked(f, U, R, out, s);
   EngineParams P{};
   bool vec_ok = (R % 4 == 0) && R <= 128 && aligned16(out) && aligned16(U);
   P.U[0] = U;

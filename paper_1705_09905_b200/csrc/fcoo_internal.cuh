@@ -70,6 +70,12 @@ struct fcoo_s {
   int64_t* blk_start = nullptr;  // device [nblocks + 1]: first stream position of block b
   int64_t* blk_end = nullptr;    // device [nblocks]: end of block b's nonzeros
   size_t bytes_blk = 0;
+  // blocked SpTTM handles (op TTM): the output rows are the fibres (distinct index tuples in
+  // lexicographic order); seg_row[s] = fibre of blocked segment s, fib_coord = the tuples
+  uint32_t* seg_row = nullptr;    // device [nsegs]
+  uint32_t* fib_coord = nullptr;  // device [nfib x n_idx]
+  int64_t nfib = 0;
+  size_t bytes_seg_row = 0, bytes_fib = 0;
   std::vector<int64_t> h_blk_start, h_blk_end;  // host copies (work tables, export)
   // work items of the blocked SpMTTKRP, one table per groups-per-CTA value gpc = 1 << k (k < 10):
   // item = (block b, first tile t0), t0 = first tile of b + j*gpc; device int2 + host copy

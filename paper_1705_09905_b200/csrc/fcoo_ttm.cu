@@ -71,11 +71,15 @@ __device__ __forceinline__ void fma4(float4& acc, float v, const float4& w) {
   unpack2(a1, acc.z, acc.w);
 }
 
+// stream stages per lane-group (kTtmStages - 1 chunks of 32 nonzeros in flight); 4 stages
+// measured the same as 2 on brainq (the kernel is issue-bound)
+constexpr int kTtmStages = 2;
+
 template <int G, bool SMEM>
 __global__ void __launch_bounds__(256) k_ttm_lean(const TtmParams P) {
-  constexpr int TB = 256, CH = 32, B = 8;
+  constexpr int TB = 256, CH = 32, B = 8, NST = kTtmStages;
   constexpr int WORDS = 2 * CH + 4;                                   // idx, val, bf word, pad
-  constexpr int RAW = 2 * WORDS, WANT = (G >= 4 ? G : 4) % 32;
+  constexpr int RAW = NST * WORDS, WANT = (G >= 4 ? G : 4) % 32;
   constexpr int STRIDE = RAW + (((WANT - RAW % 32) % 32) + 32) % 32;  // groups of a warp on distinct banks
   extern __shared__ uint4 smem_raw[];
   const int R = 4 * G;
@@ -148,15 +152,18 @@ __global__ void __launch_bounds__(256) k_ttm_lean(const TtmParams P) {
       }
       if (gl == 0 && ci < nchunk) cp_async4(my + st * WORDS + 2 * CH, P.bf + ((p0 + (int64_t)ci * CH) >> 5));
     };
-    issue(0, 0);
-    cp_async_commit();
-    for (int ci = 0; ci < nchunk_w; ++ci) {
-      if (ci + 1 < nchunk_w) issue(ci + 1, (ci + 1) & 1);
+#pragma unroll
+    for (int j = 0; j + 1 < NST; ++j) {  // NST - 1 chunks in flight
+      if (j < nchunk_w) issue(j, j);
       cp_async_commit();
-      cp_async_wait<1>();
+    }
+    for (int ci = 0; ci < nchunk_w; ++ci) {
+      if (ci + NST - 1 < nchunk_w) issue(ci + NST - 1, (ci + NST - 1) % NST);
+      cp_async_commit();
+      cp_async_wait<NST - 1>();
       __syncwarp();  // the warp's groups copy each other's chunks
       const bool on = ci < nchunk;  // this group's chunk exists
-      const uint32_t* stg = my + (ci & 1) * WORDS;
+      const uint32_t* stg = my + (ci % NST) * WORDS;
       uint32_t bfw = on ? stg[2 * CH] : 0u;
       if (ci == 0) bfw &= ~1u;  // the tile's first nonzero opens (never closes) a segment
 #pragma unroll
@@ -220,7 +227,7 @@ __global__ void __launch_bounds__(256) k_ttm_lean(const TtmParams P) {
 template <int G, bool SMEM>
 cudaError_t launch_ttm(const TtmParams& P, cudaStream_t s) {
   constexpr int TB = 256;
-  constexpr int WORDS = 2 * 32 + 4, RAW = 2 * WORDS, WANT = (G >= 4 ? G : 4) % 32;
+  constexpr int WORDS = 2 * 32 + 4, RAW = kTtmStages * WORDS, WANT = (G >= 4 ? G : 4) % 32;
   constexpr int STRIDE = RAW + (((WANT - RAW % 32) % 32) + 32) % 32;
   constexpr int SB = 16 * G >= 128 ? 16 * G : 128;
   const size_t smem = sizeof(uint32_t) * (size_t)(TB / G) * STRIDE + (SMEM ? (size_t)P.In * SB : 0);
@@ -258,7 +265,7 @@ bool run_ttm_lean(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s, 
   P.nnz = f->nnz; P.ntiles = f->ntiles; P.tile_begin = f->tile_begin; P.tile_end = f->tile_end;
   P.T = (int)f->T; P.R = R; P.In = (int)f->dims[f->mode];
   // U in shared memory up to 32 KB with rows padded to >= 128 B (the staging of 256 threads takes
-  // <= 84 KB; 2-3 CTAs per SM)
+  // 35 KB at R = 16, 70 KB at R = 8)
   const bool smem = (size_t)P.In * std::max(R * 4, 128) <= 32 * 1024;
   cudaError_t e;
   switch (q) {

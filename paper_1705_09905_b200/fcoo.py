@@ -58,14 +58,14 @@ class _Info(ctypes.Structure):
                 ("device_bytes", ctypes.c_int64), ("shard", ctypes.c_int), ("nshards", ctypes.c_int),
                 ("tile_begin", ctypes.c_int64), ("tile_end", ctypes.c_int64), ("blocked", ctypes.c_int),
                 ("block_rows", ctypes.c_int), ("nblocks", ctypes.c_int64), ("nstream", ctypes.c_int64),
-                ("pk_shift", ctypes.c_int), ("n_words", ctypes.c_int)]
+                ("pk_shift", ctypes.c_int), ("n_words", ctypes.c_int), ("nfib", ctypes.c_int64)]
 
 
 class _HostView(ctypes.Structure):
     _fields_ = [("perm", ctypes.c_void_p), ("bf", ctypes.c_void_p), ("sf", ctypes.c_void_p),
                 ("seg_base", ctypes.c_void_p), ("seg_coord", ctypes.c_void_p), ("pidx", ctypes.c_void_p),
                 ("val", ctypes.c_void_p), ("pk", ctypes.c_void_p), ("blk_start", ctypes.c_void_p),
-                ("blk_end", ctypes.c_void_p)]
+                ("blk_end", ctypes.c_void_p), ("seg_row", ctypes.c_void_p), ("fib_coord", ctypes.c_void_p)]
 
 
 class _CpOpts(ctypes.Structure):
@@ -268,6 +268,7 @@ class Info:
     nstream: int = 0
     pk_shift: int = 0
     n_words: int = 0
+    nfib: int = 0  # SpTTM: output rows (fibres)
 
 
 class Fcoo:
@@ -286,7 +287,7 @@ class Fcoo:
                     list(inf.prod_modes[: inf.n_prod]), list(inf.dims[:o]), inf.nnz, inf.nsegs, inf.ntiles,
                     inf.tile_nnz, bool(inf.dense_rows), inf.storage_bytes, inf.seg_table_bytes, inf.device_bytes,
                     inf.shard, inf.nshards, inf.tile_begin, inf.tile_end, bool(inf.blocked), inf.block_rows,
-                    inf.nblocks, inf.nstream, inf.pk_shift, inf.n_words)
+                    inf.nblocks, inf.nstream, inf.pk_shift, inf.n_words, inf.nfib)
 
     def destroy(self):
         if self.h:
@@ -371,7 +372,7 @@ def fcoo_ttm(f: Fcoo, U: torch.Tensor, R: int, out: torch.Tensor, stream=None) -
     _require_cuda(U, torch.float32, "U")
     if tuple(U.shape) != (f.info.dims[f.info.mode], R):
         raise ValueError(f"U has shape {tuple(U.shape)}, expected {(f.info.dims[f.info.mode], R)}")
-    _check_out(out, f.info.nsegs, R)
+    _check_out(out, f.info.nfib, R)
     _check(L.fcoo_ttm(f.h, ctypes.c_void_p(U.data_ptr()), R, ctypes.c_void_p(out.data_ptr()),
                       ctypes.c_void_p(_stream_ptr(stream))), "fcoo_ttm")
     return out
@@ -430,11 +431,15 @@ def fcoo_export(f: Fcoo, perm: bool = False, stream=None) -> dict:
         d["pk"] = np.zeros((i.n_words, ns), np.uint32)
         d["blk_start"] = np.zeros(i.nblocks + 1, np.int64)
         d["blk_end"] = np.zeros(i.nblocks, np.int64)
+        if i.op == OP_TTM:
+            d["seg_row"] = np.zeros(i.nsegs, np.uint32)
+    if i.op == OP_TTM:
+        d["fib_coord"] = np.zeros((i.nfib, i.n_idx), np.uint32)
     if perm:
         d["perm"] = np.zeros(ns, np.uint32)
     v = _HostView(*(d[k].ctypes.data if k in d else None
                     for k in ("perm", "bf", "sf", "seg_base", "seg_coord", "pidx", "val", "pk", "blk_start",
-                              "blk_end")))
+                              "blk_end", "seg_row", "fib_coord")))
     _check(load_library().fcoo_export(f.h, ctypes.byref(v), ctypes.c_void_p(_stream_ptr(stream))), "fcoo_export")
     return d
 

@@ -73,7 +73,7 @@ def test_blocked_build_errors(F):
     w = gen.WORKLOADS["tiny"]
     idx, val = gen.coo(w.dims, w.nnz, w.alpha, w.seed)
     coo = F.Coo.from_numpy(w.dims, idx, val)
-    for kw, code in ((dict(op=F.OP_TTM), F.ERR_ARG), (dict(deterministic=True), F.ERR_ARG),
+    for kw, code in ((dict(deterministic=True), F.ERR_ARG),
                      (dict(product_desc=True), F.ERR_ARG), (dict(block_rows=16), F.ERR_ARG),
                      (dict(block_rows=70000), F.ERR_ARG)):
         with pytest.raises(F.FcooError) as e:

@@ -14,6 +14,9 @@
 //   6 LDG+LDS+TEX : three rows per step, one per path
 // ACT: fraction of lane-groups (out of 4 per warp, in 1/4 steps) that issue the gathers (the rest
 // are predicated off) — mimics per-group reuse that skips a row.
+// SHARE (1, 2, 4, 8): consecutive lane-groups of a warp, SHARE at a time, draw the SAME shared-memory
+// row (LDS paths; LDG rows stay distinct per group) — does an LDS.128 whose quarter-warps read one
+// row cost fewer data-pipe wavefronts (warp-cooperative fibre reuse)?
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -58,7 +61,7 @@ __device__ __forceinline__ float4 lds1(bool q, uint32_t a) {
 
 template <int R, int VEC, int PATH, int U>
 __global__ void __launch_bounds__(256) k_gather(const float* __restrict__ table, cudaTextureObject_t tex, uint32_t rows,
-                                                uint32_t srows, int steps, int act4, float* __restrict__ out) {
+                                                uint32_t srows, int steps, int act4, int share, float* __restrict__ out) {
   extern __shared__ float4 smraw[];
   constexpr bool use_lds = PATH == 2 || PATH == 4 || PATH == 5 || PATH == 6;
   if (use_lds) {
@@ -75,11 +78,13 @@ __global__ void __launch_bounds__(256) k_gather(const float* __restrict__ table,
   const uint32_t sb = (uint32_t)__cvta_generic_to_shared(smraw) + col * 4;
   float4 acc = make_float4(0, 0, 0, 0);
   uint32_t x = grp * 0x9e3779b9u + 12345u;
+  uint32_t xs = (grp / (uint32_t)share) * 0x9e3779b9u + 777u;  // shared-memory row draws
   for (int s = 0; s < steps; ++s) {
     float4 r[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       x = x * 1664525u + 1013904223u;  // LCG: one IMAD per row
+      xs = xs * 1664525u + 1013904223u;
       int path = PATH;
       if (PATH == 3) path = (u & 1) ? 1 : 0;
       if (PATH == 4) path = (u & 1) ? 2 : 0;
@@ -89,7 +94,7 @@ __global__ void __launch_bounds__(256) k_gather(const float* __restrict__ table,
         const float* p = tb + (size_t)__umulhi(x, rows) * R;
         r[u] = VEC == 4 ? ldg4(active, p) : VEC == 2 ? ldg2(active, p) : ldg1(active, p);
       } else if (path == 2) {
-        const uint32_t a = sb + __umulhi(x, srows) * (R * 4);
+        const uint32_t a = sb + __umulhi(xs, srows) * (R * 4);
         r[u] = VEC == 4 ? lds4(active, a) : VEC == 2 ? lds2(active, a) : lds1(active, a);
       } else {  // texture: float4 texels, G = R/4 lanes per row (VEC == 4 only)
         r[u] = active ? tex1Dfetch<float4>(tex, (int)(__umulhi(x, rows) * (uint32_t)(R / 4) + gl)) : make_float4(0, 0, 0, 0);
@@ -103,18 +108,18 @@ __global__ void __launch_bounds__(256) k_gather(const float* __restrict__ table,
 
 template <int R, int VEC, int PATH>
 static void launch(const float* table, cudaTextureObject_t tex, uint32_t rows, uint32_t srows, int steps,
-                   int act4, float* out, unsigned blocks, size_t smem, cudaStream_t s) {
+                   int act4, int share, float* out, unsigned blocks, size_t smem, cudaStream_t s) {
   constexpr int U = (PATH == 6) ? 12 : 8;
   auto k = k_gather<R, VEC, PATH, U>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, smem ? 100 : 0);
-  k<<<blocks, 256, smem, s>>>(table, tex, rows, srows, steps, act4, out);
+  k<<<blocks, 256, smem, s>>>(table, tex, rows, srows, steps, act4, share, out);
 }
 
 template <int R>
 static void go_r(int vec, int path, const float* table, cudaTextureObject_t tex, uint32_t rows, uint32_t srows,
-                 int steps, int act4, float* out, unsigned blocks, size_t smem, cudaStream_t s) {
-#define GO(VV, PP) launch<R, VV, PP>(table, tex, rows, srows, steps, act4, out, blocks, smem, s)
+                 int steps, int act4, int share, float* out, unsigned blocks, size_t smem, cudaStream_t s) {
+#define GO(VV, PP) launch<R, VV, PP>(table, tex, rows, srows, steps, act4, share, out, blocks, smem, s)
   if (vec == 4) {
     switch (path) {
       case 0: GO(4, 0); break; case 1: GO(4, 1); break; case 2: GO(4, 2); break; case 3: GO(4, 3); break;
@@ -131,8 +136,8 @@ static void go_r(int vec, int path, const float* table, cudaTextureObject_t tex,
 }
 
 // Returns the number of row gathers issued per launch in *n_rows and the mean launch time in *ms_out.
-extern "C" int gather_bench2(const float* table, uint32_t rows, int R, int vec, int path, uint32_t srows, int act4,
-                             int blocks_per_sm, int steps, float* out, void* stream, int reps, float* ms_out,
+extern "C" int gather_bench3(const float* table, uint32_t rows, int R, int vec, int path, uint32_t srows, int act4,
+                             int share, int blocks_per_sm, int steps, float* out, void* stream, int reps, float* ms_out,
                              double* n_rows) {
   cudaStream_t s = (cudaStream_t)stream;
   int dev = 0, nsm = 148;
@@ -153,9 +158,9 @@ extern "C" int gather_bench2(const float* table, uint32_t rows, int R, int vec, 
   const bool lds = path == 2 || path == 4 || path == 5 || path == 6;
   const size_t smem = lds ? (size_t)srows * R * 4 : 0;
   auto go = [&]() {
-    if (R == 16) go_r<16>(vec, path, table, tex, rows, srows, steps, act4, out, blocks, smem, s);
-    else if (R == 32) go_r<32>(vec, path, table, tex, rows, srows, steps, act4, out, blocks, smem, s);
-    else go_r<64>(vec, path, table, tex, rows, srows, steps, act4, out, blocks, smem, s);
+    if (R == 16) go_r<16>(vec, path, table, tex, rows, srows, steps, act4, share, out, blocks, smem, s);
+    else if (R == 32) go_r<32>(vec, path, table, tex, rows, srows, steps, act4, share, out, blocks, smem, s);
+    else go_r<64>(vec, path, table, tex, rows, srows, steps, act4, share, out, blocks, smem, s);
   };
   go();
   cudaEvent_t e0, e1;

@@ -30,31 +30,42 @@ def build():
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--share", action="store_true", help="only the shared-row (warp-cooperative reuse) sweep")
     ap.add_argument("--clock-mhz", type=float, default=1965.0)
     a = ap.parse_args()
     import torch
     L = ctypes.CDLL(build())
-    L.gather_bench2.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_int, ctypes.c_int, ctypes.c_int,
-                                ctypes.c_uint32, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
+    L.gather_bench3.argtypes = [ctypes.c_void_p, ctypes.c_uint32, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                ctypes.c_uint32, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_void_p,
                                 ctypes.c_void_p, ctypes.c_int, ctypes.POINTER(ctypes.c_float),
                                 ctypes.POINTER(ctypes.c_double)]
     nsm = torch.cuda.get_device_properties(0).multi_processor_count
     out = torch.zeros(1 << 22, device="cuda")
     s = torch.cuda.current_stream().cuda_stream
 
-    def cell(R, rows, vec, path, act4=4, srows=0, bps=4, steps=400):
+    def cell(R, rows, vec, path, act4=4, srows=0, bps=4, steps=400, share=1):
         table = torch.rand(rows, R, device="cuda")
         ms, nr = ctypes.c_float(0), ctypes.c_double(0)
-        rc = L.gather_bench2(table.data_ptr(), rows, R, vec, path, srows, act4, bps, steps, out.data_ptr(), s, 5,
+        rc = L.gather_bench3(table.data_ptr(), rows, R, vec, path, srows, act4, share, bps, steps, out.data_ptr(), s, 5,
                              ctypes.byref(ms), ctypes.byref(nr))
         t = ms.value / 1e3
         rps = nr.value / t
         line = {"R": R, "rows": rows, "table_MB": rows * R * 4 / 1e6, "lanes_per_row": R // vec, "vec": vec,
                 "path": PATHS[path], "smem_rows": srows, "active_groups": act4 / 4, "ctas_per_sm": bps,
+                "groups_sharing_lds_row": share,
                 "grows_per_s": rps / 1e9, "rows_per_clk_sm": rps / (nsm * a.clock_mhz * 1e6),
                 "bytes_per_clk_sm": rps * R * 4 / (nsm * a.clock_mhz * 1e6), "rc": rc}
         print(json.dumps(line), flush=True)
 
+    if a.share:  # warp-cooperative reuse: lane-groups of a warp reading one shared-memory row
+        for R in (16, 32, 64):
+            srows = 12288 // R
+            for share in (1, 2, 4, 8):
+                if share * R // 4 > 32:
+                    continue
+                cell(R, srows, 4, 2, srows=srows, share=share)
+                cell(R, 28818, 4, 4, srows=srows, share=share)
+        return
     Rs = (32,) if a.quick else (16, 32, 64)
     for R in Rs:
         srows = 12288 // R  # 48 KB of shared memory: 4 CTAs/SM

@@ -62,6 +62,10 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--oracle-s", type=float, default=4.0)
     ap.add_argument("--ttmc-R", default="8,16,32")
+    ap.add_argument("--ttm-layout", default="auto", choices=["auto", "fcoo", "blocked"],
+                    help="auto: blocked F-COO when U does not fit the lean kernel's shared memory (32 KB)")
+    ap.add_argument("--ttm-br", type=int, default=0, help="block rows of a blocked SpTTM handle (0 = default)")
+    ap.add_argument("--ttm-tile", type=int, default=0, help="tile of the SpTTM handles (0 = automatic)")
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -83,15 +87,18 @@ def main():
         nnz, R = int(val.shape[0]), 16
         fs = gen.factors(w.dims, R, 7)
         for n in range(3):
-            h = P.fcoo_build(coo, n, op=P.OP_TTM)
+            blocked = a.ttm_layout == "blocked" or (a.ttm_layout == "auto" and w.dims[n] * max(4 * R, 128) > 32768)
+            h = P.fcoo_build(coo, n, op=P.OP_TTM, blocked=blocked, block_rows=a.ttm_br if blocked else 0,
+                             tile_nnz=a.ttm_tile)
             U = torch.from_numpy(fs[n]).cuda()
-            out = torch.empty((h.info.nsegs, R), device="cuda")
+            out = torch.empty((h.info.nfib, R), device="cuda")
             ms = gpu_ms(lambda: P.fcoo_ttm(h, U, R, out), a.reps)
             ntl = h.info.ntiles
-            b = nnz * 8 + (nnz + 7) // 8 + 4 * ((ntl + 31) // 32) + 4 * w.dims[n] * R + 4 * h.info.nsegs * R
+            b = nnz * 8 + (nnz + 7) // 8 + 4 * ((ntl + 31) // 32) + 4 * w.dims[n] * R + 4 * h.info.nfib * R
             rate, k, dt = oracle_rate(lambda k: oracle.ttm(w.dims, idx[:, :k], val[:k], n, fs[n]), nnz, a.oracle_s)
             emit({"op": "ttm", "workload": "brainq", "mode": n, "R": R, "tile": h.info.tile_nnz,
-                  "nsegs": h.info.nsegs, "ms": round(ms, 4), "gnnz_s": round(nnz / ms / 1e6, 2),
+                  "layout": "blocked" if blocked else "fcoo", "block_rows": h.info.block_rows,
+                  "nsegs": h.info.nsegs, "nfib": h.info.nfib, "ms": round(ms, 4), "gnnz_s": round(nnz / ms / 1e6, 2),
                   "gflops": round(2 * R * nnz / ms / 1e6, 1),
                   "roofline": {"bound": "hbm", "bytes": b, "achieved_gbs": round(b / ms / 1e6, 1), "peak": peak,
                                "peak_source": peak_src, "frac": round(b / ms / 1e6 / peak, 4)},
