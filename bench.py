@@ -44,6 +44,9 @@ def parse():
                          "fcoo: the plain F-COO of the paper")
     ap.add_argument("--block-rows", type=int, default=0, help="block_rows for --layout blocked (0 = default)")
     ap.add_argument("--nnz", type=int, default=None, help="override nnz (debug only; not a bench number)")
+    ap.add_argument("--combine", default="rows", choices=["rows", "allreduce"],
+                    help="N > 1: rows = distributed build (each rank holds the nnz-balanced rows of its chunk "
+                         "exchange, owned-rows all-gather); allreduce = redundant build, tile shards, sum all-reduce")
     ap.add_argument("--fused-combine", action="store_true",
                     help="N > 1: combine the ranks' partial outputs in the MTTKRP epilogue through an NVLS "
                          "multicast buffer (fcoo_mttkrp_mc) instead of a separate NCCL all-reduce")
@@ -252,9 +255,22 @@ def main():
     P.fcoo_build(coo, 0, tile_nnz=T, **bkw).destroy()  # warm-up: module load, allocator, CUB tuning
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    # N > 1: fcoo_build_sharded = the redundant build + this rank's tile-aligned slice
-    H = [P.fcoo_build_sharded(coo, n, comm, tile_nnz=T, **bkw) if world > 1 else P.fcoo_build(coo, n, tile_nnz=T, **bkw)
-         for n in range(N)]
+    rows = world > 1 and a.combine == "rows" and not a.fused_combine
+    # this rank's chunk of the input (draw order): the distributed build starts from it
+    lo_q, hi_q = nnz * rank // world, nnz * (rank + 1) // world
+    chunk = P.Coo(dims, coo.idx[:, lo_q:hi_q].contiguous(), coo.val[lo_q:hi_q].contiguous()) if rows else None
+
+    def build_all(c, ch, s=None):
+        # N > 1, rows: fcoo_build_distributed = histogram, all-reduce, nnz-balanced row ranges, bucket
+        # exchange, build of this rank's rows (SURVEY §8(e) owned-rows alternative, §8(f)-4);
+        # allreduce: fcoo_build_sharded = the redundant build + this rank's tile-aligned slice (§8(e) v1)
+        if rows:
+            return [P.fcoo_build_distributed(ch, n, comm, tile_nnz=T, stream=s, **bkw) for n in range(N)]
+        if world > 1:
+            return [P.fcoo_build_sharded(c, n, comm, tile_nnz=T, stream=s, **bkw) for n in range(N)]
+        return [P.fcoo_build(c, n, tile_nnz=T, stream=s, **bkw) for n in range(N)]
+
+    H = build_all(coo, chunk)
     T = H[0].info.tile_nnz  # the tile actually used (0 = automatic)
     torch.cuda.synchronize()
     build_ms = (time.perf_counter() - t0) * 1e3
@@ -381,7 +397,9 @@ def main():
                                f"seed {w.seed}",
                    "R": R, "modes": list(range(N)), "tile_nnz": T, "layout": a.layout,
                    "block_rows": H[0].info.block_rows if blocked else None,
-                   "parallelism": (f"nnz-sharded x{world}, factors replicated, "
+                   "parallelism": (f"row-partitioned x{world} (distributed build, nnz-balanced index-mode row "
+                                   "ranges per mode), factors replicated, owned-rows all-gather per mode" if rows else
+                                   f"nnz-sharded x{world}, factors replicated, "
                                    + ("combine fused into the MTTKRP epilogue (NVLS multicast)" if mc is not None
                                       else "NCCL all-reduce per mode")) if world > 1
                    else "1 GPU",
@@ -487,8 +505,10 @@ def main():
 
     # ---- e2e_with_build: host COO (pinned) -> device, build every mode, MTTKRP every mode -> host ----
     if not a.no_e2e:
-        idx_h = torch.from_numpy(idx_np.view(np.int32)).pin_memory()
-        val_h = torch.from_numpy(val_np).pin_memory()
+        # rows: each rank uploads only its own chunk of the COO (the distributed build exchanges the rest)
+        qs = slice(lo_q, hi_q) if rows else slice(0, nnz)
+        idx_h = torch.from_numpy(np.ascontiguousarray(idx_np[:, qs]).view(np.int32)).pin_memory()
+        val_h = torch.from_numpy(np.ascontiguousarray(val_np[qs])).pin_memory()
         h2d = idx_h.numel() * 4 + val_h.numel() * 4 + sum(f.numel() * 4 for f in f_h)
         d2h = sum(o.numel() * 4 for o in o_h)
 
@@ -497,8 +517,7 @@ def main():
             val_d = val_h.to(dev, non_blocking=True)
             fd = [f.to(dev, non_blocking=True) for f in f_h]
             c = P.Coo(dims, idx_d, val_d)
-            hs = [P.fcoo_build_sharded(c, n, comm, tile_nnz=T, stream=stream, **bkw) if world > 1
-                  else P.fcoo_build(c, n, tile_nnz=T, stream=stream, **bkw) for n in range(N)]
+            hs = build_all(None if rows else c, c if rows else None, stream)
             for n in range(N):
                 P.fcoo_mttkrp(hs[n], fd, R, outs[n], stream)
                 o_h[n].copy_(outs[n], non_blocking=True)

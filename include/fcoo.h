@@ -192,6 +192,9 @@ typedef struct {
   int n_words;             /* packed words per nonzero (blocked handles: 1 + max(0, n_prod - 2)) */
   int64_t nfib;            /* SpTTM handles: output rows = fibres (non-empty index tuples); = nsegs for a
                               plain handle, <= nsegs for a blocked one (a fibre recurs once per block); 0 for MTTKRP */
+  int row_sharded;         /* fcoo_set_row_shard / fcoo_build_distributed with nranks > 1 */
+  int row_rank, row_nranks;
+  int64_t row_begin, row_end; /* index-mode rows this handle holds ([0, I_n) when not row-sharded) */
 } fcoo_info_t;
 
 /* fcoo_info — host-side metadata; no device work. */
@@ -291,6 +294,56 @@ fcoo_status fcoo_build_sharded(const fcoo_coo* coo, int mode, const fcoo_build_o
 /* fcoo_shard_range — the tile range fcoo_set_shard uses (pure host arithmetic, no device):
  * [*begin, *end) = [floor(shard*ntiles/nshards), floor((shard+1)*ntiles/nshards)). */
 fcoo_status fcoo_shard_range(int64_t ntiles, int shard, int nshards, int64_t* begin, int64_t* end);
+
+/* ---- distributed build and owned-rows combine (SURVEY §8(e) alternative, §8(f)-4) ----
+ * The tile shards above split one redundantly-built stream and sum partial outputs.  The row-
+ * partitioned path instead gives rank k the nonzeros of the index-mode rows [b_k, b_{k+1}) only:
+ * slices (the SpMTTKRP segments, Eq.(6)) never cross ranks, so each rank's output rows
+ * there are complete and the combine is an all-gather of owned row ranges (one NCCL group of
+ * in-place broadcasts: about half the bytes of the all-reduce), and no rank sorts more than its
+ * own nonzeros.  The steps are exported separately so each can be tested on one GPU. */
+
+/* fcoo_slice_histogram — hist[i] = number of nonzeros of `coo` with coordinate i in `mode`
+ * (hist: device u32[dims[mode]], overwritten).  nnz may be 0.  Errors: ARG, ORDER, MODE,
+ * INDEX_RANGE (synchronises `stream` to report it), CUDA. */
+fcoo_status fcoo_slice_histogram(const fcoo_coo* coo, int mode, uint32_t* hist, void* stream);
+
+/* fcoo_row_partition — host arithmetic, no device.  From a (global) slice histogram hist[0..I)
+ * (host), the row bounds of nranks contiguous ranges balanced by nonzero count:
+ *   bounds[0] = 0, bounds[nranks] = I, and for 0 < k < nranks bounds[k] = the smallest r with
+ *   sum(hist[0..r)) >= ceil(k * nnz / nranks), nnz = sum(hist).
+ * A slice heavier than nnz / nranks can leave a rank with no rows (bounds[k] == bounds[k+1]).
+ * bounds: host int64[nranks + 1].  Errors: ARG. */
+fcoo_status fcoo_row_partition(const uint32_t* hist, int64_t I, int nranks, int64_t* bounds);
+
+/* fcoo_bucket_rows — stable partition of the nonzeros of `coo` by destination rank (the k with
+ * bounds[k] <= i_mode < bounds[k+1]): idx_out (host array of `order` DEVICE pointers, nnz u32
+ * each) and val_out (device, nnz f32) receive the nonzeros grouped by destination in rank order,
+ * input order kept inside a group; counts (host int64[nranks]) the group sizes.  Synchronises.
+ * Errors: ARG, ORDER, MODE, INDEX_RANGE (a coordinate >= bounds[nranks]), OOM, CUDA. */
+fcoo_status fcoo_bucket_rows(const fcoo_coo* coo, int mode, const int64_t* bounds, int nranks,
+                             uint32_t* const* idx_out, float* val_out, int64_t* counts, const fcoo_allocator* alloc,
+                             void* stream);
+
+/* fcoo_set_row_shard — declare that MTTKRP handle f holds exactly the nonzeros of rows
+ * [bounds[rank], bounds[rank+1]) of the whole tensor (bounds: host int64[nranks+1], from 0 to I_n,
+ * non-decreasing).  fcoo_mttkrp then writes those complete rows and, with a comm of nranks ranks
+ * whose rank is `rank`, all-gathers every rank's owned rows so each holds the full output; with
+ * comm == NULL the output holds this rank's rows only (the others 0).  Checks on the device that
+ * the handle's rows lie in its range (one host sync).  Excludes fcoo_set_shard tile shards and the
+ * fused multicast combine.  Errors: ARG, SHAPE (SpTTM handle), OOM, CUDA. */
+fcoo_status fcoo_set_row_shard(fcoo_t f, int rank, int nranks, const int64_t* bounds, fcoo_comm_t comm);
+
+/* fcoo_build_distributed — COLLECTIVE over comm: each rank passes its own chunk `local` of the
+ * tensor (any split of the nonzeros; nnz may be 0 on some ranks; same order and dims everywhere)
+ * and receives the F-COO handle (FCOO_OP_MTTKRP only) of its rows of `mode`:
+ *   fcoo_slice_histogram -> NCCL all-reduce -> fcoo_row_partition -> fcoo_bucket_rows ->
+ *   NCCL all-gather of the per-destination counts -> grouped ncclSend/ncclRecv of the buckets
+ *   (self included) -> fcoo_build (opts: tile, flags, block rows as usual) -> fcoo_set_row_shard.
+ * A rank whose range received no nonzeros gets an empty handle (its rows read 0).  Synchronises the
+ * host several times (setup path).  Errors: as fcoo_build, plus SHAPE (opts->op != MTTKRP), NCCL. */
+fcoo_status fcoo_build_distributed(const fcoo_coo* local, int mode, const fcoo_build_opts* opts, fcoo_comm_t comm,
+                                   const fcoo_allocator* alloc, void* stream, fcoo_t* out);
 
 /* ---- CP-ALS (Algorithm 1, generalised to order N) ----
  * Per iteration, for n = 0..N-1: M = MTTKRP_n (fcoo_mttkrp, one F-COO handle per mode built up

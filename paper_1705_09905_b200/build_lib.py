@@ -18,7 +18,7 @@ TAG = os.environ.get("FCOO_BUILD_TAG", "")
 EXTRA = os.environ.get("FCOO_NVCC_EXTRA", "").split()
 LIB = os.path.join(PKG, f"libfcoo_{TAG}.so" if TAG else "libfcoo.so")
 OBJ = os.path.join(PKG, f"build_{TAG}" if TAG else "build")
-SOURCES = ["fcoo_api.cu", "fcoo_build.cu", "fcoo_engine.cu", "fcoo_cp.cu", "fcoo_comm.cu", "fcoo_ttmc.cu", "fcoo_ttm.cu", "fcoo_tns.cpp"] + [
+SOURCES = ["fcoo_api.cu", "fcoo_build.cu", "fcoo_engine.cu", "fcoo_cp.cu", "fcoo_comm.cu", "fcoo_ttmc.cu", "fcoo_ttm.cu", "fcoo_dist.cu", "fcoo_tns.cpp"] + [
     f"fcoo_engine_np{k}.cu" for k in range(1, 8)] + [f"fcoo_blocked_np{k}_{a}.cu" for k in range(1, 5) for a in ("f32", "f64")]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

@@ -178,6 +178,11 @@ fcoo_status fcoo_info(fcoo_t f, fcoo_info_t* info) {
   if (f->blocked)  // packed words + values + bf over the padded stream, block tables
     info->device_bytes += (int64_t)(f->bytes_blk + f->bytes_seg_row + f->bytes_fib);
   info->nfib = f->op != FCOO_OP_TTM ? 0 : f->blocked ? f->nfib : f->nsegs;
+  info->row_sharded = f->row_sharded;
+  info->row_rank = f->row_rank;
+  info->row_nranks = f->row_nranks;
+  info->row_begin = f->row_sharded ? f->row_bounds[f->row_rank] : 0;
+  info->row_end = f->row_sharded ? f->row_bounds[f->row_rank + 1] : f->dims[f->mode];
   return FCOO_OK;
 }
 
@@ -282,6 +287,7 @@ fcoo_status fcoo_set_shard(fcoo_t f, int shard, int nshards, fcoo_comm_t comm) {
   f->nshards = nshards;
   f->tile_begin = b;
   f->tile_end = e;
+  if (f->row_sharded && nshards > 1) return fcoo::fail(FCOO_ERR_ARG, "handle is row-sharded (fcoo_set_row_shard)");
   f->comm = nshards > 1 ? comm : nullptr;
   return FCOO_OK;
 }

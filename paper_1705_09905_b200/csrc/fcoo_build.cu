@@ -734,6 +734,23 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
   return FCOO_OK;
 }
 
+fcoo_status build_empty(int order, const int64_t* dims, int op, int mode, const fcoo_allocator* alloc, cudaStream_t s,
+                        fcoo_t* out) {
+  if (!dims || !out) return fail(FCOO_ERR_ARG, "NULL dims/out");
+  fcoo_s tmp;
+  fcoo_status st = plan_modes(&tmp, order, dims, op, mode);
+  if (st) return st;
+  fcoo_s* f = new fcoo_s(tmp);
+  if (alloc && alloc->alloc && alloc->free) { f->alloc.a = *alloc; f->alloc.custom = true; }
+  f->build_stream = s;
+  cudaGetDevice(&f->device);
+  f->T = 32;
+  f->nnz = f->nnz_pad = f->ntiles = f->nsegs = 0;
+  f->tile_begin = f->tile_end = 0;
+  *out = f;
+  return FCOO_OK;
+}
+
 void destroy_impl(fcoo_s* f) {
   if (!f) return;
   free_handle_arrays(f);

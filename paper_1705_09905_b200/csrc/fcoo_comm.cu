@@ -58,6 +58,56 @@ fcoo_status comm_barrier(fcoo_comm_t c, cudaStream_t s) {
   return nccl_status(c, ncclAllReduce(c->scratch, c->scratch, 1, ncclInt, ncclSum, c->comm, s), "barrier");
 }
 
+// Owned-rows combine ("boundary-row fixup + all-gather of owned rows, which halves
+// the bytes" of the all-reduce): on a row-sharded handle no row is partial on two ranks, so rank k
+// broadcasts its complete rows [bounds[k], bounds[k+1]) in place; the nranks broadcasts form one
+// NCCL group (one launch).  Every rank calls it with the same bounds.
+fcoo_status comm_gather_rows(fcoo_comm_t c, float* out, const std::vector<int64_t>& bounds, int R, cudaStream_t s) {
+  if (!c || !c->comm || c->nranks == 1) return FCOO_OK;
+  if ((int)bounds.size() != c->nranks + 1) return fail(FCOO_ERR_ARG, "row bounds for %d ranks, comm has %d",
+                                                       (int)bounds.size() - 1, c->nranks);
+  ncclResult_t r = ncclGroupStart();
+  for (int k = 0; k < c->nranks && r == ncclSuccess; ++k) {
+    const size_t n = (size_t)(bounds[k + 1] - bounds[k]) * (size_t)R;
+    if (n == 0) continue;
+    float* p = out + (size_t)bounds[k] * (size_t)R;
+    r = ncclBroadcast(p, p, n, ncclFloat, k, c->comm, s);
+  }
+  const ncclResult_t r2 = ncclGroupEnd();
+  return nccl_status(c, r != ncclSuccess ? r : r2, "owned-rows gather (ncclBroadcast group)");
+}
+
+fcoo_status comm_allreduce_u32(fcoo_comm_t c, uint32_t* buf, size_t count, cudaStream_t s) {
+  if (!c || !c->comm) return FCOO_OK;
+  return nccl_status(c, ncclAllReduce(buf, buf, count, ncclUint32, ncclSum, c->comm, s), "ncclAllReduce(u32)");
+}
+
+fcoo_status comm_allgather_u64(fcoo_comm_t c, const uint64_t* send, uint64_t* recv, size_t count, cudaStream_t s) {
+  if (!c || !c->comm) return fail(FCOO_ERR_ARG, "all-gather needs a comm");
+  return nccl_status(c, ncclAllGather(send, recv, count, ncclUint64, c->comm, s), "ncclAllGather(u64)");
+}
+
+// Grouped point-to-point exchange (the all-to-all of the distributed build): items of `elem`
+// bytes, send_counts[j] of them to rank j from consecutive ranges of sendbuf, recv_counts[j] from
+// rank j into consecutive ranges of recvbuf (self included).  Counts must agree pairwise.
+fcoo_status comm_exchange(fcoo_comm_t c, const void* sendbuf, const int64_t* send_counts, void* recvbuf,
+                          const int64_t* recv_counts, size_t elem, cudaStream_t s) {
+  if (!c || !c->comm) return fail(FCOO_ERR_ARG, "exchange needs a comm");
+  const char* sb = static_cast<const char*>(sendbuf);
+  char* rb = static_cast<char*>(recvbuf);
+  size_t so = 0, ro = 0;
+  ncclResult_t r = ncclGroupStart();
+  for (int j = 0; j < c->nranks && r == ncclSuccess; ++j) {
+    const size_t ns = (size_t)send_counts[j] * elem, nr = (size_t)recv_counts[j] * elem;
+    if (ns) r = ncclSend(sb + so, ns, ncclUint8, j, c->comm, s);
+    if (r == ncclSuccess && nr) r = ncclRecv(rb + ro, nr, ncclUint8, j, c->comm, s);
+    so += ns;
+    ro += nr;
+  }
+  const ncclResult_t r2 = ncclGroupEnd();
+  return nccl_status(c, r != ncclSuccess ? r : r2, "exchange (ncclSend/ncclRecv group)");
+}
+
 void comm_rank_size(fcoo_comm_t c, int* rank, int* nranks) {
   *rank = c ? c->rank : 0;
   *nranks = c ? c->nranks : 1;

@@ -210,9 +210,14 @@ fcoo_status ensure_dpart(fcoo_s* f, size_t bytes, cudaStream_t s) {
 
 fcoo_status run_mttkrp(fcoo_s* f, const float* const* factors, int R, float* out, cudaStream_t s, const int* gate,
                        int gate_on) {
-  fcoo_status st = mttkrp_t<float>(f, factors, R, out, s, gate, gate_on);
+  fcoo_status st = FCOO_OK;
+  if (f->nnz == 0)  // a row shard that received no nonzeros (distributed build)
+    FCOO_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)f->dims[f->mode] * R, s));
+  else
+    st = mttkrp_t<float>(f, factors, R, out, s, gate, gate_on);
   if (st) return st;
   if (f->comm) return comm_allreduce(f->comm, out, (size_t)f->dims[f->mode] * R, s);
+  if (f->row_comm) return comm_gather_rows(f->row_comm, out, f->row_bounds, R, s);
   return FCOO_OK;
 }
 
@@ -223,6 +228,7 @@ fcoo_status run_mttkrp_mc(fcoo_s* f, const float* const* factors, int R, fcoo_mc
   size_t bytes = 0;
   fcoo_comm_t comm = nullptr;
   mc_views(mc, &uc, &mcp, &bytes, &comm);
+  if (f->row_sharded || f->nnz == 0) return fail(FCOO_ERR_ARG, "fused combine: row-sharded handle (use fcoo_mttkrp)");
   const size_t need = sizeof(float) * (size_t)f->dims[f->mode] * (size_t)R;
   if (bytes < need) return fail(FCOO_ERR_ARG, "multicast buffer holds %zu bytes, output needs %zu", bytes, need);
   if (f->comm && f->comm != comm) return fail(FCOO_ERR_ARG, "handle sharded over a different comm");
@@ -245,6 +251,10 @@ fcoo_status run_mttkrp_mc(fcoo_s* f, const float* const* factors, int R, fcoo_mc
 // fp64-accumulating MTTKRP (CP-ALS fit mode); sharded handles return the LOCAL partial.
 fcoo_status run_mttkrp_f64(fcoo_s* f, const float* const* factors, int R, double* out, cudaStream_t s,
                            const int* gate, int gate_on) {
+  if (f->nnz == 0) {
+    FCOO_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * (size_t)f->dims[f->mode] * R, s));
+    return FCOO_OK;
+  }
   return mttkrp_t<double>(f, factors, R, out, s, gate, gate_on);
 }
 

@@ -91,6 +91,12 @@ struct fcoo_s {
   int shard = 0, nshards = 1;
   int64_t tile_begin = 0, tile_end = 0;
   fcoo_comm_t comm = nullptr;
+  // row shard (fcoo_set_row_shard / fcoo_build_distributed, SURVEY §8(e) owned-rows combine): the
+  // handle holds only the nonzeros of index-mode rows [row_bounds[row_rank], row_bounds[row_rank+1]),
+  // so its MTTKRP rows there are complete and the ranks' owned row ranges are all-gathered
+  int row_sharded = 0, row_rank = 0, row_nranks = 1;
+  std::vector<int64_t> row_bounds;
+  fcoo_comm_t row_comm = nullptr;
   fcoo::Alloc alloc;
   cudaStream_t build_stream = nullptr;
   int device = 0;
@@ -111,6 +117,19 @@ fcoo_status comm_barrier(fcoo_comm_t comm, cudaStream_t s);
 void mc_views(fcoo_mc_t m, float** uc, float** mc, size_t* bytes, fcoo_comm_t* comm);
 fcoo_status run_mttkrp_mc(fcoo_s* f, const float* const* factors, int R, fcoo_mc_t out, cudaStream_t s);
 fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s);
+// owned-rows combine of a row-sharded handle: rank k broadcasts rows [bounds[k], bounds[k+1]) of
+// `out` (R columns) in one NCCL group, so every rank ends with the full output (fcoo_comm.cu)
+fcoo_status comm_gather_rows(fcoo_comm_t comm, float* out, const std::vector<int64_t>& bounds, int R, cudaStream_t s);
+// distributed build helpers (fcoo_comm.cu): in-place sum of u32 counts; all-gather of nranks u64
+// per rank; grouped send/recv of `elem` bytes per item (send[j]/recv[j] items to/from rank j)
+fcoo_status comm_allreduce_u32(fcoo_comm_t comm, uint32_t* buf, size_t count, cudaStream_t s);
+fcoo_status comm_allgather_u64(fcoo_comm_t comm, const uint64_t* send, uint64_t* recv, size_t count, cudaStream_t s);
+fcoo_status comm_exchange(fcoo_comm_t comm, const void* sendbuf, const int64_t* send_counts, void* recvbuf,
+                          const int64_t* recv_counts, size_t elem, cudaStream_t s);
+// a handle for (op, mode) of a tensor with no nonzeros on this rank (distributed build); its
+// SpMTTKRP output is all zero (fcoo_build.cu)
+fcoo_status build_empty(int order, const int64_t* dims, int op, int mode, const fcoo_allocator* alloc, cudaStream_t s,
+                        fcoo_t* out);
 // SpTTM through the specialised kernel (fcoo_ttm.cu) when it applies; false = use the engine
 bool run_ttm_lean(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s, fcoo_status* st);
 // deterministic handles: make f->dpart hold at least `bytes` (stream-ordered on s)

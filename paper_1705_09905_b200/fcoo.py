@@ -58,7 +58,9 @@ class _Info(ctypes.Structure):
                 ("device_bytes", ctypes.c_int64), ("shard", ctypes.c_int), ("nshards", ctypes.c_int),
                 ("tile_begin", ctypes.c_int64), ("tile_end", ctypes.c_int64), ("blocked", ctypes.c_int),
                 ("block_rows", ctypes.c_int), ("nblocks", ctypes.c_int64), ("nstream", ctypes.c_int64),
-                ("pk_shift", ctypes.c_int), ("n_words", ctypes.c_int), ("nfib", ctypes.c_int64)]
+                ("pk_shift", ctypes.c_int), ("n_words", ctypes.c_int), ("nfib", ctypes.c_int64),
+                ("row_sharded", ctypes.c_int), ("row_rank", ctypes.c_int), ("row_nranks", ctypes.c_int),
+                ("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64)]
 
 
 class _HostView(ctypes.Structure):
@@ -79,7 +81,8 @@ SYMBOLS = ["fcoo_build", "fcoo_build_sharded", "fcoo_mttkrp", "fcoo_ttm", "fcoo_
            "fcoo_comm_unique_id", "fcoo_comm_init", "fcoo_comm_destroy", "fcoo_allreduce_sum", "fcoo_set_shard",
            "fcoo_mc_alloc", "fcoo_mc_ptr", "fcoo_mc_free", "fcoo_mttkrp_mc",
            "fcoo_shard_range", "cp_als", "fcoo_tns_read", "fcoo_tns_info", "fcoo_tns_copy", "fcoo_tns_destroy",
-           "fcoo_tns_write", "fcoo_debug_flip_bit", "fcoo_status_str", "fcoo_last_error", "fcoo_launch_count"]
+           "fcoo_tns_write", "fcoo_debug_flip_bit", "fcoo_slice_histogram", "fcoo_row_partition", "fcoo_bucket_rows",
+           "fcoo_set_row_shard", "fcoo_build_distributed", "fcoo_status_str", "fcoo_last_error", "fcoo_launch_count"]
 
 _lib = None
 
@@ -121,6 +124,13 @@ def load_library():
     L.fcoo_tns_copy.argtypes = [vp, ctypes.POINTER(vp), vp]
     L.fcoo_tns_destroy.argtypes = [vp]
     L.fcoo_tns_write.argtypes = [ctypes.c_char_p, ci, i64, ctypes.POINTER(vp), vp]
+    L.fcoo_slice_histogram.argtypes = [ctypes.POINTER(_Coo), ci, vp, vp]
+    L.fcoo_row_partition.argtypes = [vp, i64, ci, vp]
+    L.fcoo_bucket_rows.argtypes = [ctypes.POINTER(_Coo), ci, vp, ci, ctypes.POINTER(vp), vp, vp,
+                                   ctypes.POINTER(_Allocator), vp]
+    L.fcoo_set_row_shard.argtypes = [vp, ci, ci, vp, vp]
+    L.fcoo_build_distributed.argtypes = [ctypes.POINTER(_Coo), ci, ctypes.POINTER(_BuildOpts), vp,
+                                         ctypes.POINTER(_Allocator), vp, ctypes.POINTER(vp)]
     L.fcoo_status_str.restype = ctypes.c_char_p
     L.fcoo_status_str.argtypes = [ci]
     L.fcoo_last_error.restype = ctypes.c_char_p
@@ -269,6 +279,11 @@ class Info:
     pk_shift: int = 0
     n_words: int = 0
     nfib: int = 0  # SpTTM: output rows (fibres)
+    row_sharded: bool = False
+    row_rank: int = 0
+    row_nranks: int = 1
+    row_begin: int = 0
+    row_end: int = 0
 
 
 class Fcoo:
@@ -287,7 +302,8 @@ class Fcoo:
                     list(inf.prod_modes[: inf.n_prod]), list(inf.dims[:o]), inf.nnz, inf.nsegs, inf.ntiles,
                     inf.tile_nnz, bool(inf.dense_rows), inf.storage_bytes, inf.seg_table_bytes, inf.device_bytes,
                     inf.shard, inf.nshards, inf.tile_begin, inf.tile_end, bool(inf.blocked), inf.block_rows,
-                    inf.nblocks, inf.nstream, inf.pk_shift, inf.n_words, inf.nfib)
+                    inf.nblocks, inf.nstream, inf.pk_shift, inf.n_words, inf.nfib, bool(inf.row_sharded),
+                    inf.row_rank, inf.row_nranks, inf.row_begin, inf.row_end)
 
     def destroy(self):
         if self.h:
@@ -328,6 +344,64 @@ def fcoo_build_sharded(coo: Coo, mode: int, comm: "Comm", op: int = OP_MTTKRP, t
     _check(L.fcoo_build_sharded(ctypes.byref(coo.c), mode, ctypes.byref(opts), comm.h, ctypes.byref(_ALLOCATOR),
                                 ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out)), "fcoo_build_sharded")
     return Fcoo(out.value, coo)
+
+
+def fcoo_slice_histogram(coo: Coo, mode: int, stream=None) -> torch.Tensor:
+    """Nonzeros per index-mode row (device int32 tensor holding the u32 counts)."""
+    hist = torch.empty(coo.dims[mode], dtype=torch.int32, device=coo.val.device)
+    _check(load_library().fcoo_slice_histogram(ctypes.byref(coo.c), mode, ctypes.c_void_p(hist.data_ptr()),
+                                               ctypes.c_void_p(_stream_ptr(stream))), "fcoo_slice_histogram")
+    return hist
+
+
+def fcoo_row_partition(hist, nranks: int):
+    """Row bounds (numpy int64[nranks + 1]) balancing the nonzeros of a host slice histogram over
+    nranks contiguous row ranges (host arithmetic in the library, no device)."""
+    import numpy as np
+    h = np.ascontiguousarray(hist, dtype=np.uint32)
+    bounds = np.zeros(nranks + 1, np.int64)
+    _check(load_library().fcoo_row_partition(h.ctypes.data, int(h.shape[0]), int(nranks), bounds.ctypes.data),
+           "fcoo_row_partition")
+    return bounds
+
+
+def fcoo_bucket_rows(coo: Coo, mode: int, bounds, stream=None):
+    """Nonzeros of coo grouped by destination rank of `bounds` -> (Coo of the grouped nonzeros,
+    numpy int64 counts per rank)."""
+    import numpy as np
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    nranks = int(b.shape[0]) - 1
+    idx = torch.empty_like(coo.idx)
+    val = torch.empty_like(coo.val)
+    ptrs = (ctypes.c_void_p * coo.order)(*[idx[m].data_ptr() for m in range(coo.order)])
+    counts = np.zeros(nranks, np.int64)
+    _check(load_library().fcoo_bucket_rows(ctypes.byref(coo.c), mode, b.ctypes.data, nranks, ptrs,
+                                           ctypes.c_void_p(val.data_ptr()), counts.ctypes.data,
+                                           ctypes.byref(_ALLOCATOR), ctypes.c_void_p(_stream_ptr(stream))),
+           "fcoo_bucket_rows")
+    return Coo(coo.dims, idx, val), counts
+
+
+def fcoo_set_row_shard(f: "Fcoo", rank: int, bounds, comm: "Comm" = None):
+    """Declare f as holding exactly rows [bounds[rank], bounds[rank+1]) of its mode (owned-rows
+    combine over comm in fcoo_mttkrp; comm None: no combine)."""
+    import numpy as np
+    b = np.ascontiguousarray(bounds, dtype=np.int64)
+    _check(load_library().fcoo_set_row_shard(f.h, int(rank), int(b.shape[0]) - 1, b.ctypes.data,
+                                             comm.h if comm is not None else None), "fcoo_set_row_shard")
+    f.info = f._info()
+
+
+def fcoo_build_distributed(local: Coo, mode: int, comm: "Comm", tile_nnz: int = 0, keep_perm: bool = False,
+                           blocked: bool = False, block_rows: int = 0, stream=None) -> "Fcoo":
+    """Collective: every rank passes its own chunk of the tensor and receives the F-COO of its
+    nnz-balanced range of mode rows (histogram, all-reduce, partition, bucket, NCCL exchange, build)."""
+    L = load_library()
+    opts = _BuildOpts(OP_MTTKRP, tile_nnz, _flags(keep_perm, False, False, blocked), block_rows)
+    out = ctypes.c_void_p()
+    _check(L.fcoo_build_distributed(ctypes.byref(local.c), mode, ctypes.byref(opts), comm.h, ctypes.byref(_ALLOCATOR),
+                                    ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out)), "fcoo_build_distributed")
+    return Fcoo(out.value, local)
 
 
 def _factor_ptrs(f: "Fcoo", factors, R: int, skip_mode: int):

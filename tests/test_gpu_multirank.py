@@ -4,6 +4,8 @@ rank checked against the fp64 oracle:
   - fcoo_build_sharded + fcoo_mttkrp on every mode, plain and blocked layouts: each rank processes
     its tile-aligned nnz shard, the partial outputs are summed by the library's NCCL all-reduce
     (comm_allreduce) and every rank holds the full result;
+  - fcoo_build_distributed from per-rank chunks + fcoo_mttkrp with the owned-rows all-gather
+    (row-partitioned handles, plain and blocked): every rank holds the full result;
   - cp_als with the comm (sharded MTTKRP, fp64 all-reduce of the last mode, replicated R x R work):
     the fit trace matches the oracle and the factors are identical on every rank.
 Skips on a box with fewer than two GPUs (this round's boxes have one; the test lights up on an
@@ -49,6 +51,22 @@ def _worker(rank, world, port, q):
                 torch.cuda.synchronize()
                 M, D = oracle.mttkrp(dims, idx, val, mode, fs)
                 assert_parity(out.cpu().numpy(), M, D, what=f"rank {rank} blocked={blocked} mode {mode}")
+                h.destroy()
+        # distributed build (each rank passes its own draw-order chunk) + owned-rows all-gather
+        nnz = val.shape[0]
+        lo, hi = nnz * rank // world, nnz * (rank + 1) // world
+        chunk = F.Coo.from_numpy(dims, idx[:, lo:hi].copy(), val[lo:hi].copy())
+        for blocked in (False, True):
+            for mode in range(3):
+                h = F.fcoo_build_distributed(chunk, mode, comm, tile_nnz=64, blocked=blocked)
+                assert h.info.row_sharded and h.info.row_rank == rank and h.info.row_nranks == world
+                sel = (idx[mode] >= h.info.row_begin) & (idx[mode] < h.info.row_end)
+                assert h.info.nnz == int(sel.sum())
+                out = torch.full((dims[mode], R), float("nan"), device="cuda")
+                F.fcoo_mttkrp(h, ft, R, out)
+                torch.cuda.synchronize()
+                M, D = oracle.mttkrp(dims, idx, val, mode, fs)
+                assert_parity(out.cpu().numpy(), M, D, what=f"rank {rank} distributed blocked={blocked} mode {mode}")
                 h.destroy()
         # sharded CP-ALS: fit trace vs the oracle, factors replicated bit for bit
         R2 = 8
