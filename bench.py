@@ -255,16 +255,16 @@ def main():
     P.fcoo_build(coo, 0, tile_nnz=T, **bkw).destroy()  # warm-up: module load, allocator, CUB tuning
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    rows = world > 1 and a.combine == "rows" and not a.fused_combine
+    row_part = world > 1 and a.combine == "rows" and not a.fused_combine
     # this rank's chunk of the input (draw order): the distributed build starts from it
     lo_q, hi_q = nnz * rank // world, nnz * (rank + 1) // world
-    chunk = P.Coo(dims, coo.idx[:, lo_q:hi_q].contiguous(), coo.val[lo_q:hi_q].contiguous()) if rows else None
+    chunk = P.Coo(dims, coo.idx[:, lo_q:hi_q].contiguous(), coo.val[lo_q:hi_q].contiguous()) if row_part else None
 
     def build_all(c, ch, s=None):
         # N > 1, rows: fcoo_build_distributed = histogram, all-reduce, nnz-balanced row ranges, bucket
         # exchange, build of this rank's rows (SURVEY §8(e) owned-rows alternative, §8(f)-4);
         # allreduce: fcoo_build_sharded = the redundant build + this rank's tile-aligned slice (§8(e) v1)
-        if rows:
+        if row_part:
             return [P.fcoo_build_distributed(ch, n, comm, tile_nnz=T, stream=s, **bkw) for n in range(N)]
         if world > 1:
             return [P.fcoo_build_sharded(c, n, comm, tile_nnz=T, stream=s, **bkw) for n in range(N)]
@@ -398,7 +398,7 @@ def main():
                    "R": R, "modes": list(range(N)), "tile_nnz": T, "layout": a.layout,
                    "block_rows": H[0].info.block_rows if blocked else None,
                    "parallelism": (f"row-partitioned x{world} (distributed build, nnz-balanced index-mode row "
-                                   "ranges per mode), factors replicated, owned-rows all-gather per mode" if rows else
+                                   "ranges per mode), factors replicated, owned-rows all-gather per mode" if row_part else
                                    f"nnz-sharded x{world}, factors replicated, "
                                    + ("combine fused into the MTTKRP epilogue (NVLS multicast)" if mc is not None
                                       else "NCCL all-reduce per mode")) if world > 1
@@ -506,7 +506,7 @@ def main():
     # ---- e2e_with_build: host COO (pinned) -> device, build every mode, MTTKRP every mode -> host ----
     if not a.no_e2e:
         # rows: each rank uploads only its own chunk of the COO (the distributed build exchanges the rest)
-        qs = slice(lo_q, hi_q) if rows else slice(0, nnz)
+        qs = slice(lo_q, hi_q) if row_part else slice(0, nnz)
         idx_h = torch.from_numpy(np.ascontiguousarray(idx_np[:, qs]).view(np.int32)).pin_memory()
         val_h = torch.from_numpy(np.ascontiguousarray(val_np[qs])).pin_memory()
         h2d = idx_h.numel() * 4 + val_h.numel() * 4 + sum(f.numel() * 4 for f in f_h)
@@ -517,7 +517,7 @@ def main():
             val_d = val_h.to(dev, non_blocking=True)
             fd = [f.to(dev, non_blocking=True) for f in f_h]
             c = P.Coo(dims, idx_d, val_d)
-            hs = build_all(None if rows else c, c if rows else None, stream)
+            hs = build_all(None if row_part else c, c if row_part else None, stream)
             for n in range(N):
                 P.fcoo_mttkrp(hs[n], fd, R, outs[n], stream)
                 o_h[n].copy_(outs[n], non_blocking=True)

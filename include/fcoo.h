@@ -78,8 +78,8 @@ typedef struct {
  * red.global.add, a tile writes the partial sums of the (at most two) segments it shares with its
  * neighbours to a per-call scratch array (2 x R per tile, through the handle's allocator), and a
  * second kernel adds the partials of each tile-crossing segment in tile order and stores the row.
- * Same sum, a fixed association: repeated calls give identical bits.  SpTTMc and the CP-ALS
- * fit-mode fp64 pass keep red.add. */
+ * Same sum, a fixed association: repeated calls give identical bits (also the CP-ALS fit-mode
+ * fp64 pass on such handles).  SpTTMc keeps red.add. */
 #define FCOO_BUILD_DETERMINISTIC 4u
 /* Blocked F-COO (reading Q22): the stream is the concatenation,
  * over b = 0, 1, ..., of the F-COO of the sub-tensor X_b = {nonzeros with floor(i_outer / BR) == b},

@@ -90,9 +90,12 @@ inline BlockedShape blocked_shape(int NP, int R, int BR, bool vec_ok) {
   sh.ncp = 0;
   sh.TB = 256;
   if (vec_ok) {
-    // copies of a narrow-row block only where they keep the CTAs per SM (3 for one product mode,
-    // else 2): measured on brainq SpTTM, occupancy outweighs the bank conflicts they remove
-    const int C = blocked_copies(R), want = NP == 1 ? 3 : 2;
+    // copies of a narrow-row block only for one product mode (SpTTM, where each row read is the
+    // only gather: 55.4 -> 52.7 us on brainq mode 1 at equal occupancy) and only where they keep
+    // the CTAs per SM (occupancy outweighs the conflicts); SpMTTKRP at R = 16 measured 13% SLOWER
+    // with copies (0.58 -> 0.67 ms, 2 CTAs/SM either way: the L1 left beside 2 x 108 KB of shared
+    // memory), so its block stays single
+    const int C = NP == 1 ? blocked_copies(R) : 1, want = NP == 1 ? 3 : 2;
     const size_t st256 = blocked_stage_bytes(NW, sh.G, 256, NST);
     auto ctas = [&](size_t bytes) { return std::min<int>(want, (int)((228 * 1024) / (bytes + st256 + 1024))); };
     if (C > 1 && ctas(blocked_block_bytes(BR, R, C)) >= ctas(sh.block_bytes) &&

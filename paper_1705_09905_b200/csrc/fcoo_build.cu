@@ -635,6 +635,7 @@ fcoo_status fibre_table(fcoo_s* f, const KeyLayout& L, cudaStream_t s) {
 
 fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opts, const fcoo_allocator* alloc,
                        cudaStream_t s, fcoo_t* out) {
+  Nvtx range("fcoo_build");
   if (!coo || !out) return fail(FCOO_ERR_ARG, "NULL coo/out");
   *out = nullptr;
   int op = opts ? opts->op : FCOO_OP_MTTKRP;

@@ -42,11 +42,13 @@ static fcoo_status nccl_status(fcoo_comm_t c, ncclResult_t r, const char* what) 
 }
 
 fcoo_status comm_allreduce(fcoo_comm_t c, float* buf, size_t count, cudaStream_t s) {
+  Nvtx range("ncclAllReduce");
   if (!c || !c->comm) return FCOO_OK;
   return nccl_status(c, ncclAllReduce(buf, buf, count, ncclFloat, ncclSum, c->comm, s), "ncclAllReduce");
 }
 
 fcoo_status comm_allreduce_f64(fcoo_comm_t c, double* buf, size_t count, cudaStream_t s) {
+  Nvtx range("ncclAllReduce(f64)");
   if (!c || !c->comm) return FCOO_OK;
   return nccl_status(c, ncclAllReduce(buf, buf, count, ncclDouble, ncclSum, c->comm, s), "ncclAllReduce(f64)");
 }
@@ -63,6 +65,7 @@ fcoo_status comm_barrier(fcoo_comm_t c, cudaStream_t s) {
 // broadcasts its complete rows [bounds[k], bounds[k+1]) in place; the nranks broadcasts form one
 // NCCL group (one launch).  Every rank calls it with the same bounds.
 fcoo_status comm_gather_rows(fcoo_comm_t c, float* out, const std::vector<int64_t>& bounds, int R, cudaStream_t s) {
+  Nvtx range("owned-rows gather");
   if (!c || !c->comm || c->nranks == 1) return FCOO_OK;
   if ((int)bounds.size() != c->nranks + 1) return fail(FCOO_ERR_ARG, "row bounds for %d ranks, comm has %d",
                                                        (int)bounds.size() - 1, c->nranks);

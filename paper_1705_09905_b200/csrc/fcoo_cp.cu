@@ -646,6 +646,7 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
   }
   // One CP-ALS iteration (Alg. 1 body), enqueued on s with no host synchronisation.
   auto iteration = [&]() -> fcoo_status {
+    fcoo::Nvtx range("cp_als iteration");
     fcoo_status st = FCOO_OK;
     for (int n = 0; n < N; ++n) {
       const int64_t In = X->dims[n];
@@ -730,15 +731,14 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
 
   // Iteration 0 runs eagerly; iteration 1 is captured into a CUDA graph and every later iteration
   // replays it (the ~45 small launches of an iteration become one graph launch).  Any capture or
-  // instantiation failure falls back to eager launches.  FCOO_CP_NO_GRAPH=1 disables the graph.
-  static const bool no_graph = getenv("FCOO_CP_NO_GRAPH") != nullptr;
+  // instantiation failure falls back to eager launches.
   cudaGraphExec_t exec = nullptr;
   uint64_t graph_kernels = 0;
   struct ExecGuard { cudaGraphExec_t& e; ~ExecGuard() { if (e) cudaGraphExecDestroy(e); } } exec_guard{exec};
   double fit_prev = 0.0;
   int it = 0;
   for (; it < o->iters && !st; ++it) {
-    if (it == 1 && !no_graph && o->iters > 2 &&
+    if (it == 1 && o->iters > 2 &&
         cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal) == cudaSuccess) {
       const uint64_t before = fcoo::g_launches.load();
       fcoo_status cst = iteration();

@@ -249,6 +249,7 @@ fcoo_status fcoo_set_row_shard(fcoo_t f, int rank, int nranks, const int64_t* bo
 fcoo_status fcoo_build_distributed(const fcoo_coo* local, int mode, const fcoo_build_opts* opts, fcoo_comm_t comm,
                                    const fcoo_allocator* alloc, void* stream, fcoo_t* out) {
   using namespace fcoo;
+  Nvtx range("fcoo_build_distributed");
   if (!comm || !out) return fail(FCOO_ERR_ARG, "NULL comm/out");
   *out = nullptr;
   fcoo_status st = check_coo_arrays(local, mode);

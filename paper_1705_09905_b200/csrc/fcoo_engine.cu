@@ -210,6 +210,7 @@ fcoo_status ensure_dpart(fcoo_s* f, size_t bytes, cudaStream_t s) {
 
 fcoo_status run_mttkrp(fcoo_s* f, const float* const* factors, int R, float* out, cudaStream_t s, const int* gate,
                        int gate_on) {
+  Nvtx range("fcoo_mttkrp");
   fcoo_status st = FCOO_OK;
   if (f->nnz == 0)  // a row shard that received no nonzeros (distributed build)
     FCOO_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)f->dims[f->mode] * R, s));
@@ -251,6 +252,7 @@ fcoo_status run_mttkrp_mc(fcoo_s* f, const float* const* factors, int R, fcoo_mc
 // fp64-accumulating MTTKRP (CP-ALS fit mode); sharded handles return the LOCAL partial.
 fcoo_status run_mttkrp_f64(fcoo_s* f, const float* const* factors, int R, double* out, cudaStream_t s,
                            const int* gate, int gate_on) {
+  Nvtx range("fcoo_mttkrp_f64");
   if (f->nnz == 0) {
     FCOO_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(double) * (size_t)f->dims[f->mode] * R, s));
     return FCOO_OK;
@@ -288,6 +290,7 @@ fcoo_status ttm_blocked(fcoo_s* f, const float* U, int R, float* out, cudaStream
 }
 
 fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s) {
+  Nvtx range("fcoo_ttm");
   if (f->blocked) return ttm_blocked(f, U, R, out, s);
   EngineParams P{};
   bool vec_ok = (R % 4 == 0) && R <= 128 && aligned16(out) && aligned16(U);

@@ -8,6 +8,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>  // header-only NVTX v3: no-ops unless a profiler is attached
+
 #include "fcoo.h"
 
 namespace fcoo {
@@ -27,6 +29,15 @@ struct Alloc {
   bool custom = false;
   void* get(size_t bytes, cudaStream_t s) const;
   void put(void* p, size_t bytes, cudaStream_t s) const;
+};
+
+// NVTX phase range (SURVEY §5 tracing: build / kernel / collective / solve phases show up by name
+// on an nsys or ncu --nvtx timeline); host-side, around the enqueue of the phase's work.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
 };
 
 struct Buf {  // RAII temp buffer

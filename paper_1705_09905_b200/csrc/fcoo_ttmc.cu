@@ -607,8 +607,7 @@ bool try_mma(const TtmcParams& P, cudaStream_t s, cudaError_t* err) {
 
 // Register tiles per lane, tried in order (balanced tiles first: fewest shared-memory loads).
 cudaError_t launch_staged(const TtmcParams& P, bool* done, cudaStream_t s) {
-  static const bool use_mma = !getenv("FCOO_TTMC_NO_MMA");
-  if (use_mma) {
+  {
     cudaError_t e = cudaSuccess;
     if (try_mma<32, 32>(P, s, &e) || try_mma<16, 16>(P, s, &e) || try_mma<16, 32>(P, s, &e) ||
         try_mma<32, 16>(P, s, &e) || try_mma<16, 64>(P, s, &e) || try_mma<64, 16>(P, s, &e) ||
@@ -637,8 +636,7 @@ cudaError_t launch_ttmc_ns(const TtmcParams& P, cudaStream_t s) {
   int64_t threads = (P.tile_end - P.tile_begin) * 32;
   unsigned blocks = (unsigned)((threads + TB - 1) / TB);
   if (blocks == 0) return cudaSuccess;
-  static const bool staged_env = !getenv("FCOO_TTMC_UNSTAGED");
-  if (staged_env) {
+  {
     bool done = false;
     cudaError_t e = launch_staged(P, &done, s);
     if (done || e != cudaSuccess) return e;
@@ -656,6 +654,7 @@ cudaError_t launch_ttmc_ns(const TtmcParams& P, cudaStream_t s) {
 }  // namespace
 
 fcoo_status run_ttmc(fcoo_s* f, const float* const* factors, const int* ranks, float* out, cudaStream_t s) {
+  Nvtx range("fcoo_ttmc");
   if (f->n_prod != 2) return fail(FCOO_ERR_ORDER, "fcoo_ttmc supports order-3 tensors (Eq.(4)); order is %d", f->order);
   // Kronecker order = ascending mode id (Eq.(4)); the handle stores product modes by extent (Q5)
   int a = 0, b = 1;
