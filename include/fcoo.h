@@ -93,9 +93,10 @@ typedef struct {
  * plus, for order >= 4, the global index of each middle product mode: 8 B/nnz + flags for a
  * 3-order tensor instead of Table II's 12.  FCOO_OP_TTM: the one product mode n is blocked (the
  * word is i_n - b*BR); segments are (block, fibre) pairs, mapped to the fibre table (output rows)
- * by a sort of the segments' tuples: a third host synchronisation (fibre count).  Requires 2 <= order <= 5 and ceil(log2 BR) + IB <= 32
- * (else FCOO_ERR_ARG); incompatible with DETERMINISTIC and PRODUCT_DESC (ARG); fcoo_ttmc rejects
- * blocked handles (SHAPE).  The build synchronises the host twice (block sizes, then errors). */
+ * by a sort of the segments' tuples.  Requires 2 <= order <= 5 and ceil(log2 BR) + IB <= 32 (else
+ * FCOO_ERR_ARG); incompatible with DETERMINISTIC and PRODUCT_DESC (ARG); fcoo_ttmc rejects blocked
+ * handles (SHAPE).  The build synchronises the host twice (block sizes, then errors), a TTM build
+ * three times (then the fibre count). */
 #define FCOO_BUILD_BLOCKED 8u
 
 /* Build options.  NULL -> {FCOO_OP_MTTKRP, 0 (automatic), 0}.
