@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--combine", default="rows", choices=["rows", "allreduce"],
                     help="N > 1: rows = distributed build (each rank holds the nnz-balanced rows of its chunk "
                          "exchange, owned-rows all-gather); allreduce = redundant build, tile shards, sum all-reduce")
+    ap.add_argument("--dist-1rank", action="store_true",
+                    help="debug: run the N > 1 row-partitioned code path on one GPU with a 1-rank NCCL comm")
     ap.add_argument("--fused-combine", action="store_true",
                     help="N > 1: combine the ranks' partial outputs in the MTTKRP epilogue through an NVLS "
                          "multicast buffer (fcoo_mttkrp_mc) instead of a separate NCCL all-reduce")
@@ -250,12 +252,14 @@ def main():
     torch.cuda.synchronize()
 
     comm = P.comm_from_process_group() if world > 1 else None
+    if a.dist_1rank and world == 1:
+        comm = P.fcoo_comm_init(0, 1, P.fcoo_comm_unique_id())
     blocked = a.layout == "blocked"
     bkw = dict(blocked=blocked, block_rows=a.block_rows) if blocked else {}
     P.fcoo_build(coo, 0, tile_nnz=T, **bkw).destroy()  # warm-up: module load, allocator, CUB tuning
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    row_part = world > 1 and a.combine == "rows" and not a.fused_combine
+    row_part = (world > 1 or a.dist_1rank) and a.combine == "rows" and not a.fused_combine
     # this rank's chunk of the input (draw order): the distributed build starts from it
     lo_q, hi_q = nnz * rank // world, nnz * (rank + 1) // world
     chunk = P.Coo(dims, coo.idx[:, lo_q:hi_q].contiguous(), coo.val[lo_q:hi_q].contiguous()) if row_part else None
@@ -392,7 +396,7 @@ def main():
     result = {
         "metric": METRIC, "value": value, "unit": "GFLOP/s", "n_gpus": world, "steps": a.steps,
         "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
-        "scaling": "strong" if world > 1 else "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"{w.name}-shaped {'x'.join(map(str, dims))}, {nnz} nnz, Zipf alpha {list(w.alpha)}, "
                                f"seed {w.seed}",
                    "R": R, "modes": list(range(N)), "tile_nnz": T, "layout": a.layout,

@@ -340,7 +340,7 @@ fcoo_status fcoo_set_row_shard(fcoo_t f, int rank, int nranks, const int64_t* bo
  * and receives the F-COO handle (FCOO_OP_MTTKRP only) of its rows of `mode`:
  *   fcoo_slice_histogram -> NCCL all-reduce -> fcoo_row_partition -> fcoo_bucket_rows ->
  *   NCCL all-gather of the per-destination counts -> grouped ncclSend/ncclRecv of the buckets
- *   (self included) -> fcoo_build (opts: tile, flags, block rows as usual) -> fcoo_set_row_shard.
+ *   (own bucket: device copy) -> fcoo_build (opts: tile, flags, block rows as usual) -> fcoo_set_row_shard.
  * A rank whose range received no nonzeros gets an empty handle (its rows read 0).  Synchronises the
  * host several times (setup path).  Errors: as fcoo_build, plus SHAPE (opts->op != MTTKRP), NCCL. */
 fcoo_status fcoo_build_distributed(const fcoo_coo* local, int mode, const fcoo_build_opts* opts, fcoo_comm_t comm,

@@ -92,22 +92,28 @@ fcoo_status comm_allgather_u64(fcoo_comm_t c, const uint64_t* send, uint64_t* re
 
 // Grouped point-to-point exchange (the all-to-all of the distributed build): items of `elem`
 // bytes, send_counts[j] of them to rank j from consecutive ranges of sendbuf, recv_counts[j] from
-// rank j into consecutive ranges of recvbuf (self included).  Counts must agree pairwise.
+// rank j into consecutive ranges of recvbuf (the own bucket by a device copy).  Counts must agree pairwise.
 fcoo_status comm_exchange(fcoo_comm_t c, const void* sendbuf, const int64_t* send_counts, void* recvbuf,
                           const int64_t* recv_counts, size_t elem, cudaStream_t s) {
   if (!c || !c->comm) return fail(FCOO_ERR_ARG, "exchange needs a comm");
   const char* sb = static_cast<const char*>(sendbuf);
   char* rb = static_cast<char*>(recvbuf);
-  size_t so = 0, ro = 0;
+  size_t so = 0, ro = 0, self_so = 0, self_ro = 0, self_n = 0;
   ncclResult_t r = ncclGroupStart();
   for (int j = 0; j < c->nranks && r == ncclSuccess; ++j) {
     const size_t ns = (size_t)send_counts[j] * elem, nr = (size_t)recv_counts[j] * elem;
-    if (ns) r = ncclSend(sb + so, ns, ncclUint8, j, c->comm, s);
-    if (r == ncclSuccess && nr) r = ncclRecv(rb + ro, nr, ncclUint8, j, c->comm, s);
+    if (j == c->rank) {  // this rank's own bucket: a device copy, not a NCCL self send/recv
+      self_so = so, self_ro = ro, self_n = ns;
+    } else {
+      if (ns) r = ncclSend(sb + so, ns, ncclUint8, j, c->comm, s);
+      if (r == ncclSuccess && nr) r = ncclRecv(rb + ro, nr, ncclUint8, j, c->comm, s);
+    }
     so += ns;
     ro += nr;
   }
   const ncclResult_t r2 = ncclGroupEnd();
+  if (self_n && cudaMemcpyAsync(rb + self_ro, sb + self_so, self_n, cudaMemcpyDeviceToDevice, s) != cudaSuccess)
+    return fail(FCOO_ERR_CUDA, "exchange: own bucket copy");
   return nccl_status(c, r != ncclSuccess ? r : r2, "exchange (ncclSend/ncclRecv group)");
 }
 

@@ -37,8 +37,7 @@ __global__ void k_slice_hist(const uint32_t* __restrict__ idx, int64_t nnz, uint
 // destination rank of nonzero q: the k with bounds[k] <= i_n < bounds[k+1]; its input ordinal
 // rides along as the payload of the (stable) radix sort by destination
 __global__ void k_dest(const uint32_t* __restrict__ idx, int64_t nnz, const int64_t* __restrict__ bounds, int nranks,
-                       uint32_t* __restrict__ dest, uint32_t* __restrict__ ord, uint32_t* __restrict__ counts,
-                       uint32_t* __restrict__ err) {
+                       uint32_t* __restrict__ dest, uint32_t* __restrict__ ord, uint32_t* __restrict__ err) {
   const int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nnz) return;
   const int64_t i = idx[q];
@@ -50,7 +49,22 @@ __global__ void k_dest(const uint32_t* __restrict__ idx, int64_t nnz, const int6
   }
   dest[q] = (uint32_t)lo;
   ord[q] = (uint32_t)q;
-  atomicAdd(&counts[lo], 1u);
+}
+
+// counts[k] = number of sorted destination keys equal to k (binary searches, one thread per rank:
+// no contended atomics over the nnz threads)
+__global__ void k_dest_counts(const uint32_t* __restrict__ sorted, int64_t n, int nranks, uint32_t* __restrict__ counts) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= nranks) return;
+  auto lower = [&](uint32_t key) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (sorted[mid] < key) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  counts[k] = (uint32_t)(lower((uint32_t)k + 1u) - lower((uint32_t)k));
 }
 
 __global__ void k_gather_u32(const uint32_t* __restrict__ src, const uint32_t* __restrict__ ord, int64_t n,
@@ -127,8 +141,7 @@ fcoo_status bucket_rows(const fcoo_coo* coo, int mode, const int64_t* bounds, in
   FCOO_CUDA_TRY(cudaMemsetAsync(cnt.p, 0, sizeof(uint32_t) * (nranks + 1), s));
   uint32_t* err = cnt.as<uint32_t>() + nranks;
   const unsigned grid = (unsigned)((nnz + 255) / 256);
-  k_dest<<<grid, 256, 0, s>>>(coo->idx[mode], nnz, db.as<int64_t>(), nranks, d0.as<uint32_t>(), o0.as<uint32_t>(),
-                              cnt.as<uint32_t>(), err);
+  k_dest<<<grid, 256, 0, s>>>(coo->idx[mode], nnz, db.as<int64_t>(), nranks, d0.as<uint32_t>(), o0.as<uint32_t>(), err);
   FCOO_LAUNCH_CHECK();
   cub::DoubleBuffer<uint32_t> dk(d0.as<uint32_t>(), d1.as<uint32_t>()), dv(o0.as<uint32_t>(), o1.as<uint32_t>());
   const int bits = std::max(1, bits_for_n(nranks));
@@ -142,6 +155,8 @@ fcoo_status bucket_rows(const fcoo_coo* coo, int mode, const int64_t* bounds, in
     count_launch(2 + (bits + 7) / 8);
   }
   const uint32_t* ord = dv.Current();
+  k_dest_counts<<<(unsigned)((nranks + 127) / 128), 128, 0, s>>>(dk.Current(), nnz, nranks, cnt.as<uint32_t>());
+  FCOO_LAUNCH_CHECK();
   for (int m = 0; m < coo->order; ++m) {
     k_gather_u32<<<grid, 256, 0, s>>>(coo->idx[m], ord, nnz, idx_out[m]);
     FCOO_LAUNCH_CHECK();
@@ -160,10 +175,16 @@ fcoo_status bucket_rows(const fcoo_coo* coo, int mode, const int64_t* bounds, in
 __global__ void k_row_minmax(const uint32_t* __restrict__ seg_coord, int64_t nsegs, int n_idx,
                              uint32_t* __restrict__ mm) {
   const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nsegs) return;
-  const uint32_t r = seg_coord[s * n_idx];
-  atomicMin(&mm[0], r);
-  atomicMax(&mm[1], r);
+  uint32_t lo = 0xffffffffu, hi = 0u;
+  if (s < nsegs) lo = hi = seg_coord[s * n_idx];
+  for (int o = 16; o > 0; o >>= 1) {  // warp reduction, one atomic pair per warp
+    lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+    hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&mm[0], lo);
+    atomicMax(&mm[1], hi);
+  }
 }
 
 }  // namespace
@@ -309,7 +330,7 @@ fcoo_status fcoo_build_distributed(const fcoo_coo* local, int mode, const fcoo_b
   int64_t total = 0;
   for (int j = 0; j < nranks; ++j) total += recv[j];
   if (total >= 4294967295LL) { release(); return fail(FCOO_ERR_ARG, "rank %d would receive %lld >= 2^32 nonzeros", rank, (long long)total); }
-  // 4. the exchange: one grouped send/recv per array (self included)
+  // 4. the exchange: one grouped send/recv per array (the own bucket by a device copy)
   for (int m = 0; m < order; ++m) ridx[m] = buf(sizeof(uint32_t) * (size_t)total)->as<uint32_t>();
   float* rval = buf(sizeof(float) * (size_t)total)->as<float>();
   for (Buf* b : bufs) if (!b->ok()) { release(); return fail(FCOO_ERR_OOM, "receive buffers"); }

@@ -10,7 +10,7 @@ fcoo_bucket_rows, fcoo_set_row_shard, fcoo_build_distributed; SURVEY §8(e) owne
   output is 0 outside its rows and matches the oracle inside (normalised 1e-4), and the owned row
   ranges assembled give the full result — plain and blocked layouts, every mode, with an empty rank;
 - a 1-rank NCCL communicator runs fcoo_build_distributed end to end (histogram all-reduce, count
-  all-gather, self send/recv, build) and equals fcoo_build; an empty local chunk gives an empty handle
+  all-gather, own-bucket copy, build) and equals fcoo_build; an empty local chunk gives an empty handle
   whose output is all zero.  The N-rank run is in test_gpu_multirank.py (skips on one GPU).
 """
 import numpy as np
