@@ -369,6 +369,11 @@ typedef struct {
   int layout;        /* 0 = automatic: every mode's handle uses the blocked F-COO (FCOO_BUILD_BLOCKED)
                         when the build allows it (not deterministic, order <= 5, packed word fits),
                         else the plain F-COO; 1 = always the plain F-COO */
+  int dist;          /* != 0 (needs comm): `tensor` is THIS RANK'S CHUNK of the nonzeros (any split; same
+                        order and dims on every rank) and every mode's handle is built by
+                        fcoo_build_distributed: each rank's MTTKRP covers its nnz-balanced rows and the
+                        owned-rows all-gather replaces the all-reduce (the last mode in fp64, gathered
+                        in fp64); |X|^2 is summed over the ranks.  Excludes deterministic. */
 } fcoo_cp_opts;
 
 /*

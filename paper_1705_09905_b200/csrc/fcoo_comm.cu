@@ -64,7 +64,9 @@ fcoo_status comm_barrier(fcoo_comm_t c, cudaStream_t s) {
 // the bytes" of the all-reduce): on a row-sharded handle no row is partial on two ranks, so rank k
 // broadcasts its complete rows [bounds[k], bounds[k+1]) in place; the nranks broadcasts form one
 // NCCL group (one launch).  Every rank calls it with the same bounds.
-fcoo_status comm_gather_rows(fcoo_comm_t c, float* out, const std::vector<int64_t>& bounds, int R, cudaStream_t s) {
+template <class T>
+static fcoo_status gather_rows_t(fcoo_comm_t c, T* out, const std::vector<int64_t>& bounds, int R, ncclDataType_t ty,
+                                 cudaStream_t s) {
   Nvtx range("owned-rows gather");
   if (!c || !c->comm || c->nranks == 1) return FCOO_OK;
   if ((int)bounds.size() != c->nranks + 1) return fail(FCOO_ERR_ARG, "row bounds for %d ranks, comm has %d",
@@ -73,11 +75,20 @@ fcoo_status comm_gather_rows(fcoo_comm_t c, float* out, const std::vector<int64_
   for (int k = 0; k < c->nranks && r == ncclSuccess; ++k) {
     const size_t n = (size_t)(bounds[k + 1] - bounds[k]) * (size_t)R;
     if (n == 0) continue;
-    float* p = out + (size_t)bounds[k] * (size_t)R;
-    r = ncclBroadcast(p, p, n, ncclFloat, k, c->comm, s);
+    T* p = out + (size_t)bounds[k] * (size_t)R;
+    r = ncclBroadcast(p, p, n, ty, k, c->comm, s);
   }
   const ncclResult_t r2 = ncclGroupEnd();
   return nccl_status(c, r != ncclSuccess ? r : r2, "owned-rows gather (ncclBroadcast group)");
+}
+
+fcoo_status comm_gather_rows(fcoo_comm_t c, float* out, const std::vector<int64_t>& bounds, int R, cudaStream_t s) {
+  return gather_rows_t<float>(c, out, bounds, R, ncclFloat, s);
+}
+
+fcoo_status comm_gather_rows_f64(fcoo_comm_t c, double* out, const std::vector<int64_t>& bounds, int R,
+                                 cudaStream_t s) {
+  return gather_rows_t<double>(c, out, bounds, R, ncclDouble, s);
 }
 
 fcoo_status comm_allreduce_u32(fcoo_comm_t c, uint32_t* buf, size_t count, cudaStream_t s) {

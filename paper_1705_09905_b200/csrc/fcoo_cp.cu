@@ -518,11 +518,22 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
   fcoo_build_opts bb = bo;
   bb.flags |= FCOO_BUILD_BLOCKED;
   const bool try_blocked = !o->deterministic && o->layout == 0 && N <= 5;
+  // dist: X is this rank's chunk; each mode's handle holds the rank's nnz-balanced rows (row shards,
+  // owned-rows all-gather: fcoo_build_distributed); else tile shards of a redundant build
+  const bool dist = o->dist && o->comm;
+  if (o->dist && (!o->comm || o->deterministic))
+    return fail(FCOO_ERR_ARG, "cp_als dist needs a comm and excludes deterministic");
   for (int n = 0; n < N; ++n) {
-    fcoo_status st = try_blocked ? fcoo_build(X, n, &bb, alloc, (void*)s, &H[n]) : FCOO_ERR_ARG;
-    if (st == FCOO_ERR_ARG) st = fcoo_build(X, n, &bo, alloc, (void*)s, &H[n]);  // layout not applicable
+    fcoo_status st;
+    if (dist) {
+      st = try_blocked ? fcoo_build_distributed(X, n, &bb, o->comm, alloc, (void*)s, &H[n]) : FCOO_ERR_ARG;
+      if (st == FCOO_ERR_ARG) st = fcoo_build_distributed(X, n, &bo, o->comm, alloc, (void*)s, &H[n]);
+    } else {
+      st = try_blocked ? fcoo_build(X, n, &bb, alloc, (void*)s, &H[n]) : FCOO_ERR_ARG;
+      if (st == FCOO_ERR_ARG) st = fcoo_build(X, n, &bo, alloc, (void*)s, &H[n]);  // layout not applicable
+    }
     if (st) { cleanup(); return st; }
-    if (o->comm && o->nranks > 1) fcoo_set_shard(H[n], o->rank, o->nranks, o->comm);
+    if (!dist && o->comm && o->nranks > 1) fcoo_set_shard(H[n], o->rank, o->nranks, o->comm);
     if (o->deterministic) {  // reserve the boundary partials now: nothing allocates during capture
       st = ensure_dpart(H[n], sizeof(double) * (size_t)H[n]->ntiles * 2 * (size_t)R, s);
       if (st) { cleanup(); return st; }
@@ -637,12 +648,14 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
   }
   // initial Grams of the given factors; |X|^2
   for (int m = 0; m < N && !st; ++m) st = gram(factors[m], X->dims[m], Gs.as<double>() + (int64_t)m * RR);
-  int nx = (int)std::min<int64_t>(maxchunks, std::max<int64_t>(1, (X->nnz + 65535) / 65536));
-  int64_t xper = (X->nnz + nx - 1) / nx;
+  // |X|^2 partials; dist: the same number of partials on every rank, summed over the ranks
+  int nx = dist ? (int)maxchunks : (int)std::min<int64_t>(maxchunks, std::max<int64_t>(1, (X->nnz + 65535) / 65536));
+  int64_t xper = std::max<int64_t>(1, (X->nnz + nx - 1) / nx);
   if (!st) {
     k_sumsq_partial<<<nx, kCT, 0, s>>>(X->val, X->nnz, xper, xpart.as<double>());
     fcoo::count_launch();
     if (cudaGetLastError() != cudaSuccess) st = fail(FCOO_ERR_CUDA, "k_sumsq_partial");
+    if (!st && dist) st = comm_allreduce_f64(o->comm, xpart.as<double>(), (size_t)nx, s);
   }
   // One CP-ALS iteration (Alg. 1 body), enqueued on s with no host synchronisation.
   auto iteration = [&]() -> fcoo_status {
@@ -667,7 +680,10 @@ fcoo_status cp_als_impl(const fcoo_coo* X, const fcoo_cp_opts* o, float* const* 
       FCOO_CUDA_TRY(cudaEventRecord(side.done, side.st));
       if (last && sharded) {
         st = run_mttkrp_f64(H[n], factors, R, M64.as<double>(), s);
-        if (!st) st = comm_allreduce_f64(o->comm, M64.as<double>(), (size_t)In * R, s);
+        if (!st && H[n]->row_comm)  // row shards: each rank's rows are complete
+          st = comm_gather_rows_f64(H[n]->row_comm, M64.as<double>(), H[n]->row_bounds, R, s);
+        else if (!st)
+          st = comm_allreduce_f64(o->comm, M64.as<double>(), (size_t)In * R, s);
       } else if (last) {
         st = run_mttkrp(H[n], factors, R, M.as<float>(), s, g, 0);
         if (!st) st = run_mttkrp_f64(H[n], factors, R, M64.as<double>(), s, g, 1);

@@ -131,6 +131,8 @@ fcoo_status run_ttm(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s
 // owned-rows combine of a row-sharded handle: rank k broadcasts rows [bounds[k], bounds[k+1]) of
 // `out` (R columns) in one NCCL group, so every rank ends with the full output (fcoo_comm.cu)
 fcoo_status comm_gather_rows(fcoo_comm_t comm, float* out, const std::vector<int64_t>& bounds, int R, cudaStream_t s);
+fcoo_status comm_gather_rows_f64(fcoo_comm_t comm, double* out, const std::vector<int64_t>& bounds, int R,
+                                 cudaStream_t s);
 // distributed build helpers (fcoo_comm.cu): in-place sum of u32 counts; all-gather of nranks u64
 // per rank; grouped send/recv of `elem` bytes per item (send[j]/recv[j] items to/from rank j)
 fcoo_status comm_allreduce_u32(fcoo_comm_t comm, uint32_t* buf, size_t count, cudaStream_t s);

@@ -73,7 +73,8 @@ class _HostView(ctypes.Structure):
 class _CpOpts(ctypes.Structure):
     _fields_ = [("R", ctypes.c_int), ("iters", ctypes.c_int), ("tol", ctypes.c_double), ("tile_nnz", ctypes.c_int),
                 ("comm", ctypes.c_void_p), ("rank", ctypes.c_int), ("nranks", ctypes.c_int),
-                ("seed", ctypes.c_uint64), ("deterministic", ctypes.c_int), ("layout", ctypes.c_int)]
+                ("seed", ctypes.c_uint64), ("deterministic", ctypes.c_int), ("layout", ctypes.c_int),
+                ("dist", ctypes.c_int)]
 
 
 # The exported symbols (every one declared in include/fcoo.h).
@@ -614,11 +615,12 @@ def fcoo_mttkrp_mc(f: Fcoo, factors, R: int, out: McBuffer, stream=None) -> torc
 
 
 def cp_als(coo: Coo, R: int, iters: int, factors, tol: float = 0.0, tile_nnz: int = 0, comm: Comm | None = None,
-           stream=None, seed: int = 0, deterministic: bool = False, layout: str = "auto"):
+           stream=None, seed: int = 0, deterministic: bool = False, layout: str = "auto", dist: bool = False):
     """In-place CP-ALS: `factors` (list of CUDA fp32 (I_m, R)) hold the initial factors (or, with
     seed != 0, are seeded on the device by the library) and receive the result.  layout "auto": the
-    blocked F-COO where the build allows it; "fcoo": the plain F-COO for every mode.
-    Returns (lambda CUDA fp32 (R,), fit_trace list)."""
+    blocked F-COO where the build allows it; "fcoo": the plain F-COO for every mode.  dist=True (with
+    a comm): `coo` is this rank's chunk of the nonzeros and every mode runs on row shards
+    (fcoo_build_distributed, owned-rows all-gather).  Returns (lambda CUDA fp32 (R,), fit_trace list)."""
     import numpy as np
     L = load_library()
     if len(factors) != coo.order:
@@ -631,7 +633,8 @@ def cp_als(coo: Coo, R: int, iters: int, factors, tol: float = 0.0, tile_nnz: in
     trace = np.zeros(iters, np.float64)
     done = ctypes.c_int(0)
     opts = _CpOpts(R, iters, tol, tile_nnz, comm.h if comm else None, comm.rank if comm else 0,
-                   comm.nranks if comm else 1, seed, 1 if deterministic else 0, 1 if layout == "fcoo" else 0)
+                   comm.nranks if comm else 1, seed, 1 if deterministic else 0, 1 if layout == "fcoo" else 0,
+                   1 if dist else 0)
     arr = (ctypes.c_void_p * len(factors))(*[U.data_ptr() for U in factors])
     _check(L.cp_als(ctypes.byref(coo.c), ctypes.byref(opts), arr, ctypes.c_void_p(lam.data_ptr()),
                     trace.ctypes.data_as(ctypes.POINTER(ctypes.c_double)), ctypes.byref(done),

@@ -237,3 +237,30 @@ def test_planted_order4_fit_crosses_exact_switch(F):
     for m in range(len(dims)):
         _close_cols(fs[m].cpu().numpy(), f_o[m], 1e-4, f"planted U_{m}")
     assert np.allclose(lam.cpu().numpy(), l_o, rtol=1e-4, atol=0)
+
+
+def test_dist_one_rank_matches_oracle(F):
+    """cp_als(dist=True) with a 1-rank NCCL comm: every mode built by fcoo_build_distributed from the
+    (whole) chunk, |X|^2 partials all-reduced; the fit trace equals the oracle's within 1e-4 and the
+    non-dist run's within the same bound (the blocked kernels' red.add order is not fixed, so the
+    two runs are not bitwise equal)."""
+    import torch
+    dims = (60, 50, 40)
+    idx, val = gen.coo(dims, 20000, (0.5, 0.5, 0.5), 803)
+    R = 8
+    init = gen.factors(dims, R, 804)
+    _, _, tr_o = oracle.cp_als(dims, idx, val, R, 8, init)
+    coo = F.Coo.from_numpy(dims, idx, val)
+    comm = F.fcoo_comm_init(0, 1, F.fcoo_comm_unique_id())
+    try:
+        fs = [torch.from_numpy(f.copy()).cuda() for f in init]
+        lam, tr = F.cp_als(coo, R, 8, fs, tile_nnz=256, comm=comm, dist=True)
+        torch.cuda.synchronize()
+        assert np.max(np.abs(np.array(tr) - tr_o)) <= 1e-4, (tr, tr_o)
+        ref, lam_ref, tr_ref = _cp(F, dims, idx, val, R, 8, init)
+        assert np.max(np.abs(np.array(tr) - tr_ref)) <= 1e-4
+        assert np.allclose(lam.cpu().numpy(), lam_ref, rtol=1e-3)
+        with pytest.raises(F.FcooError):  # dist excludes deterministic
+            F.cp_als(coo, R, 2, fs, comm=comm, dist=True, deterministic=True)
+    finally:
+        comm.destroy()

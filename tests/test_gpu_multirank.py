@@ -6,8 +6,10 @@ rank checked against the fp64 oracle:
     (comm_allreduce) and every rank holds the full result;
   - fcoo_build_distributed from per-rank chunks + fcoo_mttkrp with the owned-rows all-gather
     (row-partitioned handles, plain and blocked): every rank holds the full result;
-  - cp_als with the comm (sharded MTTKRP, fp64 all-reduce of the last mode, replicated R x R work):
-    the fit trace matches the oracle and the factors are identical on every rank.
+  - cp_als with the comm (sharded MTTKRP, fp64 all-reduce of the last mode, replicated R x R work),
+    and cp_als(dist=True) from per-rank chunks on row shards (owned-rows gathers, fp64 last mode
+    gathered, |X|^2 summed over ranks): the fit trace matches the oracle and the factors are
+    identical on every rank.
 Skips on a box with fewer than two GPUs (this round's boxes have one; the test lights up on an
 8 x B200 node)."""
 import os
@@ -80,6 +82,15 @@ def _worker(rank, world, port, q):
         gathered = [torch.empty_like(flat) for _ in range(world)]
         dist.all_gather(gathered, flat)
         assert all(torch.equal(gathered[0], g) for g in gathered), "factors differ across ranks"
+        # CP-ALS on row shards: each rank passes its chunk; same fit trace, replicated factors
+        fcp2 = [torch.from_numpy(f).cuda() for f in init]
+        lam2, trace2 = F.cp_als(chunk, R2, 6, fcp2, tile_nnz=64, comm=comm, dist=True)
+        torch.cuda.synchronize()
+        assert np.max(np.abs(np.asarray(trace2) - t_o)) <= 1e-4, (trace2, t_o)
+        flat = torch.cat([f.flatten() for f in fcp2] + [lam2])
+        gathered = [torch.empty_like(flat) for _ in range(world)]
+        dist.all_gather(gathered, flat)
+        assert all(torch.equal(gathered[0], g) for g in gathered), "row-shard factors differ across ranks"
         comm.destroy()
         dist.destroy_process_group()
         q.put((rank, "ok"))
