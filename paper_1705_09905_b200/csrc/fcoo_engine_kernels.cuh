@@ -424,7 +424,14 @@ __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_gr
 // B consecutive words from shared memory (broadcast within the group).
 template <int B>
 __device__ __forceinline__ void lds_batch(const uint32_t* p, uint32_t (&w)[B]) {
-  if constexpr (B == 8) {
+  static_assert(B == 1 || B == 2 || B == 4 || B % 4 == 0, "batch of 1, 2 or a multiple of 4 words");
+  if constexpr (B > 8) {
+#pragma unroll
+    for (int k = 0; k < B / 4; ++k) {
+      const uint4 q = reinterpret_cast<const uint4*>(p)[k];
+      w[4 * k] = q.x; w[4 * k + 1] = q.y; w[4 * k + 2] = q.z; w[4 * k + 3] = q.w;
+    }
+  } else if constexpr (B == 8) {
     uint4 lo = reinterpret_cast<const uint4*>(p)[0], hi = reinterpret_cast<const uint4*>(p)[1];
     w[0] = lo.x; w[1] = lo.y; w[2] = lo.z; w[3] = lo.w; w[4] = hi.x; w[5] = hi.y; w[6] = hi.z; w[7] = hi.w;
   } else if constexpr (B == 4) {
