@@ -342,7 +342,8 @@ fcoo_status fcoo_set_row_shard(fcoo_t f, int rank, int nranks, const int64_t* bo
  *   NCCL all-gather of the per-destination counts -> grouped ncclSend/ncclRecv of the buckets
  *   (own bucket: device copy) -> fcoo_build (opts: tile, flags, block rows as usual) -> fcoo_set_row_shard.
  * A rank whose range received no nonzeros gets an empty handle (its rows read 0).  Synchronises the
- * host several times (setup path).  Errors: as fcoo_build, plus SHAPE (opts->op != MTTKRP), NCCL. */
+ * host several times (setup path).  Errors: as fcoo_build, plus SHAPE (opts->op != MTTKRP), ARG
+ * (FCOO_BUILD_KEEP_PERM: a permutation would index the rank's received nonzeros), NCCL. */
 fcoo_status fcoo_build_distributed(const fcoo_coo* local, int mode, const fcoo_build_opts* opts, fcoo_comm_t comm,
                                    const fcoo_allocator* alloc, void* stream, fcoo_t* out);
 

@@ -276,6 +276,8 @@ fcoo_status fcoo_build_distributed(const fcoo_coo* local, int mode, const fcoo_b
   fcoo_status st = check_coo_arrays(local, mode);
   if (st) return st;
   if (opts && opts->op != FCOO_OP_MTTKRP) return fail(FCOO_ERR_SHAPE, "the distributed build is for SpMTTKRP handles");
+  // a permutation would index this rank's RECEIVED nonzeros, not the caller's chunk: not offered
+  if (opts && (opts->flags & FCOO_BUILD_KEEP_PERM)) return fail(FCOO_ERR_ARG, "KEEP_PERM is not available in the distributed build");
   cudaStream_t s = (cudaStream_t)stream;
   int rank = 0, nranks = 1;
   comm_rank_size(comm, &rank, &nranks);

@@ -393,12 +393,12 @@ def fcoo_set_row_shard(f: "Fcoo", rank: int, bounds, comm: "Comm" = None):
     f.info = f._info()
 
 
-def fcoo_build_distributed(local: Coo, mode: int, comm: "Comm", tile_nnz: int = 0, keep_perm: bool = False,
-                           blocked: bool = False, block_rows: int = 0, stream=None) -> "Fcoo":
+def fcoo_build_distributed(local: Coo, mode: int, comm: "Comm", tile_nnz: int = 0, blocked: bool = False,
+                           block_rows: int = 0, stream=None) -> "Fcoo":
     """Collective: every rank passes its own chunk of the tensor and receives the F-COO of its
     nnz-balanced range of mode rows (histogram, all-reduce, partition, bucket, NCCL exchange, build)."""
     L = load_library()
-    opts = _BuildOpts(OP_MTTKRP, tile_nnz, _flags(keep_perm, False, False, blocked), block_rows)
+    opts = _BuildOpts(OP_MTTKRP, tile_nnz, _flags(False, False, False, blocked), block_rows)
     out = ctypes.c_void_p()
     _check(L.fcoo_build_distributed(ctypes.byref(local.c), mode, ctypes.byref(opts), comm.h, ctypes.byref(_ALLOCATOR),
                                     ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out)), "fcoo_build_distributed")

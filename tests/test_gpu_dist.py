@@ -174,3 +174,22 @@ def test_distributed_build_one_rank_nccl(F, blocked):
         he.destroy()
     finally:
         comm.destroy()
+
+
+def test_distributed_build_rejects_keep_perm(F):
+    """A permutation would index the rank's received nonzeros, not its chunk: ARG (include/fcoo.h)."""
+    import ctypes
+
+    from paper_1705_09905_b200 import fcoo as FB
+    dims = (30, 20, 10)
+    idx, val = gen.coo(dims, 500, None, 105)
+    coo = F.Coo.from_numpy(dims, idx, val)
+    comm = _one_rank_comm(F)
+    try:
+        opts = FB._BuildOpts(F.OP_MTTKRP, 0, FB.BUILD_KEEP_PERM, 0)
+        out = ctypes.c_void_p()
+        rc = F.load_library().fcoo_build_distributed(ctypes.byref(coo.c), 0, ctypes.byref(opts), comm.h, None, None,
+                                                     ctypes.byref(out))
+        assert rc == F.ERR_ARG and not out.value
+    finally:
+        comm.destroy()
