@@ -193,3 +193,12 @@ def test_distributed_build_rejects_keep_perm(F):
         assert rc == F.ERR_ARG and not out.value
     finally:
         comm.destroy()
+
+
+def test_fake_ranks_order4_blocked(F):
+    """The row-partitioned steps on a 4-order tensor (blocked handles with 3 packed words per
+    nonzero), every mode, 3 fake ranks."""
+    dims = (40, 30, 20, 50)
+    idx, val = gen.coo(dims, 30000, (0.7, 0.3, 0.5, 0.2), 111)
+    for mode in range(4):
+        _fake_ranks(F, dims, idx, val, mode, 3, True)

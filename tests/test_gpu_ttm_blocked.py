@@ -117,3 +117,22 @@ def test_brainq_blocked_full_size(F):
     idx, val = gen.coo(w.dims, w.nnz, w.alpha, w.seed)
     for mode in range(3):
         _check(F, w.dims, idx, val, mode, 16, T=0, BR=0)
+
+
+def test_blocked_ttm_edge_shapes(F):
+    """Order 5; R = 128 (32-lane float4 groups) and R = 100 (scalar lanes); block rows that do not
+    divide I_n; an empty block (no nonzero has i_n in [64, 128)); a single fibre."""
+    dims = (6, 5, 4, 7, 3)
+    idx, val = gen.coo(dims, 2000, None, 107)
+    for mode in range(5):
+        _check(F, dims, idx, val, mode, 16, T=32, BR=32)
+    dims = (40, 300, 30)
+    idx, val = gen.coo(dims, 20000, (0.4, 0.2, 0.3), 109)
+    for R in (128, 100):
+        _check(F, dims, idx, val, 1, R, T=64, BR=96)
+    keep = (idx[1] < 64) | (idx[1] >= 128)
+    _check(F, dims, idx[:, keep].copy(), val[keep].copy(), 1, 16, T=32, BR=64)
+    n = 5000
+    one = np.stack([np.full(n, 3, np.uint32), np.arange(n, dtype=np.uint32) % 300, np.full(n, 7, np.uint32)])
+    one = one[:, np.unique(one[1], return_index=True)[1]].copy()
+    _check(F, dims, one, gen.uniform((one.shape[1],), 7, 0) + 0.5, 1, 32, T=32, BR=64, signed=False)
