@@ -98,6 +98,13 @@ typedef struct {
  * handles (SHAPE).  The build synchronises the host twice (block sizes, then errors), a TTM build
  * three times (then the fibre count). */
 #define FCOO_BUILD_BLOCKED 8u
+/* Second flag level (FCOO_OP_MTTKRP, plain layout, order >= 3; Fig. 2: "one F-COO
+ * serves TTM-3 and MTTKRP-1"): besides bf (slice heads), the build marks in bf2 the heads of the
+ * FIBRES of the same sorted stream -- (index tuple, every product coordinate but the last) -- with
+ * their own tile flags sf2, ordinals and fibre table, so that fcoo_ttm on this MTTKRP handle runs
+ * SpTTM (Eq.(3)) on the handle's LAST product mode (prod_modes[n_prod-1]) without a second build.
+ * Excludes BLOCKED and DETERMINISTIC (ARG). */
+#define FCOO_BUILD_FIBRE_FLAGS 16u
 
 /* Build options.  NULL -> {FCOO_OP_MTTKRP, 0 (automatic), 0}.
  * tile_nnz = T, the partition length ("threadlen", P:L272 / P:L426): a multiple of 32 in
@@ -156,7 +163,12 @@ fcoo_status fcoo_mttkrp(fcoo_t f, const float* const* factors, int R, float* out
  * (FCOO_BUILD_BLOCKED) the kernel keeps block b of U (BR rows) in shared memory and every
  * (block, fibre) segment is added into its fibre's row with red.global.add.
  *   U: device, I_n x R fp32 row-major.  out: device, nfib x R fp32 (fcoo_info), overwritten.
- * Errors: SHAPE (handle built for MTTKRP), RANK, ARG, CUDA, NCCL.  Asynchronous.
+ * On an MTTKRP handle built with FCOO_BUILD_FIBRE_FLAGS the same call runs SpTTM on the handle's
+ * last product mode m = prod_modes[n_prod-1] from the second flag level: U is I_m x R, out is
+ * nfib x R with one row per fibre in the stream's key order (fib_coord: index mode, then the other
+ * product modes in prod_modes order); it needs R % 4 == 0, R/4 a power of two <= 32, and 16-byte
+ * aligned U and out (else ARG).
+ * Errors: SHAPE (MTTKRP handle without the second flag level), RANK, ARG, CUDA, NCCL.  Asynchronous.
  */
 fcoo_status fcoo_ttm(fcoo_t f, const float* U, int R, float* out, void* stream);
 
@@ -192,10 +204,12 @@ typedef struct {
   int pk_shift;            /* IB of the packed word (blocked handles) */
   int n_words;             /* packed words per nonzero (blocked handles: 1 + max(0, n_prod - 2)) */
   int64_t nfib;            /* SpTTM handles: output rows = fibres (non-empty index tuples); = nsegs for a
-                              plain handle, <= nsegs for a blocked one (a fibre recurs once per block); 0 for MTTKRP */
+                              plain handle, <= nsegs for a blocked one (a fibre recurs once per block); MTTKRP
+                              handles: the fibres of the second flag level (FCOO_BUILD_FIBRE_FLAGS), else 0 */
   int row_sharded;         /* fcoo_set_row_shard / fcoo_build_distributed with nranks > 1 */
   int row_rank, row_nranks;
   int64_t row_begin, row_end; /* index-mode rows this handle holds ([0, I_n) when not row-sharded) */
+  int fibre_flags;         /* built with FCOO_BUILD_FIBRE_FLAGS (second flag level) */
 } fcoo_info_t;
 
 /* fcoo_info — host-side metadata; no device work. */
@@ -221,7 +235,9 @@ typedef struct {
   int64_t* blk_start;
   int64_t* blk_end;
   uint32_t* seg_row;   /* blocked SpTTM handles: u32[nsegs], the fibre (output row) of each segment */
-  uint32_t* fib_coord; /* SpTTM handles: u32[nfib*n_idx], the index tuple of each output row (plain: = seg_coord) */
+  uint32_t* fib_coord; /* SpTTM handles: u32[nfib*n_idx], the index tuple of each output row (plain: = seg_coord);
+                          fibre-flag MTTKRP handles: u32[nfib*(order-1)] (index mode, then prod_modes but the last) */
+  uint8_t* bf2;        /* fibre-flag MTTKRP handles: the second flag level, u8[ceil(S/8)] (LSB-first) */
 } fcoo_host_view;
 
 /* fcoo_export — copy the handle's arrays to host buffers; synchronises `stream`. */

@@ -139,8 +139,11 @@ fcoo_status fcoo_mttkrp_mc(fcoo_t f, const float* const* factors, int R, fcoo_mc
 
 fcoo_status fcoo_ttm(fcoo_t f, const float* U, int R, float* out, void* stream) {
   if (!f || !U || !out) return fcoo::fail(FCOO_ERR_ARG, "NULL handle/U/out");
-  if (f->op != FCOO_OP_TTM) return fcoo::fail(FCOO_ERR_SHAPE, "handle was built for SpMTTKRP");
   if (R < 1 || R > 256) return fcoo::fail(FCOO_ERR_RANK, "R=%d outside [1,256]", R);
+  if (f->op != FCOO_OP_TTM) {
+    if (!f->fibre_flags) return fcoo::fail(FCOO_ERR_SHAPE, "handle was built for SpMTTKRP (without FCOO_BUILD_FIBRE_FLAGS)");
+    return fcoo::run_ttm_fibres(f, U, R, out, (cudaStream_t)stream);
+  }
   return fcoo::run_ttm(f, U, R, out, (cudaStream_t)stream);
 }
 
@@ -177,7 +180,9 @@ fcoo_status fcoo_info(fcoo_t f, fcoo_info_t* info) {
   info->n_words = f->n_words;
   if (f->blocked)  // packed words + values + bf over the padded stream, block tables
     info->device_bytes += (int64_t)(f->bytes_blk + f->bytes_seg_row + f->bytes_fib);
-  info->nfib = f->op != FCOO_OP_TTM ? 0 : f->blocked ? f->nfib : f->nsegs;
+  info->nfib = f->op != FCOO_OP_TTM ? (f->fibre_flags ? f->nfib : 0) : f->blocked ? f->nfib : f->nsegs;
+  info->fibre_flags = f->fibre_flags;
+  if (f->fibre_flags) info->device_bytes += (int64_t)(f->bytes_l2 + f->bytes_fib);
   info->row_sharded = f->row_sharded;
   info->row_rank = f->row_rank;
   info->row_nranks = f->row_nranks;
@@ -238,6 +243,11 @@ fcoo_status fcoo_export(fcoo_t f, fcoo_host_view* v, void* stream) {
   if (v->val) FCOO_CUDA_TRY(cudaMemcpyAsync(v->val, f->val, 4 * nnz, cudaMemcpyDeviceToHost, s));
   if (f->op == FCOO_OP_TTM && v->fib_coord && f->nsegs > 0)  // plain SpTTM: the fibres are the segments
     FCOO_CUDA_TRY(cudaMemcpyAsync(v->fib_coord, f->seg_coord, 4 * f->nsegs * f->n_idx, cudaMemcpyDeviceToHost, s));
+  if (f->fibre_flags) {  // second flag level of an MTTKRP handle
+    if (v->bf2) FCOO_CUDA_TRY(cudaMemcpyAsync(v->bf2, f->bf2, (nnz + 7) / 8, cudaMemcpyDeviceToHost, s));
+    if (v->fib_coord && f->nfib > 0)
+      FCOO_CUDA_TRY(cudaMemcpyAsync(v->fib_coord, f->fib_coord, 4 * f->nfib * (f->order - 1), cudaMemcpyDeviceToHost, s));
+  }
   FCOO_CUDA_TRY(cudaStreamSynchronize(s));
   return FCOO_OK;
 }

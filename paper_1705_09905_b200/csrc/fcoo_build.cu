@@ -141,6 +141,40 @@ __global__ void k_seg_coord(const K* __restrict__ keys, const uint32_t* __restri
   for (int a = 0; a < L.n_idx; ++a) seg_coord[(int64_t)s * L.n_idx + a] = (uint32_t)((key >> L.shift[a]) & L.mask[a]);
 }
 
+// ---- second flag level (FCOO_BUILD_FIBRE_FLAGS; Fig. 2) ----
+// bf2: heads of fibres = positions whose key differs from the previous one above the last product
+// mode's bits (fib_shift = the bit offset of the second-to-last key position)
+template <class K>
+__global__ void k_fibre_flags(const K* __restrict__ keys, int fib_shift, int64_t nnz, int64_t nnz_pad,
+                              uint32_t* __restrict__ bf2, uint32_t* __restrict__ wcount) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nnz_pad) return;  // whole warps
+  bool head = false;
+  if (p < nnz) head = p == 0 || (keys[p] >> fib_shift) != (keys[p - 1] >> fib_shift);
+  const uint32_t word = __ballot_sync(0xffffffffu, head);
+  if ((threadIdx.x & 31) == 0) {
+    bf2[p >> 5] = word;
+    wcount[p >> 5] = __popc(word);
+  }
+}
+
+// fibre table: the key's fields above the last product mode (index modes, then product modes in
+// Q5 order but the last) of every bf2 head
+template <class K>
+__global__ void k_fib_coord_l2(const K* __restrict__ keys, const uint32_t* __restrict__ bf2,
+                               const uint32_t* __restrict__ wbase, KeyLayout L, int64_t nnz,
+                               uint32_t* __restrict__ fib) {
+  const int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= nnz) return;
+  const uint32_t word = bf2[p >> 5];
+  const int b = (int)(p & 31);
+  if (!((word >> b) & 1u)) return;
+  const uint32_t r = wbase[p >> 5] + __popc(word & ((1u << b) - 1u));
+  const K key = keys[p];
+  const int nf = L.order - 1;
+  for (int a = 0; a < nf; ++a) fib[(int64_t)r * nf + a] = (uint32_t)((key >> L.shift[a]) & L.mask[a]);
+}
+
 // ---- blocked layout (FCOO_BUILD_BLOCKED) ----
 // start[b] = first sorted position whose block id is >= b (start[nblocks] = nnz): thread p writes
 // start[b] for every b in (block(p-1), block(p)], so each entry is written exactly once.
@@ -293,6 +327,7 @@ void free_handle_arrays(fcoo_s* f) {
   if (f->blk_start) f->alloc.put(f->blk_start, f->bytes_blk, s);
   if (f->seg_row) f->alloc.put(f->seg_row, f->bytes_seg_row, s);
   if (f->fib_coord) f->alloc.put(f->fib_coord, f->bytes_fib, s);
+  if (f->bf2) f->alloc.put(f->bf2, f->bytes_l2, s);
   if (f->dpart) f->alloc.put(f->dpart, f->bytes_dpart, s);
   f->dpart = nullptr;
   f->bytes_dpart = 0;
@@ -303,6 +338,7 @@ void free_handle_arrays(fcoo_s* f) {
   f->pidx = nullptr; f->val = nullptr; f->bf = nullptr; f->sf = nullptr;
   f->seg_base = nullptr; f->seg_coord = nullptr; f->perm = nullptr;
   f->seg_row = nullptr; f->fib_coord = nullptr;
+  f->bf2 = nullptr; f->sf2 = nullptr; f->seg_base2 = nullptr;
 }
 
 }  // namespace
@@ -427,6 +463,46 @@ fcoo_status sort_and_flag(fcoo_s* f, const fcoo_coo* coo, const KeyLayout& L, co
   k_seg_coord<<<(unsigned)((nnz + TB - 1) / TB), TB, 0, s>>>(keys, f->bf, wbase.as<uint32_t>(), L, nnz, f->seg_coord);
   count_launch();
   if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_seg_coord: %s", cudaGetErrorString(ce));
+  if (!(flags & FCOO_BUILD_FIBRE_FLAGS)) return FCOO_OK;
+  // the second flag level on the same sorted stream (one more host sync for the fibre count)
+  f->fibre_flags = 1;
+  const size_t w4 = sizeof(uint32_t);
+  f->bytes_l2 = w4 * ((size_t)nwords + (size_t)((ntiles + 31) / 32 + 1) + (size_t)(ntiles + 1));
+  f->bf2 = reinterpret_cast<uint32_t*>(f->alloc.get(f->bytes_l2, s));
+  if (!f->bf2) return fail(FCOO_ERR_OOM, "second flag level allocation");
+  f->sf2 = f->bf2 + nwords;
+  f->seg_base2 = f->sf2 + (ntiles + 31) / 32 + 1;
+  if ((ce = cudaMemsetAsync(wcount.p, 0, sizeof(uint32_t) * (nwords + 1), s)) != cudaSuccess)
+    return fail(FCOO_ERR_CUDA, "memset: %s", cudaGetErrorString(ce));
+  const int fib_shift = L.shift[L.order - 2];
+  k_fibre_flags<K><<<(unsigned)((nnz_pad + TB - 1) / TB), TB, 0, s>>>(keys, fib_shift, nnz, nnz_pad, f->bf2,
+                                                                       wcount.as<uint32_t>());
+  count_launch();
+  if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_fibre_flags: %s", cudaGetErrorString(ce));
+  {
+    Buf scantmp(&f->alloc, scan_bytes, s);
+    if (!scantmp.ok()) return fail(FCOO_ERR_OOM, "scan scratch");
+    if ((ce = cub::DeviceScan::ExclusiveSum(scantmp.p, scan_bytes, wcount.as<uint32_t>(), wbase.as<uint32_t>(),
+                                            (int64_t)(nwords + 1), s)) != cudaSuccess)
+      return fail(FCOO_ERR_CUDA, "scan: %s", cudaGetErrorString(ce));
+    count_launch(2);
+  }
+  k_tiles<<<(unsigned)((tthreads + TB - 1) / TB), TB, 0, s>>>(f->bf2, wbase.as<uint32_t>(), ntiles, T / 32, nwords,
+                                                             f->sf2, f->seg_base2);
+  count_launch();
+  uint32_t nfib = 0;
+  if ((ce = cudaMemcpyAsync(&nfib, wbase.as<uint32_t>() + nwords, sizeof(uint32_t), cudaMemcpyDeviceToHost, s)) !=
+          cudaSuccess ||
+      (ce = cudaStreamSynchronize(s)) != cudaSuccess)
+    return fail(FCOO_ERR_CUDA, "build sync: %s", cudaGetErrorString(ce));
+  f->nfib = nfib;
+  f->fib_coord = grab<uint32_t>(f, sizeof(uint32_t) * (size_t)std::max<int64_t>(1, (int64_t)nfib * (L.order - 1)), s,
+                                &f->bytes_fib);
+  if (!f->fib_coord) return fail(FCOO_ERR_OOM, "fibre table allocation");
+  k_fib_coord_l2<K><<<(unsigned)((nnz + TB - 1) / TB), TB, 0, s>>>(keys, f->bf2, wbase.as<uint32_t>(), L, nnz,
+                                                                    f->fib_coord);
+  count_launch();
+  if ((ce = cudaGetLastError()) != cudaSuccess) return fail(FCOO_ERR_CUDA, "k_fib_coord_l2: %s", cudaGetErrorString(ce));
   return FCOO_OK;
 }
 
@@ -648,6 +724,10 @@ fcoo_status build_impl(const fcoo_coo* coo, int mode, const fcoo_build_opts* opt
   fcoo_status st = plan_modes(&tmp, coo->order, coo->dims, op, mode, (flags & FCOO_BUILD_PRODUCT_DESC) != 0);
   if (st) return st;
   const bool blocked = (flags & FCOO_BUILD_BLOCKED) != 0;
+  if (flags & FCOO_BUILD_FIBRE_FLAGS) {
+    if (op != FCOO_OP_MTTKRP || blocked || (flags & FCOO_BUILD_DETERMINISTIC) || tmp.n_prod < 2)
+      return fail(FCOO_ERR_ARG, "FCOO_BUILD_FIBRE_FLAGS needs a plain, non-deterministic MTTKRP handle of order >= 3");
+  }
   int BR = 0;
   if (blocked) {
     BR = (opts && opts->block_rows) ? opts->block_rows : 512;

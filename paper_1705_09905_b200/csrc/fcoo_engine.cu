@@ -64,6 +64,16 @@ __global__ void k_combine_boundaries(const uint32_t* __restrict__ sf, const uint
   }
 }
 
+// rows of segments crossing a tile boundary (flag level sf / seg_base) set to 0 (see above)
+fcoo_status zero_boundary_rows_f32(const uint32_t* sf, const uint32_t* seg_base, int64_t tile_begin, int64_t tile_end,
+                                   int R, float* out, cudaStream_t s) {
+  const int64_t nt = tile_end - tile_begin;
+  if (nt <= 0) return FCOO_OK;
+  k_zero_boundary_rows<float><<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(sf, seg_base, tile_begin, tile_end, R, out);
+  FCOO_LAUNCH_CHECK();
+  return FCOO_OK;
+}
+
 namespace {
 
 template <class ACC>

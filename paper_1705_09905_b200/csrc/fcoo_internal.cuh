@@ -84,7 +84,15 @@ struct fcoo_s {
   // blocked SpTTM handles (op TTM): the output rows are the fibres (distinct index tuples in
   // lexicographic order); seg_row[s] = fibre of blocked segment s, fib_coord = the tuples
   uint32_t* seg_row = nullptr;    // device [nsegs]
-  uint32_t* fib_coord = nullptr;  // device [nfib x n_idx]
+  uint32_t* fib_coord = nullptr;  // device [nfib x n_idx] (fibre-flag MTTKRP handles: [nfib x (order-1)])
+  // second flag level (FCOO_BUILD_FIBRE_FLAGS, plain MTTKRP handles; Fig. 2): bf2 marks
+  // the heads of fibres = (index tuple, every product coordinate but the last) on the same stream,
+  // with its own tile flags and fibre ordinals, so fcoo_ttm runs SpTTM on the last product mode
+  int fibre_flags = 0;
+  uint32_t* bf2 = nullptr;        // nnz_pad / 32 words
+  uint32_t* sf2 = nullptr;        // ceil(ntiles/32) words (+1)
+  uint32_t* seg_base2 = nullptr;  // ntiles + 1
+  size_t bytes_l2 = 0;
   int64_t nfib = 0;
   size_t bytes_seg_row = 0, bytes_fib = 0;
   std::vector<int64_t> h_blk_start, h_blk_end;  // host copies (work tables, export)
@@ -145,6 +153,10 @@ fcoo_status build_empty(int order, const int64_t* dims, int op, int mode, const 
                         fcoo_t* out);
 // SpTTM through the specialised kernel (fcoo_ttm.cu) when it applies; false = use the engine
 bool run_ttm_lean(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s, fcoo_status* st);
+// SpTTM on the last product mode of a fibre-flag MTTKRP handle (second flag level; fcoo_ttm.cu)
+fcoo_status run_ttm_fibres(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s);
+fcoo_status zero_boundary_rows_f32(const uint32_t* sf, const uint32_t* seg_base, int64_t tile_begin, int64_t tile_end,
+                                   int R, float* out, cudaStream_t s);
 // deterministic handles: make f->dpart hold at least `bytes` (stream-ordered on s)
 fcoo_status ensure_dpart(fcoo_s* f, size_t bytes, cudaStream_t s);
 fcoo_status run_ttmc(fcoo_s* f, const float* const* factors, const int* ranks, float* out, cudaStream_t s);

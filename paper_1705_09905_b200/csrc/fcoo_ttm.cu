@@ -256,14 +256,49 @@ cudaError_t launch_ttm(const TtmParams& P, cudaStream_t s) {
 // SpTTM through the lean kernel when it applies (fp32 float4 lanes with R = 4G, G a power of two
 // in [2, 32], 16-B aligned U and output, not deterministic); returns false to let the caller use
 // the general engine.
-bool run_ttm_lean(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s, fcoo_status* st) {
+static bool lean_applies(int R, const float* U, const float* out) {
   const int q = R / 4;
-  if (R % 4 || q < 2 || q > 32 || (q & (q - 1)) || f->deterministic) return false;
-  if ((reinterpret_cast<uintptr_t>(U) & 15u) || (reinterpret_cast<uintptr_t>(out) & 15u)) return false;
+  if (R % 4 || q < 2 || q > 32 || (q & (q - 1))) return false;
+  return !((reinterpret_cast<uintptr_t>(U) & 15u) || (reinterpret_cast<uintptr_t>(out) & 15u));
+}
+static cudaError_t launch_lean(TtmParams& P, int R, cudaStream_t s);
+
+bool run_ttm_lean(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s, fcoo_status* st) {
+  if (!lean_applies(R, U, out) || f->deterministic) return false;
   TtmParams P{};
   P.idx = f->pidx; P.val = f->val; P.bf = f->bf; P.sf = f->sf; P.seg_base = f->seg_base; P.U = U; P.out = out;
   P.nnz = f->nnz; P.ntiles = f->ntiles; P.tile_begin = f->tile_begin; P.tile_end = f->tile_end;
   P.T = (int)f->T; P.R = R; P.In = (int)f->dims[f->mode];
+  const cudaError_t e = launch_lean(P, R, s);
+  *st = e == cudaSuccess ? FCOO_OK : fail(FCOO_ERR_CUDA, "ttm launch: %s", cudaGetErrorString(e));
+  return true;
+}
+
+// SpTTM on the last product mode of an MTTKRP handle from its second flag level (Fig. 2):
+// the same stream, the last product mode's index row as the TTM product index, bf2 / sf2 /
+// seg_base2 as the fibre flags; rows of fibres that cross a tile are zeroed first, the rest stored once.
+fcoo_status run_ttm_fibres(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s) {
+  if (!lean_applies(R, U, out))
+    return fail(FCOO_ERR_ARG, "SpTTM on the fibre level needs R %% 4 == 0, R/4 a power of two <= 32, 16-B aligned U/out");
+  TtmParams P{};
+  P.idx = f->pidx + (int64_t)(f->n_prod - 1) * f->nnz_pad;
+  P.val = f->val; P.bf = f->bf2; P.sf = f->sf2; P.seg_base = f->seg_base2; P.U = U; P.out = out;
+  P.nnz = f->nnz; P.ntiles = f->ntiles; P.tile_begin = f->tile_begin; P.tile_end = f->tile_end;
+  P.T = (int)f->T; P.R = R; P.In = (int)f->dims[f->prod_modes[f->n_prod - 1]];
+  if (f->tile_begin != 0 || f->tile_end != f->ntiles) {
+    FCOO_CUDA_TRY(cudaMemsetAsync(out, 0, sizeof(float) * (size_t)f->nfib * R, s));
+  } else {
+    const fcoo_status z = zero_boundary_rows_f32(f->sf2, f->seg_base2, f->tile_begin, f->tile_end, R, out, s);
+    if (z) return z;
+  }
+  const cudaError_t e = launch_lean(P, R, s);
+  if (e != cudaSuccess) return fail(FCOO_ERR_CUDA, "ttm launch: %s", cudaGetErrorString(e));
+  if (f->comm) return comm_allreduce(f->comm, out, (size_t)f->nfib * R, s);
+  return FCOO_OK;
+}
+
+static cudaError_t launch_lean(TtmParams& P, int R, cudaStream_t s) {
+  const int q = R / 4;
   // U in shared memory up to 32 KB with rows padded to >= 128 B (the staging of 256 threads takes
   // 35 KB at R = 16, 70 KB at R = 8)
   const bool smem = (size_t)P.In * std::max(R * 4, 128) <= 32 * 1024;
@@ -275,8 +310,7 @@ bool run_ttm_lean(fcoo_s* f, const float* U, int R, float* out, cudaStream_t s, 
     case 16: e = smem ? launch_ttm<16, true>(P, s) : launch_ttm<16, false>(P, s); break;
     default: e = smem ? launch_ttm<32, true>(P, s) : launch_ttm<32, false>(P, s); break;
   }
-  *st = e == cudaSuccess ? FCOO_OK : fail(FCOO_ERR_CUDA, "ttm launch: %s", cudaGetErrorString(e));
-  return true;
+  return e;
 }
 
 }  // namespace fcoo

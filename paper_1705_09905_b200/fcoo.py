@@ -24,6 +24,7 @@ BUILD_KEEP_PERM = 1
 BUILD_PRODUCT_DESC = 2
 BUILD_DETERMINISTIC = 4
 BUILD_BLOCKED = 8
+BUILD_FIBRE_FLAGS = 16
 
 
 class FcooError(RuntimeError):
@@ -60,14 +61,15 @@ class _Info(ctypes.Structure):
                 ("block_rows", ctypes.c_int), ("nblocks", ctypes.c_int64), ("nstream", ctypes.c_int64),
                 ("pk_shift", ctypes.c_int), ("n_words", ctypes.c_int), ("nfib", ctypes.c_int64),
                 ("row_sharded", ctypes.c_int), ("row_rank", ctypes.c_int), ("row_nranks", ctypes.c_int),
-                ("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64)]
+                ("row_begin", ctypes.c_int64), ("row_end", ctypes.c_int64), ("fibre_flags", ctypes.c_int)]
 
 
 class _HostView(ctypes.Structure):
     _fields_ = [("perm", ctypes.c_void_p), ("bf", ctypes.c_void_p), ("sf", ctypes.c_void_p),
                 ("seg_base", ctypes.c_void_p), ("seg_coord", ctypes.c_void_p), ("pidx", ctypes.c_void_p),
                 ("val", ctypes.c_void_p), ("pk", ctypes.c_void_p), ("blk_start", ctypes.c_void_p),
-                ("blk_end", ctypes.c_void_p), ("seg_row", ctypes.c_void_p), ("fib_coord", ctypes.c_void_p)]
+                ("blk_end", ctypes.c_void_p), ("seg_row", ctypes.c_void_p), ("fib_coord", ctypes.c_void_p),
+                ("bf2", ctypes.c_void_p)]
 
 
 class _CpOpts(ctypes.Structure):
@@ -285,6 +287,7 @@ class Info:
     row_nranks: int = 1
     row_begin: int = 0
     row_end: int = 0
+    fibre_flags: bool = False
 
 
 class Fcoo:
@@ -304,7 +307,7 @@ class Fcoo:
                     inf.tile_nnz, bool(inf.dense_rows), inf.storage_bytes, inf.seg_table_bytes, inf.device_bytes,
                     inf.shard, inf.nshards, inf.tile_begin, inf.tile_end, bool(inf.blocked), inf.block_rows,
                     inf.nblocks, inf.nstream, inf.pk_shift, inf.n_words, inf.nfib, bool(inf.row_sharded),
-                    inf.row_rank, inf.row_nranks, inf.row_begin, inf.row_end)
+                    inf.row_rank, inf.row_nranks, inf.row_begin, inf.row_end, bool(inf.fibre_flags))
 
     def destroy(self):
         if self.h:
@@ -325,10 +328,13 @@ def _flags(keep_perm=False, product_desc=False, deterministic=False, blocked=Fal
 
 def fcoo_build(coo: Coo, mode: int, op: int = OP_MTTKRP, tile_nnz: int = 0, keep_perm: bool = False,
                product_desc: bool = False, stream=None, deterministic: bool = False, blocked: bool = False,
-               block_rows: int = 0) -> Fcoo:
-    """blocked=True: the blocked F-COO of FCOO_BUILD_BLOCKED (block_rows 0 = the library default)."""
+               block_rows: int = 0, fibre_flags: bool = False) -> Fcoo:
+    """blocked=True: the blocked F-COO of FCOO_BUILD_BLOCKED (block_rows 0 = the library default).
+    fibre_flags=True (MTTKRP, plain): the second flag level, so fcoo_ttm runs SpTTM on the handle's
+    last product mode (Fig. 2)."""
     L = load_library()
-    opts = _BuildOpts(op, tile_nnz, _flags(keep_perm, product_desc, deterministic, blocked), block_rows)
+    opts = _BuildOpts(op, tile_nnz, _flags(keep_perm, product_desc, deterministic, blocked)
+                      | (BUILD_FIBRE_FLAGS if fibre_flags else 0), block_rows)
     out = ctypes.c_void_p()
     _check(L.fcoo_build(ctypes.byref(coo.c), mode, ctypes.byref(opts), ctypes.byref(_ALLOCATOR),
                         ctypes.c_void_p(_stream_ptr(stream)), ctypes.byref(out)), "fcoo_build")
@@ -445,8 +451,10 @@ def fcoo_mttkrp(f: Fcoo, factors, R: int, out: torch.Tensor, stream=None) -> tor
 def fcoo_ttm(f: Fcoo, U: torch.Tensor, R: int, out: torch.Tensor, stream=None) -> torch.Tensor:
     L = load_library()
     _require_cuda(U, torch.float32, "U")
-    if tuple(U.shape) != (f.info.dims[f.info.mode], R):
-        raise ValueError(f"U has shape {tuple(U.shape)}, expected {(f.info.dims[f.info.mode], R)}")
+    # an MTTKRP handle with the second flag level runs SpTTM on its last product mode
+    m = f.info.mode if f.info.op == OP_TTM else f.info.prod_modes[-1]
+    if tuple(U.shape) != (f.info.dims[m], R):
+        raise ValueError(f"U has shape {tuple(U.shape)}, expected {(f.info.dims[m], R)}")
     _check_out(out, f.info.nfib, R)
     _check(L.fcoo_ttm(f.h, ctypes.c_void_p(U.data_ptr()), R, ctypes.c_void_p(out.data_ptr()),
                       ctypes.c_void_p(_stream_ptr(stream))), "fcoo_ttm")
@@ -510,11 +518,14 @@ def fcoo_export(f: Fcoo, perm: bool = False, stream=None) -> dict:
             d["seg_row"] = np.zeros(i.nsegs, np.uint32)
     if i.op == OP_TTM:
         d["fib_coord"] = np.zeros((i.nfib, i.n_idx), np.uint32)
+    elif i.fibre_flags:
+        d["fib_coord"] = np.zeros((i.nfib, i.order - 1), np.uint32)
+        d["bf2"] = np.zeros((ns + 7) // 8, np.uint8)
     if perm:
         d["perm"] = np.zeros(ns, np.uint32)
     v = _HostView(*(d[k].ctypes.data if k in d else None
                     for k in ("perm", "bf", "sf", "seg_base", "seg_coord", "pidx", "val", "pk", "blk_start",
-                              "blk_end", "seg_row", "fib_coord")))
+                              "blk_end", "seg_row", "fib_coord", "bf2")))
     _check(load_library().fcoo_export(f.h, ctypes.byref(v), ctypes.c_void_p(_stream_ptr(stream))), "fcoo_export")
     return d
 

@@ -107,6 +107,40 @@ def main():
             h.destroy()
         del coo
 
+    if "fibre" in ops:  # Fig. 2: one nell-2 stream for SpMTTKRP on mode 0 AND SpTTM on mode 2
+        w, idx, val = gen.workload("nell2")
+        coo = P.Coo.from_numpy(w.dims, idx, val)
+        nnz = int(val.shape[0])
+        import time as _t
+        for fl in (False, True):  # build cost of the second flag level
+            P.fcoo_build(coo, 0, fibre_flags=fl).destroy()
+        torch.cuda.synchronize()
+        t0 = _t.perf_counter()
+        h = P.fcoo_build(coo, 0, fibre_flags=True)
+        torch.cuda.synchronize()
+        b_fib = (_t.perf_counter() - t0) * 1e3
+        t0 = _t.perf_counter()
+        P.fcoo_build(coo, 0).destroy()
+        torch.cuda.synchronize()
+        b_plain = (_t.perf_counter() - t0) * 1e3
+        m = h.info.prod_modes[-1]
+        fs32 = [torch.from_numpy(f).cuda() for f in gen.factors(w.dims, 32, 7)]
+        outm = torch.empty((w.dims[0], 32), device="cuda")
+        ms_m = gpu_ms(lambda: P.fcoo_mttkrp(h, fs32, 32, outm), a.reps)
+        U = torch.from_numpy(gen.factors(w.dims, 16, 7)[m]).cuda()
+        outt = torch.empty((h.info.nfib, 16), device="cuda")
+        ms_t = gpu_ms(lambda: P.fcoo_ttm(h, U, 16, outt), a.reps)
+        t = P.fcoo_build(coo, m, op=P.OP_TTM)
+        outd = torch.empty((t.info.nfib, 16), device="cuda")
+        ms_d = gpu_ms(lambda: P.fcoo_ttm(t, U, 16, outd), a.reps)
+        emit({"op": "fibre_level", "workload": "nell2", "handle": "MTTKRP mode 0 + FCOO_BUILD_FIBRE_FLAGS",
+              "ttm_mode": m, "nfib": h.info.nfib, "build_ms_plain": round(b_plain, 2), "build_ms_fibre": round(b_fib, 2),
+              "mttkrp_R32_ms": round(ms_m, 4), "ttm_R16_on_mttkrp_handle_ms": round(ms_t, 4),
+              "ttm_R16_dedicated_handle_ms": round(ms_d, 4), "nnz": nnz})
+        h.destroy()
+        t.destroy()
+        del coo
+
     if "ttmc" in ops or "cp" in ops:
         w, idx, val = gen.workload("nell2")
         nnz = int(val.shape[0])
