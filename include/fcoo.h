@@ -357,8 +357,9 @@ fcoo_status fcoo_set_row_shard(fcoo_t f, int rank, int nranks, const int64_t* bo
  *   fcoo_slice_histogram -> NCCL all-reduce -> fcoo_row_partition -> fcoo_bucket_rows ->
  *   NCCL all-gather of the per-destination counts -> grouped ncclSend/ncclRecv of the buckets
  *   (own bucket: device copy) -> fcoo_build (opts: tile, flags, block rows as usual) -> fcoo_set_row_shard.
- * A rank whose range received no nonzeros gets an empty handle (its rows read 0).  Synchronises the
- * host several times (setup path).  Errors: as fcoo_build, plus SHAPE (opts->op != MTTKRP), ARG
+ * A rank whose range received no nonzeros gets an empty handle (its rows read 0).  A local failure
+ * (bad coordinate, allocation) is agreed across the ranks before each collective step, so every rank
+ * returns an error instead of waiting in a collective.  Synchronises the host several times (setup path).  Errors: as fcoo_build, plus SHAPE (opts->op != MTTKRP), ARG
  * (FCOO_BUILD_KEEP_PERM: a permutation would index the rank's received nonzeros), NCCL. */
 fcoo_status fcoo_build_distributed(const fcoo_coo* local, int mode, const fcoo_build_opts* opts, fcoo_comm_t comm,
                                    const fcoo_allocator* alloc, void* stream, fcoo_t* out);

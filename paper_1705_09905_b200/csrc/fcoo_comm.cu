@@ -91,6 +91,23 @@ fcoo_status comm_gather_rows_f64(fcoo_comm_t c, double* out, const std::vector<i
   return gather_rows_t<double>(c, out, bounds, R, ncclDouble, s);
 }
 
+// Collective status agreement: every rank passes its local status and all return the largest one
+// (FCOO_OK only if every rank succeeded), so a local failure before a collective step makes every
+// rank stop instead of leaving the others blocked in that collective.  Synchronises `s`.
+fcoo_status comm_agree(fcoo_comm_t c, fcoo_status local, cudaStream_t s) {
+  if (!c || !c->comm || c->nranks == 1) return local;
+  int v = (int)local;
+  if (cudaMemcpyAsync(c->scratch, &v, sizeof(int), cudaMemcpyHostToDevice, s) != cudaSuccess)
+    return fail(FCOO_ERR_CUDA, "status agreement upload");
+  fcoo_status st = nccl_status(c, ncclAllReduce(c->scratch, c->scratch, 1, ncclInt, ncclMax, c->comm, s), "agree");
+  if (st) return st;
+  if (cudaMemcpyAsync(&v, c->scratch, sizeof(int), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+      cudaMemsetAsync(c->scratch, 0, sizeof(int), s) != cudaSuccess || cudaStreamSynchronize(s) != cudaSuccess)
+    return fail(FCOO_ERR_CUDA, "status agreement download");
+  if (v != (int)FCOO_OK && local == FCOO_OK) return fail((fcoo_status)v, "another rank failed (status %d)", v);
+  return v == (int)FCOO_OK ? FCOO_OK : local;
+}
+
 fcoo_status comm_allreduce_u32(fcoo_comm_t c, uint32_t* buf, size_t count, cudaStream_t s) {
   if (!c || !c->comm) return FCOO_OK;
   return nccl_status(c, ncclAllReduce(buf, buf, count, ncclUint32, ncclSum, c->comm, s), "ncclAllReduce(u32)");

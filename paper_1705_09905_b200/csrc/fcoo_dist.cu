@@ -289,8 +289,8 @@ fcoo_status fcoo_build_distributed(const fcoo_coo* local, int mode, const fcoo_b
   std::vector<int64_t> bounds(nranks + 1);
   {
     Buf hist(&al, sizeof(uint32_t) * (size_t)I, s);
-    if (!hist.ok()) return fail(FCOO_ERR_OOM, "histogram allocation");
-    st = slice_hist(local, mode, hist.as<uint32_t>(), al, s);
+    st = hist.ok() ? slice_hist(local, mode, hist.as<uint32_t>(), al, s) : fail(FCOO_ERR_OOM, "histogram allocation");
+    st = comm_agree(comm, st, s);  // a bad coordinate on one rank stops every rank here
     if (st) return st;
     st = comm_allreduce_u32(comm, hist.as<uint32_t>(), (size_t)I, s);
     if (st) return st;
@@ -307,14 +307,16 @@ fcoo_status fcoo_build_distributed(const fcoo_coo* local, int mode, const fcoo_b
   std::vector<uint32_t*> sidx(order), ridx(order);
   for (int m = 0; m < order; ++m) sidx[m] = buf(sizeof(uint32_t) * (size_t)nnz)->as<uint32_t>();
   float* sval = buf(sizeof(float) * (size_t)nnz)->as<float>();
-  for (Buf* b : bufs) if (!b->ok()) { release(); return fail(FCOO_ERR_OOM, "send buffers"); }
   std::vector<int64_t> send(nranks, 0), recv(nranks, 0);
-  st = bucket_rows(local, mode, bounds.data(), nranks, sidx.data(), sval, send.data(), al, s);
+  st = FCOO_OK;
+  for (Buf* b : bufs) if (!b->ok()) st = fail(FCOO_ERR_OOM, "send buffers");
+  if (!st) st = bucket_rows(local, mode, bounds.data(), nranks, sidx.data(), sval, send.data(), al, s);
+  Buf sc(&al, sizeof(uint64_t) * nranks, s), all(&al, sizeof(uint64_t) * (size_t)nranks * nranks, s);
+  if (!st && (!sc.ok() || !all.ok())) st = fail(FCOO_ERR_OOM, "count buffers");
+  st = comm_agree(comm, st, s);
   if (st) { release(); return st; }
   // 3. who sends how much to whom: all-gather of every rank's per-destination counts
   {
-    Buf sc(&al, sizeof(uint64_t) * nranks, s), all(&al, sizeof(uint64_t) * (size_t)nranks * nranks, s);
-    if (!sc.ok() || !all.ok()) { release(); return fail(FCOO_ERR_OOM, "count buffers"); }
     std::vector<uint64_t> h(send.begin(), send.end()), ha((size_t)nranks * nranks);
     if (cudaMemcpyAsync(sc.p, h.data(), sizeof(uint64_t) * nranks, cudaMemcpyHostToDevice, s) != cudaSuccess) {
       release();
@@ -331,11 +333,17 @@ fcoo_status fcoo_build_distributed(const fcoo_coo* local, int mode, const fcoo_b
   }
   int64_t total = 0;
   for (int j = 0; j < nranks; ++j) total += recv[j];
-  if (total >= 4294967295LL) { release(); return fail(FCOO_ERR_ARG, "rank %d would receive %lld >= 2^32 nonzeros", rank, (long long)total); }
+  st = total >= 4294967295LL ? fail(FCOO_ERR_ARG, "rank %d would receive %lld >= 2^32 nonzeros", rank, (long long)total)
+                             : FCOO_OK;
   // 4. the exchange: one grouped send/recv per array (the own bucket by a device copy)
-  for (int m = 0; m < order; ++m) ridx[m] = buf(sizeof(uint32_t) * (size_t)total)->as<uint32_t>();
-  float* rval = buf(sizeof(float) * (size_t)total)->as<float>();
-  for (Buf* b : bufs) if (!b->ok()) { release(); return fail(FCOO_ERR_OOM, "receive buffers"); }
+  float* rval = nullptr;
+  if (!st) {
+    for (int m = 0; m < order; ++m) ridx[m] = buf(sizeof(uint32_t) * (size_t)total)->as<uint32_t>();
+    rval = buf(sizeof(float) * (size_t)total)->as<float>();
+    for (Buf* b : bufs) if (!b->ok()) st = fail(FCOO_ERR_OOM, "receive buffers");
+  }
+  st = comm_agree(comm, st, s);
+  if (st) { release(); return st; }
   for (int m = 0; m < order && !st; ++m)
     st = comm_exchange(comm, sidx[m], send.data(), ridx[m], recv.data(), sizeof(uint32_t), s);
   if (!st) st = comm_exchange(comm, sval, send.data(), rval, recv.data(), sizeof(float), s);

@@ -144,6 +144,8 @@ fcoo_status comm_gather_rows_f64(fcoo_comm_t comm, double* out, const std::vecto
 // distributed build helpers (fcoo_comm.cu): in-place sum of u32 counts; all-gather of nranks u64
 // per rank; grouped send/recv of `elem` bytes per item (send[j]/recv[j] items to/from rank j)
 fcoo_status comm_allreduce_u32(fcoo_comm_t comm, uint32_t* buf, size_t count, cudaStream_t s);
+// every rank's status -> the largest (collective; a local failure stops all ranks together)
+fcoo_status comm_agree(fcoo_comm_t comm, fcoo_status local, cudaStream_t s);
 fcoo_status comm_allgather_u64(fcoo_comm_t comm, const uint64_t* send, uint64_t* recv, size_t count, cudaStream_t s);
 fcoo_status comm_exchange(fcoo_comm_t comm, const void* sendbuf, const int64_t* send_counts, void* recvbuf,
                           const int64_t* recv_counts, size_t elem, cudaStream_t s);

@@ -202,3 +202,20 @@ def test_fake_ranks_order4_blocked(F):
     idx, val = gen.coo(dims, 30000, (0.7, 0.3, 0.5, 0.2), 111)
     for mode in range(4):
         _fake_ranks(F, dims, idx, val, mode, 3, True)
+
+
+def test_distributed_build_index_error(F):
+    """A coordinate beyond its extent is reported (INDEX_RANGE) before any exchange; with N ranks the
+    status is agreed across ranks before each collective step (include/fcoo.h)."""
+    dims = (30, 20, 10)
+    idx, val = gen.coo(dims, 500, None, 113)
+    idx = idx.copy()
+    idx[0, 7] = 30  # out of range in the distributed mode
+    coo = F.Coo.from_numpy(dims, idx, val)
+    comm = _one_rank_comm(F)
+    try:
+        with pytest.raises(F.FcooError) as e:
+            F.fcoo_build_distributed(coo, 0, comm)
+        assert e.value.code == F.ERR_INDEX_RANGE
+    finally:
+        comm.destroy()
